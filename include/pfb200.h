@@ -1,0 +1,258 @@
+/*
+ * pfb200.h — C ABI of the B200-native likelihood-evaluation engine.
+ *
+ * This is the drop-in boundary for the hot path of the reference `parfit`
+ * (GooFit re-architecture, /root/reference/proj/include/parfit/).  Every
+ * entry point replaces one reference interface; the citation is given per
+ * function.  Plain C types only: pointers, sizes, fixed-width integers.
+ *
+ * Ownership: the caller owns every input buffer; pf_model_create copies the
+ * event table into HBM (the reference copies it into its EventTable,
+ * engine.hpp:143,151) and the model owns all device state afterwards.
+ *
+ * Errors: functions return 0 on success, nonzero on failure, and fill
+ * `pf_status.message` with the reference's stable "code: detail" text
+ * (errors.hpp:9-16), e.g. "non-finite-metric: first offending event index 7".
+ *
+ * Threading: a model may move between threads but evaluates one call at a
+ * time (engine.hpp:134-136).  pf_eval_metric blocks until the scalar is on
+ * the host, exactly like BoundModel::eval_metric.
+ */
+#ifndef PFB200_H
+#define PFB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PF_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define PF_API __attribute__((visibility("default")))
+#else
+#define PF_API
+#endif
+
+/* Node kinds: pdf.hpp:20-30 (Exponential..Convolution) plus ArgusPdf, which
+ * the reference lacks (BASELINE config 3 needs it). */
+enum pf_kind {
+  PF_EXPONENTIAL = 0,
+  PF_GAUSSIAN = 1,
+  PF_BREIT_WIGNER = 2,
+  PF_POLYNOMIAL = 3,
+  PF_PRODUCT = 4,
+  PF_SUM = 5,
+  PF_COMPOSITE = 6,
+  PF_MAPPED = 7,
+  PF_CONVOLUTION = 8,
+  PF_ARGUS = 9
+};
+
+/* MetricKind, engine.hpp:48 */
+enum pf_metric { PF_NLL = 0, PF_CHISQ = 1 };
+
+/* Role, variable.hpp:13 */
+enum pf_role { PF_OBSERVABLE = 0, PF_PARAMETER = 1 };
+
+/* Variable, variable.hpp:18-27.  Identity is the index in pf_graph.variables:
+ * two nodes naming the same index share one registry slot. */
+typedef struct pf_variable {
+  const char* name;
+  double value;
+  double lower;
+  double upper;
+  double step;
+  int32_t fixed;
+  int32_t role; /* pf_role */
+} pf_variable;
+
+/* One PdfNode (pdf.hpp:61-205) as declared by the user, before finalize.
+ *   children: node indices (ProdPdf/AddPdf order; Composite = {outer, inner};
+ *             Convolution = {model, resolution}; Mapped = targets)
+ *   params:   variable indices in node-local declaration order
+ *   obs:      variable indices (primitives only)
+ *   reals:    MappedPdf boundaries (n_children + 1 strictly increasing values)
+ *   quadrature_points: ConvolutionPdf Q (pdf.hpp:464-466), 0 otherwise. */
+typedef struct pf_node {
+  int32_t kind; /* pf_kind */
+  const char* name;
+  int32_t n_children;
+  const int32_t* children;
+  int32_t n_params;
+  const int32_t* params;
+  int32_t n_obs;
+  const int32_t* obs;
+  int32_t n_reals;
+  const double* reals;
+  int64_t quadrature_points;
+} pf_node;
+
+typedef struct pf_graph {
+  int32_t n_variables;
+  const pf_variable* variables;
+  int32_t n_nodes;
+  const pf_node* nodes;
+  int32_t root;
+} pf_graph;
+
+/* The flat column-major EventTable (dataset.hpp:135-182).
+ * Unbinned: n_obs columns.  Binned: n_obs bin-centre columns, then content,
+ * then volume (to_event_table, dataset.hpp:161-182); total_content is
+ * BinnedDataSet::total_content() (dataset.hpp:356-358). */
+typedef struct pf_data {
+  int32_t binned;
+  int32_t n_obs;
+  const int32_t* obs; /* variable indices in column order */
+  uint64_t n_events;  /* events, or bins */
+  const double* values;
+  double total_content;
+} pf_data;
+
+/* Device placement / sharding.
+ *   device:        CUDA ordinal of the first device.
+ *   n_devices:     >1 shards events over devices device..device+n-1 in this
+ *                  process (contiguous subtrees of the reduction tree).
+ *   shard_index/shard_count: this process evaluates only subtree
+ *                  shard_index of shard_count (power of two) of the global
+ *                  reduction tree; pf_eval_partial returns its partial and
+ *                  pf_combine_partials reproduces the global value.
+ *                  shard_count = 1: whole data set. */
+typedef struct pf_options {
+  int32_t device;
+  int32_t n_devices;
+  int32_t shard_index;
+  int32_t shard_count;
+  int32_t verbose;
+  int32_t reserved[3];
+} pf_options;
+
+typedef struct pf_status {
+  int32_t code; /* 0 ok */
+  char message[512];
+} pf_status;
+
+/* Per-call diagnostics returned alongside the metric. */
+typedef struct pf_eval_info {
+  uint64_t log_floor_delta; /* events floored at 1e-300 in this call */
+  int32_t penalty;          /* 1 when the 1e300 penalty was returned */
+  int32_t norms_recomputed; /* 0 when the parameter fingerprint matched */
+} pf_eval_info;
+
+typedef struct pf_model pf_model;
+
+/* ---- model-core: finalize without a device ------------------------------ */
+
+/* GraphFinalizer::finalize (pdf.hpp:504-613) on the host only: validates the
+ * graph, assigns pre-order ids, fills the registry order and the IndexTable.
+ *   reserved_columns: 2 for binned data sets (engine.hpp:149)
+ *   param_order[n]:  variable index of registry slot i (capacity cap_params)
+ *   table/table_len: concatenated IndexTable rows (index_table.hpp:12-16)
+ *   n_columns:       data + reserved + synthetic columns.
+ * Returns the number of parameters through *n_params. */
+PF_API int pf_graph_finalize(const pf_graph* graph, int32_t n_data_obs, const int32_t* data_obs,
+                      int32_t reserved_columns, int32_t* param_order, int32_t cap_params,
+                      int32_t* n_params, uint32_t* table, int32_t cap_table,
+                      int32_t* table_len, int32_t* n_columns, pf_status* status);
+
+/* Generated per-model CUDA source (the fused evaluator) for inspection and
+ * for the NVRTC compile check that runs without a GPU.  Writes at most cap
+ * bytes (NUL-terminated) and the full length to *len. */
+PF_API int pf_graph_codegen(const pf_graph* graph, const pf_data* data, uint32_t grid_points,
+                     char* out, size_t cap, size_t* len, pf_status* status);
+
+/* Compiles the generated source for sm_100a with NVRTC (no GPU needed) and
+ * returns the cubin size; used by build() and the CPU tests. */
+PF_API int pf_graph_compile_check(const pf_graph* graph, const pf_data* data,
+                           uint32_t grid_points, size_t* cubin_bytes, pf_status* status);
+
+/* ---- parallel-engine: the hot path -------------------------------------- */
+
+/* BoundModel(pdf, data, GridSpec) — engine.hpp:139-154 (setData).
+ * Finalizes the graph, uploads the EventTable to HBM in SoA layout, compiles
+ * the fused evaluator for sm_100a and captures the per-call CUDA graphs. */
+PF_API int pf_model_create(const pf_graph* graph, const pf_data* data, uint32_t grid_points,
+                    const pf_options* options, pf_model** out, pf_status* status);
+
+PF_API void pf_model_destroy(pf_model* model);
+
+/* BoundModel::n_events / registry().n_parameters (engine.hpp:156-162). */
+PF_API uint64_t pf_model_n_events(const pf_model* model);
+PF_API int32_t pf_model_n_params(const pf_model* model);
+/* variable index (into pf_graph.variables) of registry slot i */
+PF_API int32_t pf_model_param_variable(const pf_model* model, int32_t slot);
+PF_API int32_t pf_model_n_nodes(const pf_model* model);
+PF_API int32_t pf_model_binned(const pf_model* model);
+
+/* BoundModel::eval_metric(params, metric, backend) — engine.hpp:165-218. */
+PF_API int pf_eval_metric(pf_model* model, const double* params, size_t n_params, int32_t metric,
+                   double* out, pf_eval_info* info, pf_status* status);
+
+/* K parameter vectors (row-major K x n_params) in one pass over the events:
+ * out[k] equals pf_eval_metric(params + k*n_params) bit for bit.  Serves the
+ * independent probes of numeric_gradient / numeric_hessian (fit.hpp:138-208). */
+PF_API int pf_eval_metric_batch(pf_model* model, const double* params, size_t k, size_t n_params,
+                         int32_t metric, double* out, pf_status* status);
+
+/* Shard partial (double-double hi, lo) of this process's subtree, for
+ * multi-process sharding; *penalty set when the 1e300 penalty applies. */
+PF_API int pf_eval_partial(pf_model* model, const double* params, size_t n_params, int32_t metric,
+                    double* partial_hi_lo, int32_t* penalty, pf_status* status);
+
+/* Fixed-order combine of shard_count partials (hi, lo pairs in shard order)
+ * into the global metric; identical to the single-device value. */
+PF_API double pf_combine_partials(const double* partials_hi_lo, int32_t shard_count);
+
+/* PdfNode::cached_norm / norm_error_estimate (pdf.hpp:88-92) for every node
+ * in pre-order; valid[i] = 0 where the reference would throw
+ * "stale-normalization" (nodes that are never normalised). */
+PF_API int pf_node_norms(pf_model* model, double* norms, double* errs, int32_t* valid, int32_t n_nodes);
+
+/* BoundModel::log_floor_count (engine.hpp:163) and
+ * PolynomialPdf::clamp_count (pdf.hpp:320), cumulative. */
+PF_API uint64_t pf_log_floor_count(const pf_model* model);
+PF_API uint64_t pf_clamp_count(const pf_model* model, int32_t node);
+
+/* ---- fit-manager --------------------------------------------------------- */
+
+/* FitConfig, fit.hpp:23-28 */
+typedef struct pf_fit_config {
+  int32_t minimizer; /* 0 QuasiNewton (BFGS), 1 NelderMead */
+  int32_t batch_probes; /* 1: evaluate independent FD probes in one pass */
+  uint64_t max_iterations;
+  double gradient_tolerance;
+  double simplex_tolerance;
+} pf_fit_config;
+
+/* FitResult, fit.hpp:32-43.  Arrays sized to pf_model_n_params. */
+typedef struct pf_fit_result {
+  int32_t status; /* 0 converged, 1 max-iterations, 2 failed */
+  int32_t uncertainties_available;
+  double metric_value;
+  uint64_t n_metric_calls;
+  double wall_time_s;
+  double grad_max_norm;
+  double* params;        /* external values, registry order */
+  double* uncertainties; /* external; 0 for fixed parameters */
+} pf_fit_result;
+
+/* parfit::fit(BoundModel&, MetricKind, Backend, FitConfig) — fit.hpp:498-581.
+ *   start:  initial external values (registry order), e.g. export_values()
+ *   fixed:  per registry slot, nonzero keeps the value fixed
+ *   lower/upper/step: Variable limits and steps (BoundTransform, fit.hpp:77-129) */
+PF_API int pf_fit(pf_model* model, int32_t metric, const pf_fit_config* config, const double* start,
+           const int32_t* fixed, const double* lower, const double* upper, const double* step,
+           pf_fit_result* result, pf_status* status);
+
+/* Library version / number of CUDA kernels launched so far by this process
+ * (all models), for the bench's gpu_launches accounting. */
+PF_API int32_t pf_abi_version(void);
+PF_API uint64_t pf_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PFB200_H */

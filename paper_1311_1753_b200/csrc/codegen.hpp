@@ -1,0 +1,50 @@
+// codegen.hpp — emits the fused per-model CUDA evaluator (NVRTC source).
+//
+// The reference evaluates a virtual PdfNode::raw tree per event through the
+// IndexTable's double indirection (pdf.hpp:79-80, 140-145).  Here the tree
+// is flattened at model creation into straight-line device code: parameter
+// slots and event columns become compile-time constants, so the only
+// per-event work is the arithmetic itself.
+#pragma once
+
+#include <string>
+#include <vector>
+
+#include "graph.hpp"
+
+namespace pfb {
+
+struct ConvTable {
+  int node;       // ConvolutionPdf node id
+  int slot;       // S offset of the Q model values
+  int q;
+  int after;      // stage after which it can be filled (-1 = pre)
+};
+
+struct Layout {
+  int n_nodes = 0;
+  int np = 0;                 // parameters
+  int ss = 0;                 // per-call state doubles per parameter set
+  int nc = 0;                 // model constant doubles
+  int nc_total_slot = -1;     // C index of N_tot (binned)
+  bool binned = false;
+  int ept = 16;               // events per thread (chunk = 256 * ept)
+  std::vector<int> load_cols; // data columns read per event
+  std::vector<int> poly_index; // node -> clamp counter index (-1 otherwise)
+  int n_poly = 0;
+  std::vector<double> constants;  // C buffer contents (boundaries, conv L/h)
+  std::vector<ConvTable> conv_tables;
+  std::vector<std::vector<int>> level_nodes;  // normalised nodes per level
+  std::string source;         // generated CUDA source (without library headers)
+  std::string structure_key;  // cache key of the compiled module
+};
+
+// binned: chi-squared evaluator (content/volume columns after the obs).
+Layout generate(const Program& pg, bool binned);
+
+// Embedded library headers (pf_device.cuh, pf_kernels.cuh).
+const char* device_header_source();
+const char* kernels_header_source();
+const char* counters_header_source();
+
+}  // namespace pfb

@@ -1,0 +1,271 @@
+// pf_device.cuh — device library shared by every generated evaluator.
+//
+// Compiled at model-creation time by NVRTC for sm_100a together with the
+// per-model generated code (codegen.cpp).  Contents:
+//   * double-double (DD) arithmetic: replaces the x87 `long double`
+//     accumulators of the reference (engine.hpp:57-68, pdf.hpp:163-175);
+//   * fixed-shape warp/block reductions: summation order is a pure function
+//     of the input length, never of scheduling (engine.hpp:72-78);
+//   * error/status records standing in for parfit::Error (errors.hpp);
+//   * scalar math entry points used by the node kernels.
+#pragma once
+
+typedef unsigned long long pf_u64;
+typedef long long pf_i64;
+typedef unsigned int pf_u32;
+
+#define PF_THREADS 256
+#define PF_FINAL_THREADS 1024
+#define PF_LOG_FLOOR 1e-300   // engine.hpp:50 kLogFloor
+#define PF_CHISQ_EPS 1e-9     // engine.hpp:51 kChiSqEps
+#define PF_MAX_BOX 8
+#define PF_MAX_LEVELS 14
+
+// error codes, mirrored by engine.cpp's message table
+#define PF_E_NONPOS_SIGMA 1   // pdf.hpp:256-257
+#define PF_E_NONPOS_WIDTH 2   // pdf.hpp:285
+#define PF_E_OUT_OF_DOMAIN 3  // pdf.hpp:443-444
+#define PF_E_ZERO_INTEGRAL 4  // pdf.hpp:186-187
+#define PF_E_NONPOS_ENDPOINT 5 // ArgusPdf m0 <= 0
+
+struct pf_dd {
+  double hi, lo;
+};
+
+// Per-parameter-set call record (one per k of a batch).  Initialised by the
+// pre kernel of every call; copied back to the host after the call.
+struct pf_krec {
+  pf_u64 floor_count;        // events floored at 1e-300 (engine.hpp:190-193)
+  pf_u64 first_nonfinite;    // min global index of a non-finite term (engine.hpp:210-216)
+  pf_u64 first_event_error;  // min (index << 24 | node << 8 | code) raised in the event pass
+  pf_u32 norm_error;         // min (node << 8 | code) raised while normalising
+  pf_u32 arrive[PF_MAX_LEVELS + 1];  // last-block arrival counters
+  double result_hi, result_lo;
+};
+
+struct pf_task {  // one midpoint sum: node, n points per box dimension
+  int node, n, dims, first_block;
+  int n_blocks, partial_offset, fine, pad;
+  pf_u64 points, per_block;
+  double lo[PF_MAX_BOX];
+  double h[PF_MAX_BOX];
+  double vol;
+};
+
+struct pf_args {
+  const double* data;   // column-major shard: data[col * col_stride + e]
+  pf_u64 col_stride;
+  pf_u64 n_local;       // events (bins) in this shard
+  pf_u64 event_offset;  // global index of local event 0
+  int n_chunks;         // chunks in this shard
+  int K;                // parameter sets in this call
+  int level;            // normalisation level of this launch
+  int n_tasks;
+  const double* P;      // K x PF_NP parameters
+  double* S;            // K x PF_SS per-call state (norms, derived constants)
+  const double* C;      // model constants (ranges, boundaries, ...)
+  const pf_task* tasks; // norm tasks of this level
+  pf_dd* partials;      // K x n_chunks (event pass) / K x n_partials (norms)
+  pf_krec* rec;         // K records
+  pf_u64* clamp;        // cumulative PolynomialPdf clamp counters per node
+  double total_content; // binned: N_tot (engine.hpp:153)
+};
+
+// ----------------------------------------------------------------------------
+// error/counter context carried through one evaluation
+struct pf_ctx {
+  pf_u32 err;  // (node << 8) | code of the first error, 0 when none
+};
+
+__device__ __forceinline__ void pf_fail(pf_ctx& cx, int node, int code) {
+  if (!cx.err) cx.err = ((pf_u32)node << 8) | (pf_u32)code;
+}
+
+// ----------------------------------------------------------------------------
+// double-double arithmetic (Knuth TwoSum / Dekker FastTwoSum).  Only adds are
+// involved, so FMA contraction cannot perturb them.
+__device__ __forceinline__ pf_dd pf_two_sum(double a, double b) {
+  double s = a + b;
+  double bb = s - a;
+  double e = (a - (s - bb)) + (b - bb);
+  pf_dd r;
+  r.hi = s;
+  r.lo = e;
+  return r;
+}
+
+__device__ __forceinline__ pf_dd pf_fast_two_sum(double a, double b) {
+  double s = a + b;
+  pf_dd r;
+  r.hi = s;
+  r.lo = b - (s - a);
+  return r;
+}
+
+__device__ __forceinline__ pf_dd pf_dd_add(pf_dd a, pf_dd b) {
+  pf_dd s = pf_two_sum(a.hi, b.hi);
+  pf_dd t = pf_two_sum(a.lo, b.lo);
+  double lo = s.lo + t.hi;
+  pf_dd u = pf_fast_two_sum(s.hi, lo);
+  lo = u.lo + t.lo;
+  return pf_fast_two_sum(u.hi, lo);
+}
+
+__device__ __forceinline__ pf_dd pf_dd_add_d(pf_dd a, double b) {
+  pf_dd s = pf_two_sum(a.hi, b);
+  double lo = s.lo + a.lo;
+  return pf_fast_two_sum(s.hi, lo);
+}
+
+__device__ __forceinline__ pf_dd pf_dd_zero() {
+  pf_dd z;
+  z.hi = 0.0;
+  z.lo = 0.0;
+  return z;
+}
+
+__device__ __forceinline__ double pf_dd_to_double(pf_dd a) { return a.hi + a.lo; }
+
+__device__ __forceinline__ pf_dd pf_shfl_down_dd(pf_dd v, int d) {
+  pf_dd r;
+  r.hi = __shfl_down_sync(0xffffffffu, v.hi, d);
+  r.lo = __shfl_down_sync(0xffffffffu, v.lo, d);
+  return r;
+}
+
+// Fixed-shape reduction of n DD values by ONE warp (all 32 lanes must call):
+// lane l sums the contiguous run [l*per, min((l+1)*per, n)) sequentially,
+// then a shuffle tree (16, 8, 4, 2, 1).  Result valid in lane 0.
+__device__ __forceinline__ pf_dd pf_warp_reduce_runs(const pf_dd* v, int n) {
+  const int lane = threadIdx.x & 31;
+  const int per = (n + 31) >> 5;
+  pf_dd acc = pf_dd_zero();
+  const int lo = lane * per;
+  const int hi = min(lo + per, n);
+  for (int i = lo; i < hi; ++i) acc = pf_dd_add(acc, v[i]);
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    pf_dd o = pf_shfl_down_dd(acc, d);
+    acc = pf_dd_add(acc, o);
+  }
+  return acc;
+}
+
+// ----------------------------------------------------------------------------
+// Reference reduction shape over chunk partials (engine.hpp:63-68): a
+// recursive pairwise tree that splits [lo, hi) at lo + (hi - lo) / 2.  An
+// empty range is 0 and x + 0 == x exactly, so padding the top of the tree
+// with empty subtrees leaves every value unchanged.
+__device__ pf_dd pf_pairwise_seq(const pf_dd* v, pf_u64 lo, pf_u64 hi) {
+  // iterative post-order walk with an explicit stack (depth <= 64)
+  if (hi <= lo) return pf_dd_zero();
+  pf_u64 slo[64], shi[64];
+  pf_dd sval[64];
+  int sstate[64];
+  int sp = 0;
+  slo[0] = lo;
+  shi[0] = hi;
+  sstate[0] = 0;
+  pf_dd ret = pf_dd_zero();
+  while (sp >= 0) {
+    pf_u64 l = slo[sp], h = shi[sp];
+    if (h - l == 1) {
+      ret = v[l];
+      --sp;
+      continue;
+    }
+    if (h == l) {
+      ret = pf_dd_zero();
+      --sp;
+      continue;
+    }
+    pf_u64 mid = l + (h - l) / 2;
+    if (sstate[sp] == 0) {
+      sstate[sp] = 1;
+      ++sp;
+      slo[sp] = l;
+      shi[sp] = mid;
+      sstate[sp] = 0;
+    } else if (sstate[sp] == 1) {
+      sval[sp] = ret;  // left value
+      sstate[sp] = 2;
+      ++sp;
+      slo[sp] = mid;
+      shi[sp] = h;
+      sstate[sp] = 0;
+    } else {
+      ret = pf_dd_add(sval[sp], ret);
+      --sp;
+    }
+  }
+  return ret;
+}
+
+// Block-parallel evaluation of the same tree with PF_FINAL_THREADS threads:
+// thread t owns the subtree at depth 10 selected by the bits of t, the
+// top 10 levels are a complete binary tree combined in shared memory.
+__device__ pf_dd pf_pairwise_block(const pf_dd* v, pf_u64 n, pf_dd* sm /* 1024 */) {
+  const int t = threadIdx.x;
+  pf_u64 lo = 0, hi = n;
+#pragma unroll 1
+  for (int level = 0; level < 10; ++level) {
+    pf_u64 mid = lo + (hi - lo) / 2;
+    if ((t >> (9 - level)) & 1)
+      lo = mid;
+    else
+      hi = mid;
+  }
+  sm[t] = pf_pairwise_seq(v, lo, hi);
+  __syncthreads();
+  for (int width = 512; width >= 1; width >>= 1) {
+    if (t < width) sm[t] = pf_dd_add(sm[2 * t], sm[2 * t + 1]);
+    __syncthreads();
+  }
+  return sm[0];
+}
+
+// ----------------------------------------------------------------------------
+// scalar math used by the node kernels (libdevice, <= 1 ulp)
+__device__ __forceinline__ double pf_exp(double x) { return exp(x); }
+__device__ __forceinline__ double pf_log(double x) { return log(x); }
+__device__ __forceinline__ double pf_pow(double x, double y) { return pow(x, y); }
+
+// ln 2 split so that E * PF_LN2_HI is exact for |E| < 2^21 (fdlibm constants)
+#define PF_LN2_HI 6.93147180369123816490e-01
+#define PF_LN2_LO 1.90821492927058770002e-10
+
+// Running product with an exponent register: prod(v) = m * 2^E, m in [1, 2).
+// Replaces one log per event by one log per thread and chunk; the per-event
+// rounding added is one ulp of m (below the reference's own per-term log
+// rounding), and nothing can over- or underflow.
+struct pf_prod {
+  double m;
+  int e;
+};
+
+__device__ __forceinline__ void pf_prod_init(pf_prod& p) {
+  p.m = 1.0;
+  p.e = 0;
+}
+
+__device__ __forceinline__ void pf_prod_mul(pf_prod& p, double v) {
+  // v is finite and >= 1e-300 here; keep m * v inside the normal range
+  if (v > 0x1p+900) {
+    v *= 0x1p-600;
+    p.e += 600;
+  }
+  double m = p.m * v;
+  int hi = __double2hiint(m);
+  int ex = (hi >> 20) - 1023;
+  p.e += ex;
+  p.m = __hiloint2double(hi - (ex << 20), __double2loint(m));
+}
+
+// -log(prod) as a DD value
+__device__ __forceinline__ pf_dd pf_prod_neglog(const pf_prod& p) {
+  double lm = pf_log(p.m);
+  double e = (double)p.e;
+  pf_dd s = pf_two_sum(-(e * PF_LN2_HI), -lm);
+  s.lo += -(e * PF_LN2_LO);
+  return pf_fast_two_sum(s.hi, s.lo);
+}

@@ -1,0 +1,541 @@
+// engine.cpp — the B200 BoundModel.
+//
+// setData (engine.hpp:139-154 of the reference): finalize the graph, upload
+// the EventTable once into HBM (column-major, one shard per device), compile
+// the fused evaluator with NVRTC for sm_100a and capture one CUDA graph per
+// batch width:  H2D params -> pre -> norm levels -> event -> final -> D2H.
+// eval_metric (engine.hpp:165-218): host-side contract checks and penalty
+// rules, one graph launch per shard, one synchronisation, one small D2H.
+#include "engine.hpp"
+
+#include <nvrtc.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <sstream>
+#include <unordered_map>
+
+namespace pfb {
+
+namespace {
+
+std::atomic<uint64_t> g_launches{0};
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw Error("cuda-error", std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void ckr(nvrtcResult r, const char* what) {
+  if (r != NVRTC_SUCCESS) throw Error("nvrtc-error", std::string(what) + ": " + nvrtcGetErrorString(r));
+}
+
+struct ModuleCache {
+  std::mutex mu;
+  std::unordered_map<std::string, std::vector<char>> cubins;          // by source
+  std::map<std::pair<std::string, int>, Module*> modules;             // by (source, device)
+};
+
+ModuleCache& cache() {
+  static ModuleCache* c = new ModuleCache();  // intentionally leaked (process lifetime)
+  return *c;
+}
+
+const Module* load_module(const Layout& L, int device) {
+  ModuleCache& c = cache();
+  std::lock_guard<std::mutex> lock(c.mu);
+  auto key = std::make_pair(L.structure_key, device);
+  auto it = c.modules.find(key);
+  if (it != c.modules.end()) return it->second;
+  auto cit = c.cubins.find(L.structure_key);
+  if (cit == c.cubins.end()) {
+    std::string log;
+    cit = c.cubins.emplace(L.structure_key, compile_cubin(L, &log)).first;
+  }
+  Module* m = new Module();
+  ck(cudaSetDevice(device), "cudaSetDevice");
+  ck(cudaLibraryLoadData(&m->lib, cit->second.data(), nullptr, nullptr, 0, nullptr, nullptr, 0),
+     "cudaLibraryLoadData");
+  ck(cudaLibraryGetKernel(&m->pre, m->lib, "pf_pre_kernel"), "get pf_pre_kernel");
+  ck(cudaLibraryGetKernel(&m->norm, m->lib, "pf_norm_kernel"), "get pf_norm_kernel");
+  ck(cudaLibraryGetKernel(&m->event, m->lib, "pf_event_kernel"), "get pf_event_kernel");
+  ck(cudaLibraryGetKernel(&m->final, m->lib, "pf_final_kernel"), "get pf_final_kernel");
+  ck(cudaKernelSetAttributeForDevice(m->event, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kMaxBatch * 256 * 16, device),
+     "event kernel smem attribute");
+  c.modules.emplace(key, m);
+  return m;
+}
+
+void launch(cudaKernel_t k, dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args& a) {
+  void* args[] = {&a};
+  ck(cudaLaunchKernel(reinterpret_cast<const void*>(k), grid, block, args, smem, s),
+     "cudaLaunchKernel");
+}
+
+// Split [lo, hi) the way the reference's pairwise tree does (engine.hpp:63-68)
+// and descend `depth` levels following the bits of `index` (MSB first).
+void subtree_range(uint64_t n, int shard_count, int index, uint64_t* lo, uint64_t* hi) {
+  uint64_t a = 0, b = n;
+  int depth = 0;
+  while ((1 << depth) < shard_count) ++depth;
+  for (int level = 0; level < depth; ++level) {
+    uint64_t mid = a + (b - a) / 2;
+    if ((index >> (depth - 1 - level)) & 1)
+      a = mid;
+    else
+      b = mid;
+  }
+  *lo = a;
+  *hi = b;
+}
+
+}  // namespace
+
+uint64_t kernel_launch_count() { return g_launches.load(); }
+
+std::vector<char> compile_cubin(const Layout& L, std::string* log) {
+  nvrtcProgram prog;
+  const char* headers[] = {device_header_source(), kernels_header_source(), counters_header_source()};
+  const char* names[] = {"pf_device.cuh", "pf_kernels.cuh", "pf_counters.cuh"};
+  ckr(nvrtcCreateProgram(&prog, L.source.c_str(), "pf_model.cu", 3, headers, names),
+      "nvrtcCreateProgram");
+  const char* opts[] = {"--gpu-architecture=sm_100a", "-lineinfo", "--std=c++17",
+                        "--device-as-default-execution-space"};
+  nvrtcResult r = nvrtcCompileProgram(prog, 4, opts);
+  size_t log_size = 0;
+  nvrtcGetProgramLogSize(prog, &log_size);
+  std::string lg(log_size, '\0');
+  if (log_size) nvrtcGetProgramLog(prog, &lg[0]);
+  if (log) *log = lg;
+  if (r != NVRTC_SUCCESS) {
+    nvrtcDestroyProgram(&prog);
+    throw Error("nvrtc-error", "compiling the evaluator failed:\n" + lg);
+  }
+  size_t n = 0;
+  ckr(nvrtcGetCUBINSize(prog, &n), "nvrtcGetCUBINSize");
+  std::vector<char> cubin(n);
+  ckr(nvrtcGetCUBIN(prog, cubin.data()), "nvrtcGetCUBIN");
+  nvrtcDestroyProgram(&prog);
+  return cubin;
+}
+
+// ---------------------------------------------------------------------------
+
+Model::Model(const pf_graph& g, const pf_data& d, uint32_t grid_points, const pf_options& opt) {
+  if (grid_points < 2) throw Error("bad-grid", "GridSpec needs >= 2 points");  // pdf.hpp:35-37
+  if (!d.obs && d.n_obs > 0) throw Error("bad-data", "null observable list");
+  binned_ = d.binned != 0;
+  n_events_ = d.n_events;
+  total_content_ = d.total_content;
+  pg_ = finalize(g, d.n_obs, d.obs, binned_ ? 2 : 0);
+  L_ = generate(pg_, binned_);
+  if (binned_) L_.constants[L_.nc_total_slot] = total_content_;
+  clamp_total_.assign(pg_.nodes.size(), 0);
+  norms_.assign(pg_.nodes.size(), 1.0);  // PdfNode::norm_ default (pdf.hpp:199)
+  errs_.assign(pg_.nodes.size(), 0.0);
+  norm_valid_.assign(pg_.nodes.size(), 0);
+
+  const int n_devices = std::max(1, opt.n_devices);
+  shard_count_ = std::max(1, opt.shard_count);
+  shard_index_ = opt.shard_index;
+  if (n_devices > 1 && shard_count_ > 1)
+    throw Error("bad-backend", "n_devices and shard_count cannot both exceed 1");
+  auto pow2 = [](int v) { return v > 0 && (v & (v - 1)) == 0; };
+  if (!pow2(n_devices) || !pow2(shard_count_))
+    throw Error("bad-backend", "device and shard counts must be powers of two");
+  if (shard_index_ < 0 || shard_index_ >= shard_count_)
+    throw Error("bad-backend", "shard_index out of range");
+
+  chunk_ = 256ull * static_cast<uint64_t>(L_.ept);
+  n_chunks_total_ = (n_events_ + chunk_ - 1) / chunk_;
+  const int n_cols_data = d.n_obs + (binned_ ? 2 : 0);
+  build_tasks(grid_points);
+
+  ck(cudaSetDevice(opt.device), "cudaSetDevice");
+  ck(cudaMallocHost(reinterpret_cast<void**>(&h_params_),
+                    sizeof(double) * kMaxBatch * std::max(L_.np, 1)),
+     "cudaMallocHost params");
+
+  const int G = n_devices;
+  const int groups = std::max(G, shard_count_);
+  shards_.resize(G);
+  for (int s = 0; s < G; ++s) {
+    Shard& sh = shards_[s];
+    sh.device = opt.device + s;
+    int part = shard_count_ > 1 ? shard_index_ : s;
+    subtree_range(n_chunks_total_, groups, part, &sh.chunk_lo, &sh.chunk_hi);
+    sh.n_chunks = static_cast<int>(sh.chunk_hi - sh.chunk_lo);
+    sh.event_offset = std::min(sh.chunk_lo * chunk_, n_events_);
+    uint64_t end = std::min(sh.chunk_hi * chunk_, n_events_);
+    sh.n_local = end - sh.event_offset;
+    sh.col_stride = (sh.n_local + 31) & ~31ull;
+    ck(cudaSetDevice(sh.device), "cudaSetDevice");
+    ck(cudaStreamCreateWithFlags(&sh.stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    sh.mod = load_module(L_, sh.device);
+    const size_t np = std::max(L_.np, 1);
+    ck(cudaMalloc(&sh.d_P, sizeof(double) * kMaxBatch * np), "cudaMalloc P");
+    ck(cudaMalloc(&sh.d_S, sizeof(double) * kMaxBatch * std::max(L_.ss, 1)), "cudaMalloc S");
+    ck(cudaMemset(sh.d_S, 0, sizeof(double) * kMaxBatch * std::max(L_.ss, 1)), "memset S");
+    ck(cudaMalloc(&sh.d_C, sizeof(double) * std::max<size_t>(L_.constants.size(), 1)), "cudaMalloc C");
+    if (!L_.constants.empty())
+      ck(cudaMemcpy(sh.d_C, L_.constants.data(), sizeof(double) * L_.constants.size(),
+                    cudaMemcpyHostToDevice),
+         "upload C");
+    ck(cudaMalloc(&sh.d_tasks, sizeof(Task) * std::max<size_t>(tasks_.size(), 1)), "cudaMalloc tasks");
+    if (!tasks_.empty())
+      ck(cudaMemcpy(sh.d_tasks, tasks_.data(), sizeof(Task) * tasks_.size(), cudaMemcpyHostToDevice),
+         "upload tasks");
+    size_t part_elems = static_cast<size_t>(kMaxBatch) *
+                        std::max<size_t>(std::max<size_t>(sh.n_chunks, max_norm_blocks_), 1);
+    ck(cudaMalloc(&sh.d_partials, 16 * part_elems), "cudaMalloc partials");
+    ck(cudaMalloc(&sh.d_rec, sizeof(KRec) * kMaxBatch), "cudaMalloc rec");
+    ck(cudaMalloc(&sh.d_clamp, sizeof(uint64_t) * 2 * std::max(L_.n_poly, 1)), "cudaMalloc clamp");
+    ck(cudaMemset(sh.d_clamp, 0, sizeof(uint64_t) * 2 * std::max(L_.n_poly, 1)), "memset clamp");
+    ck(cudaMallocHost(reinterpret_cast<void**>(&sh.h_rec), sizeof(KRec) * kMaxBatch), "pinned rec");
+    ck(cudaMallocHost(reinterpret_cast<void**>(&sh.h_norms),
+                      sizeof(double) * kMaxBatch * 3 * pg_.nodes.size()),
+       "pinned norms");
+    ck(cudaMallocHost(reinterpret_cast<void**>(&sh.h_clamp), sizeof(uint64_t) * std::max(L_.n_poly, 1)),
+       "pinned clamp");
+    std::memset(sh.h_clamp, 0, sizeof(uint64_t) * std::max(L_.n_poly, 1));
+    // the EventTable shard, column-major with a padded stride (double2 loads)
+    if (sh.n_local > 0) {
+      ck(cudaMalloc(&sh.d_data, sizeof(double) * sh.col_stride * n_cols_data), "cudaMalloc events");
+      ck(cudaMemcpy2D(sh.d_data, sizeof(double) * sh.col_stride, d.values + sh.event_offset,
+                      sizeof(double) * n_events_, sizeof(double) * sh.n_local, n_cols_data,
+                      cudaMemcpyHostToDevice),
+         "upload events");
+    }
+  }
+}
+
+Model::~Model() {
+  for (Shard& sh : shards_) {
+    cudaSetDevice(sh.device);
+    for (auto& kv : sh.graphs) cudaGraphExecDestroy(kv.second);
+    if (sh.stream) cudaStreamDestroy(sh.stream);
+    cudaFree(sh.d_data);
+    cudaFree(sh.d_P);
+    cudaFree(sh.d_S);
+    cudaFree(sh.d_C);
+    cudaFree(sh.d_tasks);
+    cudaFree(sh.d_partials);
+    cudaFree(sh.d_rec);
+    cudaFree(sh.d_clamp);
+    cudaFreeHost(sh.h_rec);
+    cudaFreeHost(sh.h_norms);
+    cudaFreeHost(sh.h_clamp);
+  }
+  cudaFreeHost(h_params_);
+}
+
+// Norm tasks: for every normalised node, midpoint sums at n and 2n points per
+// box dimension (pdf.hpp:148-188).  Box spacing and cell volume are computed
+// exactly as midpoint_sum does so the grid coordinates agree bit for bit.
+void Model::build_tasks(uint32_t grid_points) {
+  tasks_.clear();
+  level_first_task_.assign(L_.level_nodes.size(), 0);
+  level_n_tasks_.assign(L_.level_nodes.size(), 0);
+  level_blocks_.assign(L_.level_nodes.size(), 0);
+  max_norm_blocks_ = 0;
+  for (size_t lvl = 0; lvl < L_.level_nodes.size(); ++lvl) {
+    level_first_task_[lvl] = static_cast<int>(tasks_.size());
+    int blocks = 0;
+    for (int node : L_.level_nodes[lvl]) {
+      const Node& nd = pg_.nodes[node];
+      const int dims = static_cast<int>(nd.box.size());
+      if (dims > 8) throw Error("bad-graph", nd.name + ": more than 8 box dimensions");
+      const double cost = subtree_cost(pg_, node);
+      for (int fine = 0; fine < 2; ++fine) {
+        Task t;
+        std::memset(&t, 0, sizeof t);
+        const uint64_t n = static_cast<uint64_t>(grid_points) * (fine ? 2 : 1);
+        t.node = node;
+        t.n = static_cast<int>(n);
+        t.dims = dims;
+        t.fine = fine;
+        uint64_t total = 1;
+        for (int dd = 0; dd < dims; ++dd) {
+          const Var& v = pg_.vars[nd.box[dd].var];
+          t.lo[dd] = v.lower;
+          t.h[dd] = (v.upper - v.lower) / static_cast<double>(n);
+          total *= n;
+        }
+        double vol = 1.0;
+        for (int dd = 0; dd < dims; ++dd) vol *= t.h[dd];
+        t.vol = vol;
+        t.points = total;
+        // about 4096 raw evaluations per block, at most 4096 blocks per task
+        uint64_t per = static_cast<uint64_t>(std::max(1.0, std::floor(4096.0 / cost)));
+        uint64_t nb = (total + per - 1) / per;
+        if (nb > 4096) {
+          nb = 4096;
+          per = (total + nb - 1) / nb;
+          nb = (total + per - 1) / per;
+        }
+        t.per_block = per;
+        t.n_blocks = static_cast<int>(nb);
+        t.first_block = blocks;
+        t.partial_offset = blocks;
+        blocks += t.n_blocks;
+        tasks_.push_back(t);
+      }
+    }
+    level_n_tasks_[lvl] = static_cast<int>(tasks_.size()) - level_first_task_[lvl];
+    level_blocks_[lvl] = blocks;
+    max_norm_blocks_ = std::max(max_norm_blocks_, blocks);
+  }
+}
+
+cudaGraphExec_t Model::graph_for(Shard& sh, int K) {
+  auto it = sh.graphs.find(K);
+  if (it != sh.graphs.end()) return it->second;
+  ck(cudaSetDevice(sh.device), "cudaSetDevice");
+  const size_t np = std::max(L_.np, 1);
+  Args a;
+  std::memset(&a, 0, sizeof a);
+  a.data = sh.d_data;
+  a.col_stride = sh.col_stride;
+  a.n_local = sh.n_local;
+  a.event_offset = sh.event_offset;
+  a.n_chunks = sh.n_chunks;
+  a.K = K;
+  a.P = sh.d_P;
+  a.S = sh.d_S;
+  a.C = sh.d_C;
+  a.partials = sh.d_partials;
+  a.rec = sh.d_rec;
+  // norm-stage clamps are counted once (shard 0); the others discard them
+  uint64_t* norm_clamp = (&sh == &shards_[0] && shard_index_ == 0) ? sh.d_clamp
+                                                                     : sh.d_clamp + std::max(L_.n_poly, 1);
+  a.total_content = total_content_;
+  int kernels = 0;
+  cudaGraph_t graph;
+  ck(cudaStreamBeginCapture(sh.stream, cudaStreamCaptureModeThreadLocal), "begin capture");
+  ck(cudaMemcpyAsync(sh.d_P, h_params_, sizeof(double) * K * np, cudaMemcpyHostToDevice, sh.stream),
+     "capture H2D params");
+  a.clamp = norm_clamp;
+  launch(sh.mod->pre, dim3(K), dim3(256), 0, sh.stream, a);
+  ++kernels;
+  for (size_t lvl = 0; lvl < L_.level_nodes.size(); ++lvl) {
+    Args b = a;
+    b.level = static_cast<int>(lvl);
+    b.n_tasks = level_n_tasks_[lvl];
+    b.tasks = sh.d_tasks + level_first_task_[lvl];
+    launch(sh.mod->norm, dim3(level_blocks_[lvl], K), dim3(256), 0, sh.stream, b);
+    ++kernels;
+  }
+  if (sh.n_local > 0) {
+    Args e = a;
+    e.clamp = sh.d_clamp;
+    const int grid = std::max(1, std::min(sh.n_chunks, 148 * 16));
+    launch(sh.mod->event, dim3(grid), dim3(256), static_cast<size_t>(K) * 256 * 16, sh.stream, e);
+    launch(sh.mod->final, dim3(K), dim3(1024), 0, sh.stream, e);
+    kernels += 2;
+  }
+  ck(cudaMemcpyAsync(sh.h_rec, sh.d_rec, sizeof(KRec) * K, cudaMemcpyDeviceToHost, sh.stream),
+     "capture D2H rec");
+  const size_t nn = pg_.nodes.size();
+  ck(cudaMemcpy2DAsync(sh.h_norms, sizeof(double) * 3 * nn, sh.d_S, sizeof(double) * L_.ss,
+                       sizeof(double) * 3 * nn, K, cudaMemcpyDeviceToHost, sh.stream),
+     "capture D2H norms");
+  if (L_.n_poly > 0)
+    ck(cudaMemcpyAsync(sh.h_clamp, sh.d_clamp, sizeof(uint64_t) * L_.n_poly, cudaMemcpyDeviceToHost,
+                       sh.stream),
+       "capture D2H clamp");
+  ck(cudaStreamEndCapture(sh.stream, &graph), "end capture");
+  cudaGraphExec_t exec;
+  ck(cudaGraphInstantiate(&exec, graph, 0), "cudaGraphInstantiate");
+  cudaGraphDestroy(graph);
+  sh.kernels_per_graph = kernels;
+  sh.graphs.emplace(K, exec);
+  return exec;
+}
+
+void Model::check_call(size_t n, int metric) const {
+  if (n != pg_.param_vars.size())
+    throw Error("size-mismatch", "eval_metric: parameter vector length");
+  if (binned_ && metric == PF_NLL) throw Error("metric-mismatch", "NLL needs an unbinned data set");
+  if (!binned_ && metric == PF_CHISQ)
+    throw Error("metric-mismatch", "chi-squared needs a binned data set");
+  if (metric != PF_NLL && metric != PF_CHISQ) throw Error("bad-metric", "unknown metric kind");
+}
+
+// AddPdf::params_valid (pdf.hpp:381-390) over the whole tree (pdf.hpp:96-100)
+bool Model::params_valid(const double* p) const {
+  for (const Node& n : pg_.nodes) {
+    if (n.kind != PF_SUM) continue;
+    double fsum = 0.0;
+    for (int slot : n.params) {
+      double f = p[slot];
+      if (f < 0.0 || f > 1.0) return false;
+      fsum += f;
+    }
+    if (fsum > 1.0) return false;
+  }
+  return true;
+}
+
+std::string Model::error_message(uint32_t code_node) const {
+  const int code = code_node & 0xff;
+  const int node = static_cast<int>(code_node >> 8);
+  const std::string name = node < static_cast<int>(pg_.nodes.size()) ? pg_.nodes[node].name : "?";
+  switch (code) {
+    case 1: return "nonpositive-sigma: " + name;
+    case 2: return "nonpositive-width: " + name;
+    case 3: return "out-of-domain: " + name + ": x outside mapped range";
+    case 4: return "zero-integral: degenerate PDF '" + name + "'";
+    case 5: return "nonpositive-endpoint: " + name;
+  }
+  return "device-error: code " + std::to_string(code);
+}
+
+void Model::run(const double* params, int K, std::vector<Raw>& out, bool partial_only) {
+  const size_t np = std::max(L_.np, 1);
+  if (L_.np > 0) std::memcpy(h_params_, params, sizeof(double) * K * L_.np);
+  for (Shard& sh : shards_) {
+    cudaGraphExec_t g = graph_for(sh, K);
+    ck(cudaSetDevice(sh.device), "cudaSetDevice");
+    ck(cudaGraphLaunch(g, sh.stream), "cudaGraphLaunch");
+    g_launches += sh.kernels_per_graph;
+  }
+  for (Shard& sh : shards_) ck(cudaStreamSynchronize(sh.stream), "cudaStreamSynchronize");
+  (void)np;
+  out.assign(K, Raw());
+  const size_t nn = pg_.nodes.size();
+  // errors first, in parameter-set order (the sequential reference stops at
+  // the first throwing call)
+  for (int k = 0; k < K; ++k) {
+    uint32_t norm_err = ~0u;
+    uint64_t ev_err = ~0ull, nonfinite = ~0ull;
+    for (Shard& sh : shards_) {
+      norm_err = std::min(norm_err, sh.h_rec[k].norm_error);
+      ev_err = std::min(ev_err, sh.h_rec[k].first_event_error);
+      nonfinite = std::min(nonfinite, sh.h_rec[k].first_nonfinite);
+    }
+    if (norm_err != ~0u) {  // refresh_normalizations threw (engine.hpp:174-178)
+      out[k].penalty = true;
+      continue;
+    }
+    // norms are replicated on every shard; keep the last successful set
+    const double* hn = shards_[0].h_norms + static_cast<size_t>(k) * 3 * nn;
+    for (size_t i = 0; i < nn; ++i) {
+      if (!pg_.nodes[i].normalised) continue;
+      norms_[i] = hn[3 * i];
+      errs_[i] = hn[3 * i + 1];
+      norm_valid_[i] = 1;
+    }
+    if (ev_err != ~0ull) throw Error("event-error", error_message(static_cast<uint32_t>(ev_err & 0xffffff)));
+    for (Shard& sh : shards_) floor_total_ += sh.h_rec[k].floor_count;
+    // shard partials combined by the top levels of the pairwise tree
+    std::vector<double> parts;
+    for (Shard& sh : shards_) {
+      parts.push_back(sh.n_local > 0 ? sh.h_rec[k].result_hi : 0.0);
+      parts.push_back(sh.n_local > 0 ? sh.h_rec[k].result_lo : 0.0);
+    }
+    if (partial_only || shards_.size() == 1) {
+      out[k].hi = parts[0];
+      out[k].lo = parts[1];
+    } else {
+      double r = pf_combine_partials(parts.data(), static_cast<int32_t>(shards_.size()));
+      out[k].hi = r;
+      out[k].lo = 0.0;
+    }
+    if (!partial_only) {
+      double r = out[k].hi + out[k].lo;
+      if (!std::isfinite(r)) {
+        if (nonfinite != ~0ull)
+          throw Error("non-finite-metric", "first offending event index " + std::to_string(nonfinite));
+        throw Error("non-finite-metric", "non-finite reduction");
+      }
+    }
+  }
+  if (L_.n_poly > 0) {
+    std::fill(clamp_total_.begin(), clamp_total_.end(), 0);
+    for (Shard& sh : shards_)
+      for (size_t i = 0; i < pg_.nodes.size(); ++i)
+        if (L_.poly_index[i] >= 0) clamp_total_[i] += sh.h_clamp[L_.poly_index[i]];
+  }
+}
+
+// BoundModel::eval_metric (engine.hpp:165-218)
+double Model::eval(const double* params, size_t n, int metric, pf_eval_info* info) {
+  check_call(n, metric);
+  if (info) std::memset(info, 0, sizeof *info);
+  if (!params_valid(params)) {
+    if (info) info->penalty = 1;
+    return kPenaltyValue;
+  }
+  const uint64_t floors0 = floor_total_;
+  std::vector<Raw> out;
+  run(params, 1, out, false);
+  if (info) {
+    info->norms_recomputed = 1;
+    info->log_floor_delta = floor_total_ - floors0;
+  }
+  if (out[0].penalty) {
+    if (info) info->penalty = 1;
+    return kPenaltyValue;
+  }
+  return out[0].hi + out[0].lo;
+}
+
+void Model::eval_batch(const double* params, size_t K, size_t n, int metric, double* result) {
+  check_call(n, metric);
+  // invalid parameter sets are answered on the host; the rest go to the GPU
+  std::vector<size_t> live;
+  for (size_t k = 0; k < K; ++k) {
+    if (params_valid(params + k * n))
+      live.push_back(k);
+    else
+      result[k] = kPenaltyValue;
+  }
+  std::vector<double> packed;
+  std::vector<Raw> out;
+  for (size_t first = 0; first < live.size(); first += kMaxBatch) {
+    const size_t cnt = std::min<size_t>(kMaxBatch, live.size() - first);
+    packed.resize(cnt * std::max<size_t>(n, 1));
+    for (size_t j = 0; j < cnt; ++j)
+      std::memcpy(packed.data() + j * n, params + live[first + j] * n, sizeof(double) * n);
+    run(packed.data(), static_cast<int>(cnt), out, false);
+    for (size_t j = 0; j < cnt; ++j)
+      result[live[first + j]] = out[j].penalty ? kPenaltyValue : out[j].hi + out[j].lo;
+  }
+}
+
+void Model::eval_partial(const double* params, size_t n, int metric, double* hi_lo, int* penalty) {
+  check_call(n, metric);
+  *penalty = 0;
+  hi_lo[0] = hi_lo[1] = 0.0;
+  if (!params_valid(params)) {
+    *penalty = 1;
+    return;
+  }
+  std::vector<Raw> out;
+  run(params, 1, out, true);
+  if (out[0].penalty) {
+    *penalty = 1;
+    return;
+  }
+  hi_lo[0] = out[0].hi;
+  hi_lo[1] = out[0].lo;
+}
+
+uint64_t Model::clamp_count(int node) const {
+  if (node < 0 || node >= static_cast<int>(clamp_total_.size())) return 0;
+  return clamp_total_[node];
+}
+
+void Model::norms(double* norms, double* errs, int32_t* valid, int n) const {
+  for (int i = 0; i < n && i < static_cast<int>(norms_.size()); ++i) {
+    if (norms) norms[i] = norms_[i];
+    if (errs) errs[i] = errs_[i];
+    if (valid) valid[i] = norm_valid_[i];
+  }
+}
+
+}  // namespace pfb

@@ -1,0 +1,145 @@
+// engine.hpp — BoundModel on B200: HBM event store, compiled evaluator and
+// per-call CUDA graphs.  Restates engine.hpp:137-236 of the reference.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "codegen.hpp"
+#include "graph.hpp"
+
+namespace pfb {
+
+constexpr double kPenaltyValue = 1e300;  // engine.hpp:52
+constexpr int kMaxBatch = 32;            // parameter sets per launch
+
+// host mirrors of the device structs (pf_device.cuh); layouts must match
+struct KRec {
+  uint64_t floor_count;
+  uint64_t first_nonfinite;
+  uint64_t first_event_error;
+  uint32_t norm_error;
+  uint32_t arrive[15];
+  double result_hi, result_lo;
+};
+static_assert(sizeof(KRec) == 104, "pf_krec layout");
+
+struct Task {
+  int node, n, dims, first_block;
+  int n_blocks, partial_offset, fine, pad;
+  uint64_t points, per_block;
+  double lo[8];
+  double h[8];
+  double vol;
+};
+static_assert(sizeof(Task) == 184, "pf_task layout");
+
+struct Args {
+  const double* data;
+  uint64_t col_stride;
+  uint64_t n_local;
+  uint64_t event_offset;
+  int n_chunks;
+  int K;
+  int level;
+  int n_tasks;
+  const double* P;
+  double* S;
+  const double* C;
+  const Task* tasks;
+  void* partials;
+  KRec* rec;
+  uint64_t* clamp;
+  double total_content;
+};
+
+struct Module {
+  cudaLibrary_t lib = nullptr;
+  cudaKernel_t pre = nullptr, norm = nullptr, event = nullptr, final = nullptr;
+};
+
+// NVRTC compile of (library headers + generated source) for sm_100a.
+std::vector<char> compile_cubin(const Layout& L, std::string* log);
+
+struct Shard {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  uint64_t chunk_lo = 0, chunk_hi = 0;  // global chunk range
+  uint64_t n_local = 0, event_offset = 0, col_stride = 0;
+  int n_chunks = 0;
+  const Module* mod = nullptr;
+  double* d_data = nullptr;
+  double* d_P = nullptr;
+  double* d_S = nullptr;
+  double* d_C = nullptr;
+  Task* d_tasks = nullptr;  // all levels, concatenated
+  void* d_partials = nullptr;
+  KRec* d_rec = nullptr;
+  uint64_t* d_clamp = nullptr;
+  KRec* h_rec = nullptr;       // pinned
+  double* h_norms = nullptr;   // pinned, K x 3 n_nodes
+  uint64_t* h_clamp = nullptr; // pinned
+  std::map<int, cudaGraphExec_t> graphs;
+  int kernels_per_graph = 0;
+};
+
+class Model {
+ public:
+  Model(const pf_graph& g, const pf_data& d, uint32_t grid_points, const pf_options& opt);
+  ~Model();
+  Model(const Model&) = delete;
+  Model& operator=(const Model&) = delete;
+
+  // BoundModel::eval_metric (engine.hpp:165-218)
+  double eval(const double* params, size_t n, int metric, pf_eval_info* info);
+  // K independent evaluations, bitwise equal to K eval() calls
+  void eval_batch(const double* params, size_t K, size_t n, int metric, double* out);
+  // this process's shard partial (shard_count > 1)
+  void eval_partial(const double* params, size_t n, int metric, double* hi_lo, int* penalty);
+
+  const Program& program() const { return pg_; }
+  const Layout& layout() const { return L_; }
+  uint64_t n_events() const { return n_events_; }
+  bool binned() const { return binned_; }
+  uint64_t floor_count() const { return floor_total_; }
+  uint64_t clamp_count(int node) const;
+  void norms(double* norms, double* errs, int32_t* valid, int n) const;
+
+ private:
+  struct Raw {  // per-k outcome of one device pass
+    bool penalty = false;
+    double hi = 0, lo = 0;
+  };
+  void check_call(size_t n, int metric) const;
+  bool params_valid(const double* p) const;
+  void run(const double* params, int K, std::vector<Raw>& out, bool partial_only);
+  cudaGraphExec_t graph_for(Shard& s, int K);
+  void build_tasks(uint32_t grid_points);
+  std::string error_message(uint32_t code_node) const;
+
+  Program pg_;
+  Layout L_;
+  bool binned_ = false;
+  uint64_t n_events_ = 0;
+  double total_content_ = 0;
+  uint64_t chunk_ = 0, n_chunks_total_ = 0;
+  int shard_count_ = 1, shard_index_ = 0;
+  std::vector<Shard> shards_;
+  std::vector<Task> tasks_;              // host copy, all levels
+  std::vector<int> level_first_task_, level_n_tasks_, level_blocks_;
+  int max_norm_blocks_ = 0;
+  double* h_params_ = nullptr;  // pinned, kMaxBatch x np
+  uint64_t floor_total_ = 0;
+  std::vector<uint64_t> clamp_total_;
+  std::vector<double> norms_, errs_;
+  std::vector<int32_t> norm_valid_;
+};
+
+uint64_t kernel_launch_count();
+
+}  // namespace pfb

@@ -1,0 +1,177 @@
+"""GPU parity: the CUDA path (through the C ABI) against the C oracle and the
+compiled reference, on the reference tests' own inputs where they exist.
+
+Tolerance (BASELINE.json north_star): NLL / chi2 at fixed parameters within
+1e-12 relative of the CPU oracle.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_1311_1753_b200 import parfit as pf
+
+pytestmark = pytest.mark.gpu
+REL = 1e-12
+
+
+def close(a, b, rel=REL):
+    return abs(a - b) <= rel * max(abs(a), abs(b))
+
+
+def mixture(a=-0.6, m=5.0, s=1.0, f=0.4, lo=0.0, hi=10.0):
+    x = pf.new_observable("x", lo, hi)
+    av = pf.new_parameter("a", a, 0.1, -5, 5)
+    mv = pf.new_parameter("m", m, 0.1, 0, 10)
+    sv = pf.new_parameter("s", s, 0.1, 0.1, 5)
+    fv = pf.new_parameter("f", f, 0.01, 0, 1)
+    pdf = pf.add_pdf("mix", [pf.exp_pdf("e", x, av), pf.gaussian_pdf("g", x, mv, sv)], [fv])
+    return x, pdf
+
+
+def test_golden_acceptance_criterion5():
+    """acceptance.cpp:305-348: 1e6 events, mt19937_64(31), x = 10 u;
+    reference prints NLL 3218448.5501374062."""
+    x, pdf = mixture()
+    ds = pf.UnbinnedDataSet.from_columns([x], 10.0 * oracle.mt64_uniform(31, 1_000_000))
+    bm = pf.BoundModel(pdf, ds)
+    assert [p.name for p in bm.registry().parameters()] == ["f", "a", "m", "s"]
+    nll = bm.eval_metric(bm.registry().export_values())
+    assert close(nll, 3218448.5501374062), f"{nll!r}"
+    # node norms: e = 1.6625354130382941, g = 2.5066268375731329
+    e, g = pdf.children()
+    assert close(e.cached_norm(), 1.6625354130382941, 1e-14)
+    assert close(g.cached_norm(), 2.5066268375731329, 1e-14)
+    assert abs(pdf.cached_norm() - 1.0) < 1e-9
+
+
+def test_three_event_exponential():
+    """test_engine.cpp:82-97"""
+    x = pf.new_observable("x", 0, 21.49)
+    alpha = pf.new_parameter("alpha", -2, 0.1, -10, 10)
+    ds = pf.UnbinnedDataSet(x)
+    for v in (3.0, 5.0, 1.0):
+        x.value = v
+        ds.add_event()
+    bm = pf.BoundModel(pf.exp_pdf("e", x, alpha), ds)
+    nll = bm.eval_metric(bm.registry().export_values())
+    norm = (1.0 - math.exp(-2.0 * 21.49)) / 2.0
+    expect = -(-2.0 * (3 + 5 + 1)) + 3 * math.log(norm)
+    assert abs(nll - expect) <= 1e-9 * abs(expect)
+    o = oracle.Oracle(bm.pdf(), ds)
+    assert close(nll, o.eval([-2.0]))
+
+
+def test_empty_dataset_zero():
+    """test_engine.cpp:52-59"""
+    x = pf.new_observable("x", 0, 10)
+    a = pf.new_parameter("a", -2, 0.1, -10, 10)
+    bm = pf.BoundModel(pf.exp_pdf("e", x, a), pf.UnbinnedDataSet(x))
+    assert bm.eval_metric(bm.registry().export_values()) == 0.0
+
+
+def test_uniform_single_event_log10():
+    """test_engine.cpp:70-80"""
+    x = pf.new_observable("x", 0, 10)
+    c0 = pf.new_parameter("c0", 1, 0.1, 0.5, 5)
+    ds = pf.UnbinnedDataSet(x)
+    x.value = 4.2
+    ds.add_event()
+    bm = pf.BoundModel(pf.polynomial_pdf("u", x, [c0]), ds)
+    assert abs(bm.eval_metric(bm.registry().export_values()) - math.log(10.0)) <= 1e-10 * math.log(10)
+
+
+def test_matched_bins_zero_chi2():
+    """test_engine.cpp:99-109"""
+    x = pf.new_observable("x", 0, 10)
+    c0 = pf.new_parameter("c0", 1, 0.1, 0.5, 5)
+    b = pf.BinnedDataSet([x], [10])
+    for i in range(10):
+        b.fill([0.5 + i], 5.0)
+    bm = pf.BoundModel(pf.polynomial_pdf("u", x, [c0]), b)
+    assert abs(bm.eval_metric(bm.registry().export_values(), pf.MetricKind.ChiSquared)) <= 1e-15
+
+
+def test_floor_counter():
+    """test_engine.cpp:150-166"""
+    x = pf.new_observable("x", 0, 10)
+    c0 = pf.new_parameter("c0", 0, 0.1, -5, 5)
+    c1 = pf.new_parameter("c1", 1, 0.1, -5, 5)
+    ds = pf.UnbinnedDataSet(x)
+    for v in (0.0, 5.0):
+        x.value = v
+        ds.add_event()
+    bm = pf.BoundModel(pf.polynomial_pdf("ramp", x, [c0, c1]), ds)
+    nll = bm.eval_metric(bm.registry().export_values())
+    assert math.isfinite(nll)
+    assert bm.log_floor_count() == 1
+    o = oracle.Oracle(bm.pdf(), ds)
+    assert close(nll, o.eval(bm.registry().export_values()))
+
+
+def test_penalty_for_fraction_sum():
+    """test_engine.cpp:168-186"""
+    x = pf.new_observable("x", 0, 10)
+    a = pf.new_parameter("a", -2, 0.1, -10, 10)
+    m = pf.new_parameter("m", 5, 0.1, 0, 10)
+    s = pf.new_parameter("s", 1, 0.1, 0.1, 5)
+    f1 = pf.new_parameter("f1", 0.8, 0.01, 0, 1)
+    f2 = pf.new_parameter("f2", 0.8, 0.01, 0, 1)
+    pdf = pf.add_pdf("mix", [pf.exp_pdf("e", x, a), pf.gaussian_pdf("g", x, m, s),
+                             pf.gaussian_pdf("g2", x, m, s)], [f1, f2])
+    ds = pf.UnbinnedDataSet(x)
+    x.value = 5
+    ds.add_event()
+    bm = pf.BoundModel(pdf, ds)
+    assert bm.eval_metric(bm.registry().export_values()) == pf.kPenaltyValue
+
+
+def test_metric_mismatch_raises():
+    """test_engine.cpp:111-121"""
+    x = pf.new_observable("x", 0, 10)
+    c0 = pf.new_parameter("c0", 1, 0.1, 0.5, 5)
+    ds = pf.UnbinnedDataSet(x)
+    x.value = 1
+    ds.add_event()
+    bm = pf.BoundModel(pf.polynomial_pdf("p", x, [c0]), ds)
+    with pytest.raises(pf.Error, match="metric-mismatch"):
+        bm.eval_metric(bm.registry().export_values(), pf.MetricKind.ChiSquared)
+
+
+@pytest.mark.parametrize("n", [1, 255, 4096, 4097, 50_000, 1_000_003])
+def test_mixture_vs_oracle_ragged(n):
+    """backend-equivalence inputs (test_engine.cpp:123-148) at ragged sizes"""
+    x, pdf = mixture(a=-0.7, m=5, s=1, f=0.5)
+    ds = pf.UnbinnedDataSet.from_columns([x], 10.0 * oracle.mt64_uniform(77, n))
+    bm = pf.BoundModel(pdf, ds)
+    o = oracle.Oracle(pdf, ds)
+    rng = np.random.default_rng(n)
+    for _ in range(4):
+        p = [rng.uniform(0, 1), rng.uniform(-2, 0), rng.uniform(3, 7), rng.uniform(0.5, 2)]
+        assert close(bm.eval_metric(p), o.eval(p))
+
+
+def test_batch_is_bitwise_sequential():
+    x, pdf = mixture()
+    ds = pf.UnbinnedDataSet.from_columns([x], 10.0 * oracle.mt64_uniform(5, 300_000))
+    bm = pf.BoundModel(pdf, ds)
+    rng = np.random.default_rng(3)
+    P = np.array([[rng.uniform(0, 1), rng.uniform(-2, 0), rng.uniform(3, 7), rng.uniform(0.5, 2)]
+                  for _ in range(40)])
+    P[7, 0] = 1.5  # invalid fraction -> penalty in the batch too
+    batch = bm.eval_metric_batch(P)
+    seq = np.array([bm.eval_metric(p) for p in P])
+    assert np.array_equal(batch, seq)
+    assert batch[7] == pf.kPenaltyValue
+
+
+def test_reference_matches_on_random_points():
+    if not oracle.Reference.available():
+        pytest.skip("oracle/_ref not built")
+    x, pdf = mixture()
+    ds = pf.UnbinnedDataSet.from_columns([x], 10.0 * oracle.mt64_uniform(9, 200_000))
+    bm = pf.BoundModel(pdf, ds)
+    r = oracle.Reference(pdf, ds)
+    for p in ([0.4, -0.6, 5, 1], [0.1, -1.5, 4.2, 0.7], [0.9, -0.1, 6.1, 1.9]):
+        assert close(bm.eval_metric(p), r.eval(p))
