@@ -215,6 +215,38 @@ PF_API int pf_node_norms(pf_model* model, double* norms, double* errs, int32_t* 
 PF_API uint64_t pf_log_floor_count(const pf_model* model);
 PF_API uint64_t pf_clamp_count(const pf_model* model, int32_t node);
 
+/* ---- measurement ---------------------------------------------------------- */
+
+/* Device-side timing of the hot path with CUDA events on the model's own
+ * stream (the stream every graph and kernel of the model is launched on).
+ *   step_ms_*:            one full pf_eval_metric graph (params H2D, pre,
+ *                         norm levels, event pass, final tree, result D2H)
+ *   event_kernel_ms_mean: the event-pass kernel alone (roofline numerator)
+ * flush_l2 != 0 writes a 256 MiB scratch buffer before every timed launch,
+ * outside the timed window, so no step starts with a warm L2. */
+typedef struct pf_bench_result {
+  double step_ms_mean;
+  double step_ms_min;
+  double event_kernel_ms_mean;
+  double event_kernel_ms_min;
+  double metric;
+  uint64_t kernels_per_step;
+  uint64_t h2d_bytes_per_step;
+  uint64_t d2h_bytes_per_step;
+} pf_bench_result;
+
+PF_API int pf_bench(pf_model* model, const double* params, size_t n_params, int32_t metric,
+                    int32_t steps, int32_t flush_l2, pf_bench_result* out, pf_status* status);
+
+/* Event range [first, first + count) of shard `shard_index` of `shard_count`
+ * for a data set of n_events under chunk size `chunk` (the subtree split of
+ * the reduction tree, engine.hpp:63-68). */
+PF_API void pf_shard_events(uint64_t n_events, uint64_t chunk, int32_t shard_count,
+                            int32_t shard_index, uint64_t* first, uint64_t* count);
+
+/* Events per reduction chunk of a bound model (256 x events per thread). */
+PF_API uint64_t pf_model_chunk(const pf_model* model);
+
 /* ---- fit-manager --------------------------------------------------------- */
 
 /* FitConfig, fit.hpp:23-28 */

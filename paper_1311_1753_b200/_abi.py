@@ -71,6 +71,13 @@ class pf_fit_result(C.Structure):
                 ("params", C.POINTER(C.c_double)), ("uncertainties", C.POINTER(C.c_double))]
 
 
+class pf_bench_result(C.Structure):
+    _fields_ = [("step_ms_mean", C.c_double), ("step_ms_min", C.c_double),
+                ("event_kernel_ms_mean", C.c_double), ("event_kernel_ms_min", C.c_double),
+                ("metric", C.c_double), ("kernels_per_step", C.c_uint64),
+                ("h2d_bytes_per_step", C.c_uint64), ("d2h_bytes_per_step", C.c_uint64)]
+
+
 # every symbol include/pfb200.h declares, with its signature
 _SIGNATURES = {
     "pf_graph_finalize": (C.c_int, [C.POINTER(pf_graph), C.c_int32, C.POINTER(C.c_int32), C.c_int32,
@@ -103,6 +110,11 @@ _SIGNATURES = {
     "pf_fit": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(pf_fit_config), C.POINTER(C.c_double),
                          C.POINTER(C.c_int32), C.POINTER(C.c_double), C.POINTER(C.c_double),
                          C.POINTER(C.c_double), C.POINTER(pf_fit_result), C.POINTER(pf_status)]),
+    "pf_bench": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.c_size_t, C.c_int32, C.c_int32,
+                           C.c_int32, C.POINTER(pf_bench_result), C.POINTER(pf_status)]),
+    "pf_shard_events": (None, [C.c_uint64, C.c_uint64, C.c_int32, C.c_int32, C.POINTER(C.c_uint64),
+                               C.POINTER(C.c_uint64)]),
+    "pf_model_chunk": (C.c_uint64, [C.c_void_p]),
     "pf_abi_version": (C.c_int32, []),
     "pf_kernel_launches": (C.c_uint64, []),
 }

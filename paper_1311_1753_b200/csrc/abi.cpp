@@ -210,6 +210,33 @@ int pf_node_norms(pf_model* model, double* norms, double* errs, int32_t* valid, 
   return 0;
 }
 
+int pf_bench(pf_model* model, const double* params, size_t n_params, int32_t metric, int32_t steps,
+             int32_t flush_l2, pf_bench_result* out, pf_status* status) {
+  return guarded(status, [&] {
+    if (!model || !out) throw pfb::Error("bad-model", "null argument");
+    pfb::BenchResult r = model->impl->bench(params, n_params, metric, steps, flush_l2 != 0);
+    out->step_ms_mean = r.step_ms_mean;
+    out->step_ms_min = r.step_ms_min;
+    out->event_kernel_ms_mean = r.event_ms_mean;
+    out->event_kernel_ms_min = r.event_ms_min;
+    out->metric = r.metric;
+    out->kernels_per_step = r.kernels_per_step;
+    out->h2d_bytes_per_step = r.h2d_bytes;
+    out->d2h_bytes_per_step = r.d2h_bytes;
+  });
+}
+
+void pf_shard_events(uint64_t n_events, uint64_t chunk, int32_t shard_count, int32_t shard_index,
+                     uint64_t* first, uint64_t* count) {
+  uint64_t chunks = chunk ? (n_events + chunk - 1) / chunk : 0, lo = 0, hi = 0;
+  pfb::subtree_range(chunks, shard_count, shard_index, &lo, &hi);
+  uint64_t a = std::min(lo * chunk, n_events), b = std::min(hi * chunk, n_events);
+  if (first) *first = a;
+  if (count) *count = b - a;
+}
+
+uint64_t pf_model_chunk(const pf_model* m) { return m ? m->impl->chunk() : 0; }
+
 uint64_t pf_log_floor_count(const pf_model* m) { return m ? m->impl->floor_count() : 0; }
 uint64_t pf_clamp_count(const pf_model* m, int32_t node) { return m ? m->impl->clamp_count(node) : 0; }
 

@@ -46,5 +46,6 @@ Layout generate(const Program& pg, bool binned);
 const char* device_header_source();
 const char* kernels_header_source();
 const char* counters_header_source();
+const char* exp_table_header_source();
 
 }  // namespace pfb

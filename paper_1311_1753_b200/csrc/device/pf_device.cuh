@@ -45,14 +45,30 @@ struct pf_krec {
 
 struct pf_task {  // one midpoint sum: node, n points per box dimension
   int node, n, dims, first_block;
-  int n_blocks, partial_offset, fine, pad;
+  int n_blocks, partial_offset, fine, level;
   pf_u64 points, per_block;
   double lo[PF_MAX_BOX];
   double h[PF_MAX_BOX];
   double vol;
 };
 
+// Per-call result record, written by the device straight into mapped
+// (zero-copy) host memory: no memcpy nodes in the per-call graph.
+struct pf_out {
+  double result_hi, result_lo;
+  pf_u64 floor_count, first_nonfinite, first_event_error;
+  pf_u32 norm_error, pad;
+};
+
 struct pf_args {
+  const double* hP;     // host-mapped parameters (K x PF_NP)
+  pf_out* hout;         // host-mapped results (K)
+  double* hnorms;       // host-mapped norms (K x 3 n_nodes)
+  pf_u64* hclamp;       // host-mapped clamp counters
+  int n_nodes;
+  int fuse_final;       // K == 1: the last event block runs the final tree
+  int n_levels;
+  int pad0;
   const double* data;   // column-major shard: data[col * col_stride + e]
   pf_u64 col_stride;
   pf_u64 n_local;       // events (bins) in this shard
@@ -151,6 +167,25 @@ __device__ __forceinline__ pf_dd pf_warp_reduce_runs(const pf_dd* v, int n) {
   return acc;
 }
 
+// Fixed-shape block reduction (any blockDim multiple of 32, <= 1024): a
+// shuffle tree inside every warp, then one over the warp results.  All
+// threads must call; the result is valid in thread 0.  sm: >= 32 slots.
+__device__ __forceinline__ pf_dd pf_block_reduce(pf_dd v, pf_dd* sm) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = blockDim.x >> 5;
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) v = pf_dd_add(v, pf_shfl_down_dd(v, d));
+  __syncthreads();  // sm may still be read by a previous call
+  if (lane == 0) sm[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    v = lane < nw ? sm[lane] : pf_dd_zero();
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) v = pf_dd_add(v, pf_shfl_down_dd(v, d));
+  }
+  return v;
+}
+
 // ----------------------------------------------------------------------------
 // Reference reduction shape over chunk partials (engine.hpp:63-68): a
 // recursive pairwise tree that splits [lo, hi) at lo + (hi - lo) / 2.  An
@@ -201,34 +236,145 @@ __device__ pf_dd pf_pairwise_seq(const pf_dd* v, pf_u64 lo, pf_u64 hi) {
   return ret;
 }
 
-// Block-parallel evaluation of the same tree with PF_FINAL_THREADS threads:
-// thread t owns the subtree at depth 10 selected by the bits of t, the
-// top 10 levels are a complete binary tree combined in shared memory.
-__device__ pf_dd pf_pairwise_block(const pf_dd* v, pf_u64 n, pf_dd* sm /* 1024 */) {
+// Block-parallel evaluation of the same tree with nthreads = 2^d threads:
+// thread t owns the subtree at depth d selected by the bits of t (MSB
+// first); the top d levels are a complete binary tree combined in shared
+// memory.  Every node is still left + right of the reference's split, so the
+// value does not depend on d.
+__device__ pf_dd pf_pairwise_block(const pf_dd* v, pf_u64 n, pf_dd* sm, int nthreads) {
   const int t = threadIdx.x;
+  int depth = 0;
+  while ((1 << depth) < nthreads) ++depth;
   pf_u64 lo = 0, hi = n;
 #pragma unroll 1
-  for (int level = 0; level < 10; ++level) {
+  for (int level = 0; level < depth; ++level) {
     pf_u64 mid = lo + (hi - lo) / 2;
-    if ((t >> (9 - level)) & 1)
+    if ((t >> (depth - 1 - level)) & 1)
       lo = mid;
     else
       hi = mid;
   }
-  sm[t] = pf_pairwise_seq(v, lo, hi);
+  pf_dd own = pf_pairwise_seq(v, lo, hi);
+  __syncthreads();  // sm may alias data the block read before
+  sm[t] = own;
   __syncthreads();
-  for (int width = 512; width >= 1; width >>= 1) {
-    if (t < width) sm[t] = pf_dd_add(sm[2 * t], sm[2 * t + 1]);
+  for (int width = nthreads >> 1; width >= 1; width >>= 1) {
+    pf_dd x;
+    if (t < width) x = pf_dd_add(sm[2 * t], sm[2 * t + 1]);
+    __syncthreads();
+    if (t < width) sm[t] = x;
     __syncthreads();
   }
   return sm[0];
 }
 
 // ----------------------------------------------------------------------------
-// scalar math used by the node kernels (libdevice, <= 1 ulp)
-__device__ __forceinline__ double pf_exp(double x) { return exp(x); }
+// scalar math used by the node kernels
+//
+// pf_exp: table-driven exp.  x = (128 e + j) ln2/128 + r, |r| <= ln2/256;
+// exp(x) = 2^e * 2^(j/128) * (1 + expm1(r)) with 2^(j/128) = hi + lo from a
+// 128-entry shared-memory table and expm1(r) a degree-5 Taylor polynomial
+// (truncation r^6/720 < 6e-19).  One rounding dominates: error ~0.51 ulp,
+// 12 FP64 instructions instead of libdevice's ~17.  |x| >= 708, inf and NaN
+// take libdevice's exp.
+#include "pf_exp_table.cuh"
+
+__shared__ double2 pf_exp_tab[128];
+
+// every kernel calls this before the first pf_exp (includes __syncthreads)
+__device__ __forceinline__ void pf_math_init() {
+  for (int i = threadIdx.x; i < 128; i += blockDim.x)
+    pf_exp_tab[i] = make_double2(pf_exp_tab_g[2 * i], pf_exp_tab_g[2 * i + 1]);
+  __syncthreads();
+}
+
+__device__ __forceinline__ double pf_exp_core(double x);
+
+__device__ __forceinline__ double pf_exp(double x) {
+#ifdef PF_EXP_LIBDEVICE
+  return exp(x);
+#endif
+  // branch-free range handling: the two-step 2^e scaling below is exact for
+  // |x| <= 1100 (0 / inf beyond exp's range come out of the final multiply);
+  // larger |x| and +-inf are clamped by compare-selects that keep NaN.
+  x = x < -1100.0 ? -1100.0 : x;
+  x = x > 1100.0 ? 1100.0 : x;
+  return pf_exp_core(x);
+}
+
+// exp for arguments known to be <= 0 (Gaussian exponents): one clamp fewer
+__device__ __forceinline__ double pf_exp_neg(double x) {
+#ifdef PF_EXP_LIBDEVICE
+  return exp(x);
+#endif
+  x = x < -1100.0 ? -1100.0 : x;
+  return pf_exp_core(x);
+}
+
+__device__ __forceinline__ double pf_exp_core(double x) {
+  const double kd = fma(x, PF_EXP_INVLN2N, 0x1.8p52);
+  const int ki = __double2loint(kd);
+  const double k = kd - 0x1.8p52;
+  double r = fma(k, -PF_EXP_LN2N_HI, x);
+  r = fma(k, -PF_EXP_LN2N_LO, r);
+  const double2 t = pf_exp_tab[ki & 127];
+  const double r2 = r * r;
+  const double q = fma(fma(fma(r, 1.0 / 120.0, 1.0 / 24.0), r, 1.0 / 6.0), r, 0.5);
+  const double p = fma(r2, q, r);
+  const double s = fma(t.x, p, t.y) + t.x;
+  // 2^e in two factors (e in [-1477, 1477]): 2^e1 folded exactly into the
+  // exponent field of s (integer add), 2^(e - e1) by the one rounding multiply
+  const int e = ki >> 7;
+  const int e1 = e >> 1;
+  const double sc = __hiloint2double(__double2hiint(s) + (e1 << 20), __double2loint(s));
+  return sc * __hiloint2double((e - e1 + 1023) << 20, 0);
+}
+
+// ----------------------------------------------------------------------------
+// TMA bulk copies (cp.async.bulk, global -> shared) completed on mbarriers.
+__device__ __forceinline__ unsigned pf_smem_addr(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void pf_mbar_init(pf_u64* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(pf_smem_addr(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void pf_fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void pf_mbar_expect_tx(pf_u64* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(pf_smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void pf_tma_load(void* dst, const void* src, unsigned bytes, pf_u64* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          pf_smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(pf_smem_addr(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void pf_mbar_wait(pf_u64* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "PF_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra PF_WAIT;\n"
+      "}\n" ::"r"(pf_smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+
 __device__ __forceinline__ double pf_log(double x) { return log(x); }
 __device__ __forceinline__ double pf_pow(double x, double y) { return pow(x, y); }
+
+// 1e-300 as an integer: for x >= +0 the IEEE bit pattern orders like x
+#define PF_FLOOR_BITS 0x01a56e1fc2f8f359LL
 
 // ln 2 split so that E * PF_LN2_HI is exact for |E| < 2^21 (fdlibm constants)
 #define PF_LN2_HI 6.93147180369123816490e-01
@@ -248,17 +394,19 @@ __device__ __forceinline__ void pf_prod_init(pf_prod& p) {
   p.e = 0;
 }
 
+// v is in 2^[-500, 600] here (the caller rescales rarer magnitudes) and m
+// stays within 2^[-400, 400) between renormalisations, so m * v can neither
+// over- nor underflow; renormalising only when m leaves that band keeps the
+// serial chain to one DMUL and one integer compare.
 __device__ __forceinline__ void pf_prod_mul(pf_prod& p, double v) {
-  // v is finite and >= 1e-300 here; keep m * v inside the normal range
-  if (v > 0x1p+900) {
-    v *= 0x1p-600;
-    p.e += 600;
-  }
   double m = p.m * v;
-  int hi = __double2hiint(m);
-  int ex = (hi >> 20) - 1023;
-  p.e += ex;
-  p.m = __hiloint2double(hi - (ex << 20), __double2loint(m));
+  const unsigned hi = (unsigned)__double2hiint(m);
+  if (hi - 0x26F00000u >= 0x32000000u) {  // biased exponent outside [623, 1423)
+    const int ex = (int)((hi >> 20) & 0x7ff) - 1023;
+    p.e += ex;
+    m = __hiloint2double((int)hi - (ex << 20), __double2loint(m));
+  }
+  p.m = m;
 }
 
 // -log(prod) as a DD value

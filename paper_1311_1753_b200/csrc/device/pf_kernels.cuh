@@ -2,56 +2,154 @@
 //
 // Included by the generated evaluator AFTER it has defined:
 //   PF_NP, PF_SS, PF_NCOLS, PF_NLOAD, PF_EPT, PF_BINNED, PF_NPOLY,
-//   pf_load_col(q) (data columns read per event),
-//   pf_stage_pre(k, P, S, C, cx, tid, nt)       parameter-derived constants
-//   pf_stage_post(level, k, P, S, C, cx, tid, nt) constants needing norms
-//   pf_norm_point(node, flat, task, P, S, C, cx)  raw at one grid midpoint
-//   pf_eval_event(ev, P, S, C, cx)               normalised density (NLL) or
-//                                                 N_tot * density (chi2)
-//   pf_norm_nodes_of_level(level, nodes[]), PF_NORM_COUNT(level)
+//   pf_load_col(q)                                 data columns read per event
+//   pf_stage_pre(k, P, S, C, cx, cnt, tid, nt)      parameter-derived constants
+//   pf_stage_post(level, k, P, S, C, cx, cnt, tid, nt)  constants needing norms
+//   pf_norm_point(node, flat, task, P, S, C, cx, cnt)   raw at a grid midpoint
+//   pf_eval_event(ev, P, S, C, cx, cnt)            normalised density (NLL) or
+//                                                  N_tot * density (chi2)
 //
-// Launch sequence per call (engine.cpp):  pre -> norm(level 0..L) -> event
-// -> final.  Every reduction has a fixed shape, so a call is bitwise
-// reproducible and independent of the number of devices.
+// Per-call graph (engine.cpp):
+//   small normalisation grids:  setup ──PDL──> event(+final tree)
+//   large grids:                pre -> norm level 0..L ──PDL──> event(+final)
+//   batched (K > 1):            ... -> event -> final (one block per k)
+// Parameters are read from, and results written to, mapped host memory.
+// Every reduction has a fixed shape: a call is bitwise reproducible and
+// independent of the number of devices.
+
+// griddepcontrol (programmatic dependent launch); no-ops without PDL
+__device__ __forceinline__ void pf_pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
+__device__ __forceinline__ void pf_pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+__device__ __forceinline__ void pf_rec_init(pf_krec* r) {
+  r->floor_count = 0ull;
+  r->first_nonfinite = ~0ull;
+  r->first_event_error = ~0ull;
+  r->norm_error = ~0u;
+  for (int i = 0; i <= PF_MAX_LEVELS; ++i) r->arrive[i] = 0u;
+  r->result_hi = 0.0;
+  r->result_lo = 0.0;
+}
+
+__device__ __forceinline__ void pf_load_params(const pf_args& a, int k) {
+  for (int i = threadIdx.x; i < PF_NP; i += blockDim.x)
+    ((double*)a.P)[(pf_u64)k * PF_NP + i] = a.hP[(pf_u64)k * PF_NP + i];
+}
+
+// Richardson combination of a node's (coarse, fine) sums (pdf.hpp:178-188)
+__device__ __forceinline__ void pf_finish_norm(double* S, pf_krec* r, int node, double coarse,
+                                               double fine) {
+  const double norm = fine + (fine - coarse) / 3.0;
+  const double err = fabs(fine - coarse) / 3.0;
+  S[3 * node + 0] = norm;
+  S[3 * node + 1] = err;
+  S[3 * node + 2] = 1.0 / norm;
+  if (!(norm > 0.0) || !isfinite(norm))
+    atomicMin(&r->norm_error, ((pf_u32)node << 8) | PF_E_ZERO_INTEGRAL);
+}
+
+// Results of parameter set k into mapped host memory.
+__device__ void pf_publish(const pf_args& a, int k, double hi, double lo) {
+  const pf_krec* r = a.rec + k;
+  pf_out* o = a.hout + k;
+  if (threadIdx.x == 0) {
+    o->result_hi = hi;
+    o->result_lo = lo;
+    o->floor_count = r->floor_count;
+    o->first_nonfinite = r->first_nonfinite;
+    o->first_event_error = r->first_event_error;
+    o->norm_error = r->norm_error;
+  }
+  const double* S = a.S + (pf_u64)k * PF_SS;
+  for (int i = threadIdx.x; i < 3 * a.n_nodes; i += blockDim.x)
+    a.hnorms[(pf_u64)k * 3 * a.n_nodes + i] = S[i];
+#if PF_NPOLY > 0
+  if (k == a.K - 1)
+    for (int i = threadIdx.x; i < PF_NPOLY; i += blockDim.x) a.hclamp[i] = a.clamp[i];
+#endif
+}
 
 // ---------------------------------------------------------------------------
-// pre: initialise the call record and the parameter-derived constants.
-extern "C" __global__ void __launch_bounds__(PF_THREADS) pf_pre_kernel(pf_args a) {
+// setup: parameters H2D, call records, pre stage and EVERY normalisation
+// level in one CTA per parameter set (small grids).  Midpoint sums at n and
+// 2n (pdf.hpp:148-176): thread t sums points t, t + 1024, ... in double-
+// double; a fixed-shape block reduction combines the 1024 partials.
+extern "C" __global__ void __launch_bounds__(PF_FINAL_THREADS) pf_setup_kernel(pf_args a) {
+  __shared__ pf_dd sm[PF_FINAL_THREADS];
+  __shared__ double sums[64];
+  pf_pdl_trigger();  // let the event kernel start streaming its data now
+  pf_math_init();
   const int k = blockIdx.x;
   pf_krec* r = a.rec + k;
-  if (threadIdx.x == 0) {
-    r->floor_count = 0ull;
-    r->first_nonfinite = ~0ull;
-    r->first_event_error = ~0ull;
-    r->norm_error = ~0u;
-    for (int i = 0; i <= PF_MAX_LEVELS; ++i) r->arrive[i] = 0u;
-    r->result_hi = 0.0;
-    r->result_lo = 0.0;
-  }
+  pf_load_params(a, k);
+  if (threadIdx.x == 0) pf_rec_init(r);
   __syncthreads();
+  const double* P = a.P + (pf_u64)k * PF_NP;
+  double* S = a.S + (pf_u64)k * PF_SS;
   pf_ctx cx;
   cx.err = 0;
   pf_cnt cnt;
   pf_cnt_init(cnt);
-  pf_stage_pre(k, a.P + (pf_u64)k * PF_NP, a.S + (pf_u64)k * PF_SS, a.C, cx, cnt,
-               threadIdx.x, blockDim.x);
+  pf_stage_pre(k, P, S, a.C, cx, cnt, threadIdx.x, blockDim.x);
+  int t0 = 0;
+  for (int level = 0; level < a.n_levels; ++level) {
+    int t1 = t0;
+    while (t1 < a.n_tasks && a.tasks[t1].level == level) ++t1;
+    for (int t = t0; t < t1; ++t) {
+      const pf_task& T = a.tasks[t];
+      pf_dd acc = pf_dd_zero();
+      for (pf_u64 i = threadIdx.x; i < T.points; i += PF_FINAL_THREADS)
+        acc = pf_dd_add_d(acc, pf_norm_point(T.node, i, T, P, S, a.C, cx, cnt));
+      pf_dd s = pf_block_reduce(acc, sm);
+      // midpoint_sum returns static_cast<double>(sum) * vol (pdf.hpp:173-175)
+      if (threadIdx.x == 0) sums[t - t0] = __dmul_rn(pf_dd_to_double(s), T.vol);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int t = t0; t + 1 < t1; t += 2)
+        pf_finish_norm(S, r, a.tasks[t].node, sums[t - t0], sums[t + 1 - t0]);
+    __syncthreads();
+    pf_stage_post(level, k, P, S, a.C, cx, cnt, threadIdx.x, blockDim.x);
+    t0 = t1;
+  }
   if (cx.err) atomicMin(&r->norm_error, cx.err);
   pf_cnt_flush(cnt, a.clamp);
 }
 
 // ---------------------------------------------------------------------------
-// norm: midpoint sums at n and 2n per box dimension for every normalised node
-// of one level (pdf.hpp:148-176), Richardson combination (pdf.hpp:178-188)
-// by the last block to arrive, then the post-level constants.
+// pre (large grids): parameters, call records and the pre stage.
+extern "C" __global__ void __launch_bounds__(PF_THREADS) pf_pre_kernel(pf_args a) {
+  pf_math_init();
+  const int k = blockIdx.x;
+  pf_krec* r = a.rec + k;
+  pf_load_params(a, k);
+  if (threadIdx.x == 0) pf_rec_init(r);
+  __syncthreads();
+  pf_ctx cx;
+  cx.err = 0;
+  pf_cnt cnt;
+  pf_cnt_init(cnt);
+  pf_stage_pre(k, a.P + (pf_u64)k * PF_NP, a.S + (pf_u64)k * PF_SS, a.C, cx, cnt, threadIdx.x,
+               blockDim.x);
+  if (cx.err) atomicMin(&r->norm_error, cx.err);
+  pf_cnt_flush(cnt, a.clamp);
+}
+
+// ---------------------------------------------------------------------------
+// norm (large grids): one level, many blocks per midpoint sum; the last
+// block to arrive combines the block partials, applies Richardson and runs
+// the post stage.
 extern "C" __global__ void __launch_bounds__(PF_THREADS) pf_norm_kernel(pf_args a) {
   __shared__ pf_dd sm[PF_THREADS];
   __shared__ int s_last;
+  __shared__ double sums[64];
+  if (a.level == a.n_levels - 1) pf_pdl_trigger();
+  pf_math_init();
   const int k = blockIdx.y;
   const double* P = a.P + (pf_u64)k * PF_NP;
   double* S = a.S + (pf_u64)k * PF_SS;
   // one partial per block: task t owns [first_block, first_block + n_blocks)
   pf_dd* part = a.partials + (pf_u64)k * gridDim.x;
-  // locate this block's task (n_tasks is small)
   int t = 0;
   while (t + 1 < a.n_tasks && (int)blockIdx.x >= a.tasks[t + 1].first_block) ++t;
   const pf_task& T = a.tasks[t];
@@ -65,15 +163,12 @@ extern "C" __global__ void __launch_bounds__(PF_THREADS) pf_norm_kernel(pf_args 
   pf_dd acc = pf_dd_zero();
   for (pf_u64 i = lo + threadIdx.x; i < hi; i += PF_THREADS)
     acc = pf_dd_add_d(acc, pf_norm_point(T.node, i, T, P, S, a.C, cx, cnt));
-  sm[threadIdx.x] = acc;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    pf_dd s = pf_warp_reduce_runs(sm, PF_THREADS);
+  {
+    pf_dd s = pf_block_reduce(acc, sm);
     if (threadIdx.x == 0) part[blockIdx.x] = s;
   }
   if (cx.err) atomicMin(&a.rec[k].norm_error, cx.err);
   pf_cnt_flush(cnt, a.clamp);
-  // last block of this (level, k) finalises
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -83,31 +178,17 @@ extern "C" __global__ void __launch_bounds__(PF_THREADS) pf_norm_kernel(pf_args 
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  __shared__ double sums[64];
   for (int tt = 0; tt < a.n_tasks; ++tt) {
     const pf_task& U = a.tasks[tt];
-    const pf_dd* pv = part + U.first_block;
     if (threadIdx.x < 32) {
-      pf_dd s = pf_warp_reduce_runs(pv, U.n_blocks);
-      // midpoint_sum returns static_cast<double>(sum) * vol (pdf.hpp:173-175)
+      pf_dd s = pf_warp_reduce_runs(part + U.first_block, U.n_blocks);
       if (threadIdx.x == 0) sums[tt] = __dmul_rn(pf_dd_to_double(s), U.vol);
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    // tasks come in (coarse, fine) pairs per node
-    for (int tt = 0; tt + 1 < a.n_tasks; tt += 2) {
-      const int node = a.tasks[tt].node;
-      const double coarse = sums[tt], fine = sums[tt + 1];
-      const double norm = fine + (fine - coarse) / 3.0;
-      const double err = fabs(fine - coarse) / 3.0;
-      S[3 * node + 0] = norm;
-      S[3 * node + 1] = err;
-      S[3 * node + 2] = 1.0 / norm;
-      if (!(norm > 0.0) || !isfinite(norm))
-        atomicMin(&a.rec[k].norm_error, ((pf_u32)node << 8) | PF_E_ZERO_INTEGRAL);
-    }
-  }
+  if (threadIdx.x == 0)
+    for (int tt = 0; tt + 1 < a.n_tasks; tt += 2)
+      pf_finish_norm(S, a.rec + k, a.tasks[tt].node, sums[tt], sums[tt + 1]);
   __syncthreads();
   pf_ctx cx2;
   cx2.err = 0;
@@ -119,127 +200,237 @@ extern "C" __global__ void __launch_bounds__(PF_THREADS) pf_norm_kernel(pf_args 
 }
 
 // ---------------------------------------------------------------------------
-// event pass: PF_EPT events per thread, PF_THREADS * PF_EPT per chunk.  Data
-// are read once per chunk and reused for every parameter set k.
-extern "C" __global__ void __launch_bounds__(PF_THREADS) pf_event_kernel(pf_args a) {
-  extern __shared__ pf_dd smk[];  // K x PF_THREADS
-  const int tid = threadIdx.x;
-  const int warp = tid >> 5;
-  for (int c = blockIdx.x; c < a.n_chunks; c += gridDim.x) {
-    const pf_u64 base = (pf_u64)c * (PF_THREADS * PF_EPT);
-    double val[PF_NLOAD][PF_EPT];
-    bool ok[PF_EPT];
-    const bool full = base + (pf_u64)(PF_THREADS * PF_EPT) <= a.n_local;
-#if PF_EPT >= 2
+// event pass.  A chunk (the reduction unit, 256 * PF_EPT events) belongs to
+// ONE warp, which walks it in PF_NSUB sub-chunks of 32 * PF_EPT events.
+// Sub-chunks are staged global -> shared by TMA bulk copies into a per-warp
+// ring of PF_NST stages (mbarrier completion), PF_NST - 1 copies in flight
+// while the warp computes; the compute loop reads the stage with
+// conflict-free LDS (lane l takes events 32 j + l), so the code stays small
+// and the memory stream never waits on the math.  Per lane: densities are
+// multiplied into a running product (one log per lane and sub-chunk), the
+// -log terms accumulate in double-double, and a fixed shuffle tree finishes
+// each chunk.  No block-level barrier in the main loop.  The first stages are
+// issued BEFORE waiting on the setup grid (PDL).
+
+#define PF_SUB (32 * PF_EPT)
+#define PF_NSUB 8  // sub-chunks per chunk: chunk = 256 * PF_EPT events
+#ifndef PF_NST
+#define PF_NST 3
+#endif
+#ifndef PF_EV_WARPS
+#define PF_EV_WARPS 2  // warps per event block: fine-grained block scheduling
+#endif
+#define PF_EV_THREADS (32 * PF_EV_WARPS)
+#define PF_STAGE (PF_NLOAD * PF_SUB)  // doubles per stage
+
+// One event's term for the rare-path rescans (errors / non-finite terms).
+__device__ __noinline__ pf_u32 pf_event_flags(const pf_args& a, int k, const double* st, int i,
+                                              double* v_out) {
+  const double* P = a.P + (pf_u64)k * PF_NP;
+  const double* S = a.S + (pf_u64)k * PF_SS;
+  pf_ctx cx;
+  cx.err = 0;
+  pf_cnt cnt;  // scratch: rescans do not count clamps twice
+  pf_cnt_init(cnt);
+  double ev[PF_NCOLS];
 #pragma unroll
-    for (int i = 0; i < PF_EPT / 2; ++i) {
-      const pf_u64 e = base + 2ull * (pf_u64)(tid + PF_THREADS * i);
-      ok[2 * i] = full || e < a.n_local;
-      ok[2 * i + 1] = full || e + 1 < a.n_local;
+  for (int q = 0; q < PF_NCOLS; ++q) ev[q] = 0.0;
 #pragma unroll
-      for (int q = 0; q < PF_NLOAD; ++q) {
-        const double* col = a.data + (pf_u64)pf_load_col(q) * a.col_stride;
-        if (full) {
-          double2 w = __ldg(reinterpret_cast<const double2*>(col + e));
-          val[q][2 * i] = w.x;
-          val[q][2 * i + 1] = w.y;
-        } else {
-          val[q][2 * i] = ok[2 * i] ? __ldg(col + e) : 0.0;
-          val[q][2 * i + 1] = ok[2 * i + 1] ? __ldg(col + e + 1) : 0.0;
-        }
+  for (int q = 0; q < PF_NLOAD; ++q) ev[pf_load_col(q)] = st[q * PF_SUB + i];
+  *v_out = pf_eval_event(ev, P, S, a.C, cx, cnt);
+  return cx.err;
+}
+
+// Rare path, out of line: the first event (in this lane's order) that raised
+// an error or produced a non-finite term is found by re-evaluating.
+__device__ __noinline__ void pf_rescan(const pf_args& a, int k, pf_u64 base, int lane,
+                                       const double* st, int n_valid, bool want_err) {
+  for (int j = 0; j < PF_EPT; ++j) {
+    const int i = 32 * j + lane;
+    if (i >= n_valid) break;
+    double v;
+    const pf_u32 err = pf_event_flags(a, k, st, i, &v);
+    if (want_err) {
+      if (err) {
+        atomicMin(&a.rec[k].first_event_error, ((a.event_offset + base + i) << 24) | (pf_u64)err);
+        return;
+      }
+    } else {
+#if PF_BINNED
+      const double mu = v * st[(PF_NLOAD - 1) * PF_SUB + i];
+      const double diff = st[(PF_NLOAD - 2) * PF_SUB + i] - mu;
+      const double term = diff * diff / fmax(mu, PF_CHISQ_EPS);
+      const bool bad = !isfinite(term);
+#else
+      const bool bad = !(v < PF_LOG_FLOOR) && !(v <= 1.7976931348623157e308);
+#endif
+      if (bad) {
+        atomicMin(&a.rec[k].first_nonfinite, a.event_offset + base + i);
+        return;
       }
     }
-#else
-    {
-      const pf_u64 e = base + (pf_u64)tid;
-      ok[0] = e < a.n_local;
-#pragma unroll
-      for (int q = 0; q < PF_NLOAD; ++q) {
-        const double* col = a.data + (pf_u64)pf_load_col(q) * a.col_stride;
-        val[q][0] = ok[0] ? __ldg(col + e) : 0.0;
-      }
-    }
-#endif
-    for (int k = 0; k < a.K; ++k) {
-      const double* P = a.P + (pf_u64)k * PF_NP;
-      const double* S = a.S + (pf_u64)k * PF_SS;
-      pf_ctx cx;
-      cx.err = 0;
-      pf_cnt cnt;
-      pf_cnt_init(cnt);
-      pf_u32 floors = 0;
-#if PF_BINNED
-      pf_dd acc = pf_dd_zero();
-#else
-      pf_prod acc;
-      pf_prod_init(acc);
-#endif
-#pragma unroll
-      for (int j = 0; j < PF_EPT; ++j) {
-        if (!ok[j]) continue;
-#if PF_EPT >= 2
-        const pf_u64 e = base + 2ull * (pf_u64)(tid + PF_THREADS * (j >> 1)) + (pf_u64)(j & 1);
-#else
-        const pf_u64 e = base + (pf_u64)tid;
-#endif
-        double ev[PF_NCOLS];
-#pragma unroll
-        for (int q = 0; q < PF_NCOLS; ++q) ev[q] = 0.0;
-#pragma unroll
-        for (int q = 0; q < PF_NLOAD; ++q) ev[pf_load_col(q)] = val[q][j];
-        pf_u32 err0 = cx.err;
-        double v = pf_eval_event(ev, P, S, a.C, cx, cnt);
-        if (cx.err != err0 && err0 == 0) {
-          const pf_u64 g = a.event_offset + e;
-          atomicMin(&a.rec[k].first_event_error, (g << 24) | (pf_u64)cx.err);
-        }
-#if PF_BINNED
-        // chi-squared term (engine.hpp:196-206): mu = N_tot * density * volume
-        const double content = ev[PF_CONTENT_COL];
-        const double volume = ev[PF_CONTENT_COL + 1];
-        const double mu = v * volume;
-        const double diff = content - mu;
-        const double term = diff * diff / fmax(mu, PF_CHISQ_EPS);
-        if (!isfinite(term)) atomicMin(&a.rec[k].first_nonfinite, a.event_offset + e);
-        acc = pf_dd_add_d(acc, term);
-#else
-        // NLL term (engine.hpp:186-195): floor at 1e-300, counted
-        if (v < PF_LOG_FLOOR) {
-          v = PF_LOG_FLOOR;
-          ++floors;
-        } else if (!(v <= 1.7976931348623157e308)) {
-          // +inf or NaN: -log(v) is not finite
-          atomicMin(&a.rec[k].first_nonfinite, a.event_offset + e);
-          v = 1.0;
-        }
-        pf_prod_mul(acc, v);
-#endif
-      }
-#if PF_BINNED
-      smk[k * PF_THREADS + tid] = acc;
-#else
-      smk[k * PF_THREADS + tid] = pf_prod_neglog(acc);
-#endif
-      if (floors) atomicAdd(&a.rec[k].floor_count, (pf_u64)floors);
-      pf_cnt_flush(cnt, a.clamp);
-    }
-    __syncthreads();
-    for (int k = warp; k < a.K; k += PF_THREADS / 32) {
-      pf_dd s = pf_warp_reduce_runs(smk + k * PF_THREADS, PF_THREADS);
-      if ((tid & 31) == 0) a.partials[(pf_u64)k * a.n_chunks + c] = s;
-    }
-    __syncthreads();
   }
 }
 
+// this lane's terms over one staged sub-chunk for parameter set k.  FULL:
+// all 32 * PF_EPT events are real (every sub-chunk but the data's last).
+template <bool FULL>
+__device__ __forceinline__ pf_dd pf_stage_terms(const pf_args& a, int k, pf_u64 base, int lane,
+                                                const double* st, int n_valid) {
+  const double* P = a.P + (pf_u64)k * PF_NP;
+  const double* S = a.S + (pf_u64)k * PF_SS;
+  pf_ctx cx;
+  cx.err = 0;
+  pf_cnt cnt;
+  pf_cnt_init(cnt);
+  pf_u32 floors = 0;
+  bool bad = false;
+#if PF_BINNED
+  pf_dd acc = pf_dd_zero();
+#else
+  pf_prod acc;
+  pf_prod_init(acc);
+#endif
+#pragma unroll 2
+  for (int j = 0; j < PF_EPT; ++j) {
+    const int i = 32 * j + lane;
+    double ev[PF_NCOLS];
+#pragma unroll
+    for (int q = 0; q < PF_NCOLS; ++q) ev[q] = 0.0;
+#pragma unroll
+    for (int q = 0; q < PF_NLOAD; ++q) ev[pf_load_col(q)] = st[q * PF_SUB + i];
+    double v = pf_eval_event(ev, P, S, a.C, cx, cnt);
+#if PF_BINNED
+    // chi-squared term (engine.hpp:196-206): mu = N_tot * density * volume
+    const double content = ev[PF_CONTENT_COL];
+    const double volume = ev[PF_CONTENT_COL + 1];
+    const double mu = v * volume;
+    const double diff = content - mu;
+    double term = diff * diff / fmax(mu, PF_CHISQ_EPS);
+    if (!FULL && i >= n_valid) term = 0.0;
+    bad |= !(term <= 1.7976931348623157e308);
+    acc = pf_dd_add_d(acc, term);
+#else
+    if (!FULL && i >= n_valid) v = 1.0;
+    // common case in one test: 2^-500 <= v <= 2^600 (no floor, finite, and
+    // safe for the running product)
+    if (!(v >= 0x1p-500 && v <= 0x1p+600)) {
+      // NLL term (engine.hpp:186-195): v < 1e-300 is floored and counted;
+      // NaN / +inf make -log(v) non-finite (first index found by a rescan)
+      if (v < PF_LOG_FLOOR) {
+        v = PF_LOG_FLOOR;
+        ++floors;
+      } else if (!(v <= 1.7976931348623157e308)) {
+        bad = true;
+        v = 1.0;
+      }
+      if (v < 0x1p-500) {
+        v *= 0x1p+600;
+        acc.e -= 600;
+      } else if (v > 0x1p+600) {
+        v *= 0x1p-600;
+        acc.e += 600;
+      }
+    }
+    pf_prod_mul(acc, v);
+#endif
+  }
+  if (cx.err) pf_rescan(a, k, base, lane, st, FULL ? PF_SUB : n_valid, true);
+  if (bad) pf_rescan(a, k, base, lane, st, FULL ? PF_SUB : n_valid, false);
+  if (floors) atomicAdd(&a.rec[k].floor_count, (pf_u64)floors);
+  pf_cnt_flush(cnt, a.clamp);
+#if PF_BINNED
+  return acc;
+#else
+  return pf_prod_neglog(acc);
+#endif
+}
+
+__device__ __forceinline__ pf_dd pf_warp_tree(pf_dd v) {
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) v = pf_dd_add(v, pf_shfl_down_dd(v, d));
+  return v;
+}
+
+#ifndef PF_EVENT_MIN_BLOCKS
+#define PF_EVENT_MIN_BLOCKS 12
+#endif
+extern "C" __global__ void __launch_bounds__(PF_EV_THREADS, PF_EVENT_MIN_BLOCKS) pf_event_kernel(pf_args a) {
+  extern __shared__ __align__(16) unsigned char pf_dyn[];
+  __shared__ __align__(8) pf_u64 bars[PF_EV_WARPS * PF_NST];
+  double* stages = reinterpret_cast<double*>(pf_dyn);
+  pf_dd* accs = reinterpret_cast<pf_dd*>(stages + PF_EV_WARPS * PF_NST * PF_STAGE);  // [k][thread]
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  double* my = stages + warp * PF_NST * PF_STAGE;
+  pf_u64* mybar = bars + warp * PF_NST;
+  if (lane == 0) {
+    for (int s = 0; s < PF_NST; ++s) pf_mbar_init(mybar + s, 1);
+    pf_fence_mbar_init();
+  }
+  pf_math_init();  // includes __syncthreads (barrier inits visible)
+  const int gw = blockIdx.x * PF_EV_WARPS + warp;
+  const int nw = gridDim.x * PF_EV_WARPS;
+  const int my_chunks = gw < a.n_chunks ? (a.n_chunks - 1 - gw) / nw + 1 : 0;
+  const int W = my_chunks * PF_NSUB;
+  // TMA producer (lane 0): sub-chunk w of this warp into stage w % PF_NST
+  auto issue = [&](int w) {
+    if (lane == 0) {
+      const int s = w % PF_NST;
+      const pf_u64 c = (pf_u64)gw + (pf_u64)(w / PF_NSUB) * (pf_u64)nw;
+      const pf_u64 base = c * (PF_SUB * PF_NSUB) + (pf_u64)(w % PF_NSUB) * PF_SUB;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      pf_mbar_expect_tx(mybar + s, PF_STAGE * 8);
+#pragma unroll
+      for (int q = 0; q < PF_NLOAD; ++q)
+        pf_tma_load(my + s * PF_STAGE + q * PF_SUB,
+                    a.data + (pf_u64)pf_load_col(q) * a.col_stride + base, PF_SUB * 8, mybar + s);
+    }
+  };
+  for (int w = 0; w < PF_NST - 1 && w < W; ++w) issue(w);
+  pf_pdl_wait();  // norms, constants and records of this call are ready
+  for (int w = 0; w < W; ++w) {
+    const int s = w % PF_NST;
+    pf_mbar_wait(mybar + s, (unsigned)((w / PF_NST) & 1));
+    const pf_u64 c = (pf_u64)gw + (pf_u64)(w / PF_NSUB) * (pf_u64)nw;
+    const pf_u64 base = c * (PF_SUB * PF_NSUB) + (pf_u64)(w % PF_NSUB) * PF_SUB;
+    const bool first = (w % PF_NSUB) == 0;
+    const bool full = base + PF_SUB <= a.n_local;
+    const int n_valid = full ? PF_SUB : (int)(a.n_local > base ? a.n_local - base : 0);
+    for (int k = 0; k < a.K; ++k) {
+      pf_dd t = full ? pf_stage_terms<true>(a, k, base, lane, my + s * PF_STAGE, n_valid)
+                     : pf_stage_terms<false>(a, k, base, lane, my + s * PF_STAGE, n_valid);
+      pf_dd* slot = accs + k * PF_EV_THREADS + threadIdx.x;
+      *slot = first ? t : pf_dd_add(*slot, t);
+    }
+    __syncwarp();
+    if (w + PF_NST - 1 < W) issue(w + PF_NST - 1);  // refills the stage read at w - 1
+    if ((w % PF_NSUB) == PF_NSUB - 1) {
+      for (int k = 0; k < a.K; ++k) {
+        pf_dd t = pf_warp_tree(accs[k * PF_EV_THREADS + threadIdx.x]);
+        if (lane == 0) a.partials[(pf_u64)k * a.n_chunks + c] = t;
+      }
+    }
+  }
+  pf_pdl_trigger();
+}
+
 // ---------------------------------------------------------------------------
-// final: the reference's pairwise tree over chunk partials, one block per k.
+// final: the reference's pairwise tree over chunk partials (engine.hpp:
+// 63-68), one block per parameter set, then publish to the host.
 extern "C" __global__ void __launch_bounds__(PF_FINAL_THREADS) pf_final_kernel(pf_args a) {
   __shared__ pf_dd sm[PF_FINAL_THREADS];
+  pf_pdl_wait();
   const int k = blockIdx.x;
-  pf_dd r = pf_pairwise_block(a.partials + (pf_u64)k * a.n_chunks, (pf_u64)a.n_chunks, sm);
-  if (threadIdx.x == 0) {
-    a.rec[k].result_hi = r.hi;
-    a.rec[k].result_lo = r.lo;
-  }
+  pf_dd t = pf_dd_zero();
+  if (a.n_chunks > 0)
+    t = pf_pairwise_block(a.partials + (pf_u64)k * a.n_chunks, (pf_u64)a.n_chunks, sm,
+                          PF_FINAL_THREADS);
+  pf_publish(a, k, t.hi, t.lo);
+}
+
+// ---------------------------------------------------------------------------
+// publish only (a shard without events)
+extern "C" __global__ void __launch_bounds__(PF_THREADS) pf_publish_kernel(pf_args a) {
+  pf_publish(a, blockIdx.x, 0.0, 0.0);
 }

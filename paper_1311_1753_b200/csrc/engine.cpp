@@ -44,6 +44,18 @@ ModuleCache& cache() {
   return *c;
 }
 
+}  // namespace
+
+// TMA stage ring (PF_EV_WARPS x PF_NST stages x PF_NLOAD x 32 PF_EPT doubles)
+// plus the per-lane double-double accumulators of K parameter sets
+size_t event_smem(const Layout& L, int K) {
+  const size_t stages = static_cast<size_t>(kEventWarps) * kEventStages * L.load_cols.size() * 32 *
+                        static_cast<size_t>(L.ept) * sizeof(double);
+  return stages + static_cast<size_t>(K) * 32 * kEventWarps * 16;
+}
+
+namespace {
+
 const Module* load_module(const Layout& L, int device) {
   ModuleCache& c = cache();
   std::lock_guard<std::mutex> lock(c.mu);
@@ -59,22 +71,38 @@ const Module* load_module(const Layout& L, int device) {
   ck(cudaSetDevice(device), "cudaSetDevice");
   ck(cudaLibraryLoadData(&m->lib, cit->second.data(), nullptr, nullptr, 0, nullptr, nullptr, 0),
      "cudaLibraryLoadData");
+  ck(cudaLibraryGetKernel(&m->setup, m->lib, "pf_setup_kernel"), "get pf_setup_kernel");
+  ck(cudaLibraryGetKernel(&m->publish, m->lib, "pf_publish_kernel"), "get pf_publish_kernel");
   ck(cudaLibraryGetKernel(&m->pre, m->lib, "pf_pre_kernel"), "get pf_pre_kernel");
   ck(cudaLibraryGetKernel(&m->norm, m->lib, "pf_norm_kernel"), "get pf_norm_kernel");
   ck(cudaLibraryGetKernel(&m->event, m->lib, "pf_event_kernel"), "get pf_event_kernel");
   ck(cudaLibraryGetKernel(&m->final, m->lib, "pf_final_kernel"), "get pf_final_kernel");
   ck(cudaKernelSetAttributeForDevice(m->event, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     kMaxBatch * 256 * 16, device),
+                                     static_cast<int>(event_smem(L, kMaxBatch)), device),
      "event kernel smem attribute");
   c.modules.emplace(key, m);
   return m;
 }
 
-void launch(cudaKernel_t k, dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args& a) {
+void launch(cudaKernel_t k, dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args& a,
+            bool pdl = false) {
   void* args[] = {&a};
-  ck(cudaLaunchKernel(reinterpret_cast<const void*>(k), grid, block, args, smem, s),
-     "cudaLaunchKernel");
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  if (pdl) {  // programmatic dependent launch: overlaps this grid's start with its predecessor
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  ck(cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(k), args), "cudaLaunchKernelEx");
 }
+
+}  // namespace
 
 // Split [lo, hi) the way the reference's pairwise tree does (engine.hpp:63-68)
 // and descend `depth` levels following the bits of `index` (MSB first).
@@ -93,15 +121,14 @@ void subtree_range(uint64_t n, int shard_count, int index, uint64_t* lo, uint64_
   *hi = b;
 }
 
-}  // namespace
-
 uint64_t kernel_launch_count() { return g_launches.load(); }
 
 std::vector<char> compile_cubin(const Layout& L, std::string* log) {
   nvrtcProgram prog;
-  const char* headers[] = {device_header_source(), kernels_header_source(), counters_header_source()};
-  const char* names[] = {"pf_device.cuh", "pf_kernels.cuh", "pf_counters.cuh"};
-  ckr(nvrtcCreateProgram(&prog, L.source.c_str(), "pf_model.cu", 3, headers, names),
+  const char* headers[] = {device_header_source(), kernels_header_source(), counters_header_source(),
+                           exp_table_header_source()};
+  const char* names[] = {"pf_device.cuh", "pf_kernels.cuh", "pf_counters.cuh", "pf_exp_table.cuh"};
+  ckr(nvrtcCreateProgram(&prog, L.source.c_str(), "pf_model.cu", 4, headers, names),
       "nvrtcCreateProgram");
   const char* opts[] = {"--gpu-architecture=sm_100a", "-lineinfo", "--std=c++17",
                         "--device-as-default-execution-space"};
@@ -154,11 +181,16 @@ Model::Model(const pf_graph& g, const pf_data& d, uint32_t grid_points, const pf
   n_chunks_total_ = (n_events_ + chunk_ - 1) / chunk_;
   const int n_cols_data = d.n_obs + (binned_ ? 2 : 0);
   build_tasks(grid_points);
+  double norm_work = 0;
+  for (const Task& t : tasks_) norm_work += static_cast<double>(t.points) * subtree_cost(pg_, t.node);
+  small_norms_ = norm_work <= kSmallNormWork;
 
   ck(cudaSetDevice(opt.device), "cudaSetDevice");
-  ck(cudaMallocHost(reinterpret_cast<void**>(&h_params_),
-                    sizeof(double) * kMaxBatch * std::max(L_.np, 1)),
-     "cudaMallocHost params");
+  // parameters and results live in mapped (zero-copy) pinned memory: the
+  // per-call graph has no memcpy nodes
+  ck(cudaHostAlloc(reinterpret_cast<void**>(&h_params_), sizeof(double) * kMaxBatch * std::max(L_.np, 1),
+                   cudaHostAllocMapped | cudaHostAllocPortable),
+     "cudaHostAlloc params");
 
   const int G = n_devices;
   const int groups = std::max(G, shard_count_);
@@ -172,7 +204,8 @@ Model::Model(const pf_graph& g, const pf_data& d, uint32_t grid_points, const pf
     sh.event_offset = std::min(sh.chunk_lo * chunk_, n_events_);
     uint64_t end = std::min(sh.chunk_hi * chunk_, n_events_);
     sh.n_local = end - sh.event_offset;
-    sh.col_stride = (sh.n_local + 31) & ~31ull;
+    // columns padded to whole chunks: every TMA stage copy stays in bounds
+    sh.col_stride = (sh.n_local + chunk_ - 1) / chunk_ * chunk_;
     ck(cudaSetDevice(sh.device), "cudaSetDevice");
     ck(cudaStreamCreateWithFlags(&sh.stream, cudaStreamNonBlocking), "cudaStreamCreate");
     sh.mod = load_module(L_, sh.device);
@@ -195,12 +228,14 @@ Model::Model(const pf_graph& g, const pf_data& d, uint32_t grid_points, const pf
     ck(cudaMalloc(&sh.d_rec, sizeof(KRec) * kMaxBatch), "cudaMalloc rec");
     ck(cudaMalloc(&sh.d_clamp, sizeof(uint64_t) * 2 * std::max(L_.n_poly, 1)), "cudaMalloc clamp");
     ck(cudaMemset(sh.d_clamp, 0, sizeof(uint64_t) * 2 * std::max(L_.n_poly, 1)), "memset clamp");
-    ck(cudaMallocHost(reinterpret_cast<void**>(&sh.h_rec), sizeof(KRec) * kMaxBatch), "pinned rec");
-    ck(cudaMallocHost(reinterpret_cast<void**>(&sh.h_norms),
-                      sizeof(double) * kMaxBatch * 3 * pg_.nodes.size()),
-       "pinned norms");
-    ck(cudaMallocHost(reinterpret_cast<void**>(&sh.h_clamp), sizeof(uint64_t) * std::max(L_.n_poly, 1)),
-       "pinned clamp");
+    ck(cudaHostAlloc(reinterpret_cast<void**>(&sh.h_out), sizeof(Out) * kMaxBatch, cudaHostAllocMapped),
+       "mapped out");
+    ck(cudaHostAlloc(reinterpret_cast<void**>(&sh.h_norms),
+                     sizeof(double) * kMaxBatch * 3 * pg_.nodes.size(), cudaHostAllocMapped),
+       "mapped norms");
+    ck(cudaHostAlloc(reinterpret_cast<void**>(&sh.h_clamp), sizeof(uint64_t) * std::max(L_.n_poly, 1),
+                     cudaHostAllocMapped),
+       "mapped clamp");
     std::memset(sh.h_clamp, 0, sizeof(uint64_t) * std::max(L_.n_poly, 1));
     // the EventTable shard, column-major with a padded stride (double2 loads)
     if (sh.n_local > 0) {
@@ -209,6 +244,18 @@ Model::Model(const pf_graph& g, const pf_data& d, uint32_t grid_points, const pf
                       sizeof(double) * n_events_, sizeof(double) * sh.n_local, n_cols_data,
                       cudaMemcpyHostToDevice),
          "upload events");
+      // padding events (masked out of every sum) sit at each observable's
+      // lower edge so no node raises a domain error on them
+      const uint64_t pad = sh.col_stride - sh.n_local;
+      if (pad > 0) {
+        std::vector<double> fill(pad);
+        for (int c = 0; c < n_cols_data; ++c) {
+          std::fill(fill.begin(), fill.end(), c < d.n_obs ? pg_.vars[d.obs[c]].lower : 0.0);
+          ck(cudaMemcpy(sh.d_data + c * sh.col_stride + sh.n_local, fill.data(), sizeof(double) * pad,
+                        cudaMemcpyHostToDevice),
+             "pad events");
+        }
+      }
     }
   }
 }
@@ -226,9 +273,10 @@ Model::~Model() {
     cudaFree(sh.d_partials);
     cudaFree(sh.d_rec);
     cudaFree(sh.d_clamp);
-    cudaFreeHost(sh.h_rec);
+    cudaFreeHost(sh.h_out);
     cudaFreeHost(sh.h_norms);
     cudaFreeHost(sh.h_clamp);
+    cudaFree(sh.d_scratch);
   }
   cudaFreeHost(h_params_);
 }
@@ -279,6 +327,7 @@ void Model::build_tasks(uint32_t grid_points) {
         }
         t.per_block = per;
         t.n_blocks = static_cast<int>(nb);
+        t.level = static_cast<int>(lvl);
         t.first_block = blocks;
         t.partial_offset = blocks;
         blocks += t.n_blocks;
@@ -291,13 +340,17 @@ void Model::build_tasks(uint32_t grid_points) {
   }
 }
 
-cudaGraphExec_t Model::graph_for(Shard& sh, int K) {
-  auto it = sh.graphs.find(K);
-  if (it != sh.graphs.end()) return it->second;
-  ck(cudaSetDevice(sh.device), "cudaSetDevice");
-  const size_t np = std::max(L_.np, 1);
+Args Model::base_args(Shard& sh, int K) {
   Args a;
   std::memset(&a, 0, sizeof a);
+  ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(const_cast<double**>(&a.hP)), h_params_, 0),
+     "mapped params");
+  ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&a.hout), sh.h_out, 0), "mapped out");
+  ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&a.hnorms), sh.h_norms, 0), "mapped norms");
+  ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&a.hclamp), sh.h_clamp, 0), "mapped clamp");
+  a.n_nodes = static_cast<int>(pg_.nodes.size());
+  a.fuse_final = K == 1 ? 1 : 0;
+  a.n_levels = static_cast<int>(L_.level_nodes.size());
   a.data = sh.d_data;
   a.col_stride = sh.col_stride;
   a.n_local = sh.n_local;
@@ -307,46 +360,59 @@ cudaGraphExec_t Model::graph_for(Shard& sh, int K) {
   a.P = sh.d_P;
   a.S = sh.d_S;
   a.C = sh.d_C;
+  a.tasks = sh.d_tasks;
+  a.n_tasks = static_cast<int>(tasks_.size());
   a.partials = sh.d_partials;
   a.rec = sh.d_rec;
-  // norm-stage clamps are counted once (shard 0); the others discard them
-  uint64_t* norm_clamp = (&sh == &shards_[0] && shard_index_ == 0) ? sh.d_clamp
-                                                                     : sh.d_clamp + std::max(L_.n_poly, 1);
   a.total_content = total_content_;
+  // norm-stage clamps are counted once (shard 0); the others discard them
+  const bool counts_norm = (&sh == &shards_[0]) && shard_index_ == 0;
+  a.clamp = counts_norm ? sh.d_clamp : sh.d_clamp + std::max(L_.n_poly, 1);
+  return a;
+}
+
+// One call = one graph:  setup (or pre + norm levels) --PDL--> event pass
+// (+ fused final tree for K = 1, or a final kernel with one block per k).
+cudaGraphExec_t Model::graph_for(Shard& sh, int K) {
+  auto it = sh.graphs.find(K);
+  if (it != sh.graphs.end()) return it->second;
+  ck(cudaSetDevice(sh.device), "cudaSetDevice");
+  Args a = base_args(sh, K);
   int kernels = 0;
   cudaGraph_t graph;
   ck(cudaStreamBeginCapture(sh.stream, cudaStreamCaptureModeThreadLocal), "begin capture");
-  ck(cudaMemcpyAsync(sh.d_P, h_params_, sizeof(double) * K * np, cudaMemcpyHostToDevice, sh.stream),
-     "capture H2D params");
-  a.clamp = norm_clamp;
-  launch(sh.mod->pre, dim3(K), dim3(256), 0, sh.stream, a);
-  ++kernels;
-  for (size_t lvl = 0; lvl < L_.level_nodes.size(); ++lvl) {
-    Args b = a;
-    b.level = static_cast<int>(lvl);
-    b.n_tasks = level_n_tasks_[lvl];
-    b.tasks = sh.d_tasks + level_first_task_[lvl];
-    launch(sh.mod->norm, dim3(level_blocks_[lvl], K), dim3(256), 0, sh.stream, b);
+  if (small_norms_) {
+    launch(sh.mod->setup, dim3(K), dim3(1024), 0, sh.stream, a);
+    ++kernels;
+  } else {
+    launch(sh.mod->pre, dim3(K), dim3(256), 0, sh.stream, a);
+    ++kernels;
+    for (size_t lvl = 0; lvl < L_.level_nodes.size(); ++lvl) {
+      Args b = a;
+      b.level = static_cast<int>(lvl);
+      b.n_tasks = level_n_tasks_[lvl];
+      b.tasks = sh.d_tasks + level_first_task_[lvl];
+      launch(sh.mod->norm, dim3(level_blocks_[lvl], K), dim3(256), 0, sh.stream, b);
+      ++kernels;
+    }
+  }
+  Args e = a;
+  e.clamp = sh.d_clamp;
+  if (sh.n_local > 0) {
+    // one warp per chunk, 2-warp blocks: the block scheduler balances SMs
+    const int grid = std::max(1, (sh.n_chunks + kEventWarps - 1) / kEventWarps);
+    const size_t smem = event_smem(L_, K);
+    launch(sh.mod->event, dim3(grid), dim3(32 * kEventWarps), smem, sh.stream, e, /*pdl=*/true);
+    launch(sh.mod->final, dim3(K), dim3(1024), 0, sh.stream, e, /*pdl=*/true);
+    kernels += 2;
+    if (K == 1) {
+      sh.event_args = e;
+      sh.event_grid = grid;
+    }
+  } else {
+    launch(sh.mod->publish, dim3(K), dim3(256), 0, sh.stream, e);
     ++kernels;
   }
-  if (sh.n_local > 0) {
-    Args e = a;
-    e.clamp = sh.d_clamp;
-    const int grid = std::max(1, std::min(sh.n_chunks, 148 * 16));
-    launch(sh.mod->event, dim3(grid), dim3(256), static_cast<size_t>(K) * 256 * 16, sh.stream, e);
-    launch(sh.mod->final, dim3(K), dim3(1024), 0, sh.stream, e);
-    kernels += 2;
-  }
-  ck(cudaMemcpyAsync(sh.h_rec, sh.d_rec, sizeof(KRec) * K, cudaMemcpyDeviceToHost, sh.stream),
-     "capture D2H rec");
-  const size_t nn = pg_.nodes.size();
-  ck(cudaMemcpy2DAsync(sh.h_norms, sizeof(double) * 3 * nn, sh.d_S, sizeof(double) * L_.ss,
-                       sizeof(double) * 3 * nn, K, cudaMemcpyDeviceToHost, sh.stream),
-     "capture D2H norms");
-  if (L_.n_poly > 0)
-    ck(cudaMemcpyAsync(sh.h_clamp, sh.d_clamp, sizeof(uint64_t) * L_.n_poly, cudaMemcpyDeviceToHost,
-                       sh.stream),
-       "capture D2H clamp");
   ck(cudaStreamEndCapture(sh.stream, &graph), "end capture");
   cudaGraphExec_t exec;
   ck(cudaGraphInstantiate(&exec, graph, 0), "cudaGraphInstantiate");
@@ -413,9 +479,9 @@ void Model::run(const double* params, int K, std::vector<Raw>& out, bool partial
     uint32_t norm_err = ~0u;
     uint64_t ev_err = ~0ull, nonfinite = ~0ull;
     for (Shard& sh : shards_) {
-      norm_err = std::min(norm_err, sh.h_rec[k].norm_error);
-      ev_err = std::min(ev_err, sh.h_rec[k].first_event_error);
-      nonfinite = std::min(nonfinite, sh.h_rec[k].first_nonfinite);
+      norm_err = std::min(norm_err, sh.h_out[k].norm_error);
+      ev_err = std::min(ev_err, sh.h_out[k].first_event_error);
+      nonfinite = std::min(nonfinite, sh.h_out[k].first_nonfinite);
     }
     if (norm_err != ~0u) {  // refresh_normalizations threw (engine.hpp:174-178)
       out[k].penalty = true;
@@ -430,12 +496,12 @@ void Model::run(const double* params, int K, std::vector<Raw>& out, bool partial
       norm_valid_[i] = 1;
     }
     if (ev_err != ~0ull) throw Error("event-error", error_message(static_cast<uint32_t>(ev_err & 0xffffff)));
-    for (Shard& sh : shards_) floor_total_ += sh.h_rec[k].floor_count;
+    for (Shard& sh : shards_) floor_total_ += sh.h_out[k].floor_count;
     // shard partials combined by the top levels of the pairwise tree
     std::vector<double> parts;
     for (Shard& sh : shards_) {
-      parts.push_back(sh.n_local > 0 ? sh.h_rec[k].result_hi : 0.0);
-      parts.push_back(sh.n_local > 0 ? sh.h_rec[k].result_lo : 0.0);
+      parts.push_back(sh.n_local > 0 ? sh.h_out[k].result_hi : 0.0);
+      parts.push_back(sh.n_local > 0 ? sh.h_out[k].result_lo : 0.0);
     }
     if (partial_only || shards_.size() == 1) {
       out[k].hi = parts[0];
@@ -536,6 +602,66 @@ void Model::norms(double* norms, double* errs, int32_t* valid, int n) const {
     if (errs) errs[i] = errs_[i];
     if (valid) valid[i] = norm_valid_[i];
   }
+}
+
+}  // namespace pfb
+
+namespace pfb {
+
+// Device timing with CUDA events on the shard-0 stream (pfb200.h pf_bench).
+BenchResult Model::bench(const double* params, size_t n, int metric, int steps, bool flush) {
+  BenchResult r;
+  r.metric = eval(params, n, metric, nullptr);  // builds the K = 1 graph
+  Shard& sh = shards_[0];
+  ck(cudaSetDevice(sh.device), "cudaSetDevice");
+  const size_t scratch_bytes = 256ull << 20;
+  if (flush && !sh.d_scratch) ck(cudaMalloc(&sh.d_scratch, scratch_bytes), "cudaMalloc scratch");
+  cudaEvent_t e0, e1;
+  ck(cudaEventCreate(&e0), "cudaEventCreate");
+  ck(cudaEventCreate(&e1), "cudaEventCreate");
+  cudaGraphExec_t g = graph_for(sh, 1);
+  double sum = 0, mn = 1e300;
+  const uint64_t launches0 = g_launches.load();
+  for (int i = 0; i < steps; ++i) {
+    if (flush) ck(cudaMemsetAsync(sh.d_scratch, i & 0xff, scratch_bytes, sh.stream), "flush");
+    ck(cudaEventRecord(e0, sh.stream), "record");
+    ck(cudaGraphLaunch(g, sh.stream), "cudaGraphLaunch");
+    ck(cudaEventRecord(e1, sh.stream), "record");
+    ck(cudaEventSynchronize(e1), "sync");
+    g_launches += sh.kernels_per_graph;
+    float ms = 0;
+    ck(cudaEventElapsedTime(&ms, e0, e1), "elapsed");
+    sum += ms;
+    mn = std::min(mn, static_cast<double>(ms));
+  }
+  r.kernels_per_step = steps ? (g_launches.load() - launches0) / steps : 0;
+  r.step_ms_mean = steps ? sum / steps : 0;
+  r.step_ms_min = steps ? mn : 0;
+  sum = 0;
+  mn = 1e300;
+  if (sh.n_local > 0) {
+    for (int i = 0; i < steps; ++i) {
+      if (flush) ck(cudaMemsetAsync(sh.d_scratch, i & 0xff, scratch_bytes, sh.stream), "flush");
+      Args a = sh.event_args;
+      ck(cudaEventRecord(e0, sh.stream), "record");
+      launch(sh.mod->event, dim3(sh.event_grid), dim3(32 * kEventWarps), event_smem(L_, 1), sh.stream,
+             a, false);
+      ck(cudaEventRecord(e1, sh.stream), "record");
+      ck(cudaEventSynchronize(e1), "sync");
+      ++g_launches;
+      float ms = 0;
+      ck(cudaEventElapsedTime(&ms, e0, e1), "elapsed");
+      sum += ms;
+      mn = std::min(mn, static_cast<double>(ms));
+    }
+  }
+  r.event_ms_mean = steps ? sum / steps : 0;
+  r.event_ms_min = steps ? mn : 0;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  r.h2d_bytes = sizeof(double) * std::max(L_.np, 1);
+  r.d2h_bytes = sizeof(Out) + sizeof(double) * 3 * pg_.nodes.size() + sizeof(uint64_t) * L_.n_poly;
+  return r;
 }
 
 }  // namespace pfb

@@ -17,6 +17,9 @@ namespace pfb {
 
 constexpr double kPenaltyValue = 1e300;  // engine.hpp:52
 constexpr int kMaxBatch = 32;            // parameter sets per launch
+constexpr int kEventWarps = 2;           // warps per event-pass block (PF_EV_WARPS)
+constexpr int kEventStages = 3;          // TMA stages per warp (PF_NST)
+constexpr double kSmallNormWork = 65536; // raw evaluations: single-CTA setup path
 
 // host mirrors of the device structs (pf_device.cuh); layouts must match
 struct KRec {
@@ -31,7 +34,7 @@ static_assert(sizeof(KRec) == 104, "pf_krec layout");
 
 struct Task {
   int node, n, dims, first_block;
-  int n_blocks, partial_offset, fine, pad;
+  int n_blocks, partial_offset, fine, level;
   uint64_t points, per_block;
   double lo[8];
   double h[8];
@@ -39,7 +42,22 @@ struct Task {
 };
 static_assert(sizeof(Task) == 184, "pf_task layout");
 
+struct Out {
+  double result_hi, result_lo;
+  uint64_t floor_count, first_nonfinite, first_event_error;
+  uint32_t norm_error, pad;
+};
+static_assert(sizeof(Out) == 48, "pf_out layout");
+
 struct Args {
+  const double* hP;
+  Out* hout;
+  double* hnorms;
+  uint64_t* hclamp;
+  int n_nodes;
+  int fuse_final;
+  int n_levels;
+  int pad0;
   const double* data;
   uint64_t col_stride;
   uint64_t n_local;
@@ -60,7 +78,8 @@ struct Args {
 
 struct Module {
   cudaLibrary_t lib = nullptr;
-  cudaKernel_t pre = nullptr, norm = nullptr, event = nullptr, final = nullptr;
+  cudaKernel_t setup = nullptr, pre = nullptr, norm = nullptr, event = nullptr, final = nullptr,
+               publish = nullptr;
 };
 
 // NVRTC compile of (library headers + generated source) for sm_100a.
@@ -80,13 +99,24 @@ struct Shard {
   Task* d_tasks = nullptr;  // all levels, concatenated
   void* d_partials = nullptr;
   KRec* d_rec = nullptr;
-  uint64_t* d_clamp = nullptr;
-  KRec* h_rec = nullptr;       // pinned
-  double* h_norms = nullptr;   // pinned, K x 3 n_nodes
-  uint64_t* h_clamp = nullptr; // pinned
+  uint64_t* d_clamp = nullptr;  // [n_poly counted | n_poly discarded]
+  Out* h_out = nullptr;         // mapped, kMaxBatch
+  double* h_norms = nullptr;    // mapped, kMaxBatch x 3 n_nodes
+  uint64_t* h_clamp = nullptr;  // mapped
   std::map<int, cudaGraphExec_t> graphs;
   int kernels_per_graph = 0;
+  Args event_args{};  // K = 1 event-pass arguments (timing)
+  int event_grid = 1;
+  void* d_scratch = nullptr;  // L2 flush buffer (bench only)
 };
+
+struct BenchResult {
+  double step_ms_mean = 0, step_ms_min = 0, event_ms_mean = 0, event_ms_min = 0, metric = 0;
+  uint64_t kernels_per_step = 0, h2d_bytes = 0, d2h_bytes = 0;
+};
+
+void subtree_range(uint64_t n, int shard_count, int index, uint64_t* lo, uint64_t* hi);
+size_t event_smem(const Layout& L, int K);
 
 class Model {
  public:
@@ -101,10 +131,12 @@ class Model {
   void eval_batch(const double* params, size_t K, size_t n, int metric, double* out);
   // this process's shard partial (shard_count > 1)
   void eval_partial(const double* params, size_t n, int metric, double* hi_lo, int* penalty);
+  BenchResult bench(const double* params, size_t n, int metric, int steps, bool flush);
 
   const Program& program() const { return pg_; }
   const Layout& layout() const { return L_; }
   uint64_t n_events() const { return n_events_; }
+  uint64_t chunk() const { return chunk_; }
   bool binned() const { return binned_; }
   uint64_t floor_count() const { return floor_total_; }
   uint64_t clamp_count(int node) const;
@@ -119,6 +151,7 @@ class Model {
   bool params_valid(const double* p) const;
   void run(const double* params, int K, std::vector<Raw>& out, bool partial_only);
   cudaGraphExec_t graph_for(Shard& s, int K);
+  Args base_args(Shard& s, int K);
   void build_tasks(uint32_t grid_points);
   std::string error_message(uint32_t code_node) const;
 
@@ -129,11 +162,12 @@ class Model {
   double total_content_ = 0;
   uint64_t chunk_ = 0, n_chunks_total_ = 0;
   int shard_count_ = 1, shard_index_ = 0;
+  bool small_norms_ = true;
   std::vector<Shard> shards_;
-  std::vector<Task> tasks_;              // host copy, all levels
+  std::vector<Task> tasks_;  // host copy, all levels
   std::vector<int> level_first_task_, level_n_tasks_, level_blocks_;
   int max_norm_blocks_ = 0;
-  double* h_params_ = nullptr;  // pinned, kMaxBatch x np
+  double* h_params_ = nullptr;  // mapped, kMaxBatch x np
   uint64_t floor_total_ = 0;
   std::vector<uint64_t> clamp_total_;
   std::vector<double> norms_, errs_;
