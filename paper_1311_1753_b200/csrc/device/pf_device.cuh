@@ -20,6 +20,7 @@ typedef unsigned int pf_u32;
 #define PF_CHISQ_EPS 1e-9     // engine.hpp:51 kChiSqEps
 #define PF_MAX_BOX 8
 #define PF_MAX_LEVELS 14
+#define PF_MAX_INLINE 64  // parameters passed inline in the kernel arguments
 
 // error codes, mirrored by engine.cpp's message table
 #define PF_E_NONPOS_SIGMA 1   // pdf.hpp:256-257
@@ -85,6 +86,12 @@ struct pf_args {
   pf_krec* rec;         // K records
   pf_u64* clamp;        // cumulative PolynomialPdf clamp counters per node
   double total_content; // binned: N_tot (engine.hpp:153)
+  pf_dd* gpartials;     // K x n_groups (groups of 32 chunks)
+  pf_u32* gcount;       // per-group ticket counters (self-resetting)
+  pf_u32* done;         // closed-group counter (self-resetting)
+  int npin;             // K = 1: parameters passed inline (pin[0..npin))
+  int pad1;
+  double pin[PF_MAX_INLINE];
 };
 
 // ----------------------------------------------------------------------------
@@ -191,49 +198,54 @@ __device__ __forceinline__ pf_dd pf_block_reduce(pf_dd v, pf_dd* sm) {
 // recursive pairwise tree that splits [lo, hi) at lo + (hi - lo) / 2.  An
 // empty range is 0 and x + 0 == x exactly, so padding the top of the tree
 // with empty subtrees leaves every value unchanged.
+//
+// Stack-free sequential evaluation: the tree over [lo, hi) is embedded in the
+// complete binary tree of depth s = ceil(log2 m); virtual leaf p (descend s
+// levels by the bits of p) is an element or empty, and a binary-counter merge
+// over the 2^s virtual leaves forms every node as left + right.
 __device__ pf_dd pf_pairwise_seq(const pf_dd* v, pf_u64 lo, pf_u64 hi) {
-  // iterative post-order walk with an explicit stack (depth <= 64)
-  if (hi <= lo) return pf_dd_zero();
-  pf_u64 slo[64], shi[64];
-  pf_dd sval[64];
-  int sstate[64];
-  int sp = 0;
-  slo[0] = lo;
-  shi[0] = hi;
-  sstate[0] = 0;
-  pf_dd ret = pf_dd_zero();
-  while (sp >= 0) {
-    pf_u64 l = slo[sp], h = shi[sp];
-    if (h - l == 1) {
-      ret = v[l];
-      --sp;
-      continue;
+  const pf_u64 m = hi > lo ? hi - lo : 0;
+  if (m == 0) return pf_dd_zero();
+  if (m == 1) return v[lo];
+  const int s = 64 - __clzll(m - 1);
+  pf_dd stk[40];
+  int top = 0;
+  for (pf_u64 p = 0; p < (1ull << s); ++p) {
+    pf_u64 a = lo, b = hi;
+    for (int lev = 0; lev < s; ++lev) {
+      const pf_u64 mid = a + (b - a) / 2;
+      if ((p >> (s - 1 - lev)) & 1)
+        a = mid;
+      else
+        b = mid;
     }
-    if (h == l) {
-      ret = pf_dd_zero();
-      --sp;
-      continue;
-    }
-    pf_u64 mid = l + (h - l) / 2;
-    if (sstate[sp] == 0) {
-      sstate[sp] = 1;
-      ++sp;
-      slo[sp] = l;
-      shi[sp] = mid;
-      sstate[sp] = 0;
-    } else if (sstate[sp] == 1) {
-      sval[sp] = ret;  // left value
-      sstate[sp] = 2;
-      ++sp;
-      slo[sp] = mid;
-      shi[sp] = h;
-      sstate[sp] = 0;
-    } else {
-      ret = pf_dd_add(sval[sp], ret);
-      --sp;
-    }
+    pf_dd x = (b - a == 1) ? v[a] : pf_dd_zero();
+    for (pf_u64 q = p; q & 1; q >>= 1) x = pf_dd_add(stk[--top], x);
+    stk[top++] = x;
   }
-  return ret;
+  return stk[0];
+}
+
+// The same tree evaluated by one warp: lane l owns the subtree at depth 5
+// selected by the bits of l; sibling lanes combine as (2i, 2i+1) pairs.
+// All 32 lanes must call; the result is valid in lane 0.
+__device__ pf_dd pf_pairwise_warp(const pf_dd* v, pf_u64 n) {
+  const int lane = threadIdx.x & 31;
+  pf_u64 a = 0, b = n;
+  for (int lev = 0; lev < 5; ++lev) {
+    const pf_u64 mid = a + (b - a) / 2;
+    if ((lane >> (4 - lev)) & 1)
+      a = mid;
+    else
+      b = mid;
+  }
+  pf_dd x = pf_pairwise_seq(v, a, b);
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const pf_dd o = pf_shfl_down_dd(x, d);
+    if ((lane & (2 * d - 1)) == 0) x = pf_dd_add(x, o);
+  }
+  return x;
 }
 
 // Block-parallel evaluation of the same tree with nthreads = 2^d threads:

@@ -33,7 +33,7 @@ __device__ __forceinline__ void pf_rec_init(pf_krec* r) {
 
 __device__ __forceinline__ void pf_load_params(const pf_args& a, int k) {
   for (int i = threadIdx.x; i < PF_NP; i += blockDim.x)
-    ((double*)a.P)[(pf_u64)k * PF_NP + i] = a.hP[(pf_u64)k * PF_NP + i];
+    ((double*)a.P)[(pf_u64)k * PF_NP + i] = a.npin ? a.pin[i] : a.hP[(pf_u64)k * PF_NP + i];
 }
 
 // Richardson combination of a node's (coarse, fine) sums (pdf.hpp:178-188)
@@ -69,56 +69,116 @@ __device__ void pf_publish(const pf_args& a, int k, double hi, double lo) {
 #endif
 }
 
+#define PF_SETUP_THREADS 512  // 128 registers: the level's 8 reductions interleave unspilled
+
 // ---------------------------------------------------------------------------
 // setup: parameters H2D, call records, pre stage and EVERY normalisation
 // level in one CTA per parameter set (small grids).  Midpoint sums at n and
 // 2n (pdf.hpp:148-176): thread t sums points t, t + 1024, ... in double-
 // double; a fixed-shape block reduction combines the 1024 partials.
-extern "C" __global__ void __launch_bounds__(PF_FINAL_THREADS) pf_setup_kernel(pf_args a) {
-  __shared__ pf_dd sm[PF_FINAL_THREADS];
-  __shared__ double sums[64];
+extern "C" __global__ void __launch_bounds__(PF_SETUP_THREADS) pf_setup_kernel(const __grid_constant__ pf_args a) {
+  // parameters and the per-call state live in shared memory while the CTA
+  // works (every S read/write is an LDS/STS, not an L2 round trip); the task
+  // table is staged too.  The state is written to global memory at the end.
+  extern __shared__ __align__(16) double pf_sdyn[];
+  __shared__ pf_dd wsum[8][32];
+  __shared__ double sums[8];
+  __shared__ pf_task tk[16];
   pf_pdl_trigger();  // let the event kernel start streaming its data now
-  pf_math_init();
+#ifdef PF_SETUP_TRACE
+  __shared__ long long trs[32];
+  __shared__ const char* trn[32];
+  int ntr = 0;
+  long long tr0 = clock64();
+#define PF_TRACE(tag) if (threadIdx.x == 0 && ntr < 32) { trs[ntr] = clock64() - tr0; trn[ntr++] = tag; }
+#else
+#define PF_TRACE(tag)
+#endif
   const int k = blockIdx.x;
+  double* P = pf_sdyn;
+  double* S = pf_sdyn + PF_NP;
+  // K = 1: parameters arrive inline in the kernel arguments (constant bank,
+  // updated per call on the instantiated graph); batches read mapped memory
+  for (int i = threadIdx.x; i < PF_NP; i += blockDim.x)
+    P[i] = a.npin ? a.pin[i] : a.hP[(pf_u64)k * PF_NP + i];
+  for (int i = threadIdx.x; i < PF_SS; i += blockDim.x) S[i] = 0.0;
+  const int nt = min(a.n_tasks, 16);
+  for (int i = threadIdx.x; i < nt * (int)(sizeof(pf_task) / 8); i += blockDim.x)
+    reinterpret_cast<pf_u64*>(tk)[i] = reinterpret_cast<const pf_u64*>(a.tasks)[i];
   pf_krec* r = a.rec + k;
-  pf_load_params(a, k);
   if (threadIdx.x == 0) pf_rec_init(r);
-  __syncthreads();
-  const double* P = a.P + (pf_u64)k * PF_NP;
-  double* S = a.S + (pf_u64)k * PF_SS;
+  pf_math_init();  // includes __syncthreads
+  PF_TRACE("init");
   pf_ctx cx;
   cx.err = 0;
   pf_cnt cnt;
   pf_cnt_init(cnt);
   pf_stage_pre(k, P, S, a.C, cx, cnt, threadIdx.x, blockDim.x);
+  PF_TRACE("pre");
   int t0 = 0;
   for (int level = 0; level < a.n_levels; ++level) {
     int t1 = t0;
-    while (t1 < a.n_tasks && a.tasks[t1].level == level) ++t1;
-    for (int t = t0; t < t1; ++t) {
-      const pf_task& T = a.tasks[t];
+    while (t1 < nt && tk[t1].level == level) ++t1;
+    const int nl = min(t1 - t0, 8);
+    // every midpoint sum of the level first (thread t: points t, t + 1024, ...)
+    pf_dd accl[8];
+    for (int q = 0; q < nl; ++q) {
+      const pf_task& T = tk[t0 + q];
       pf_dd acc = pf_dd_zero();
-      for (pf_u64 i = threadIdx.x; i < T.points; i += PF_FINAL_THREADS)
+      for (pf_u64 i = threadIdx.x; i < T.points; i += PF_SETUP_THREADS)
         acc = pf_dd_add_d(acc, pf_norm_point(T.node, i, T, P, S, a.C, cx, cnt));
-      pf_dd s = pf_block_reduce(acc, sm);
+      accl[q] = acc;
+    }
+    // then all of the level's fixed-shape block reductions together, so
+    // their double-double latency chains overlap (warp trees, then one
+    // warp per sum over the 32 warp results)
+    pf_dd x[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) x[q] = q < nl ? accl[q] : pf_dd_zero();
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (q < nl) x[q] = pf_dd_add(x[q], pf_shfl_down_dd(x[q], d));
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0)
+      for (int q = 0; q < nl; ++q) wsum[q][warp] = x[q];
+    __syncthreads();
+    if (warp < nl) {
+      pf_dd y = lane < PF_SETUP_THREADS / 32 ? wsum[warp][lane] : pf_dd_zero();
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) y = pf_dd_add(y, pf_shfl_down_dd(y, d));
       // midpoint_sum returns static_cast<double>(sum) * vol (pdf.hpp:173-175)
-      if (threadIdx.x == 0) sums[t - t0] = __dmul_rn(pf_dd_to_double(s), T.vol);
+      if (lane == 0) sums[warp] = __dmul_rn(pf_dd_to_double(y), tk[t0 + warp].vol);
     }
     __syncthreads();
+    PF_TRACE("sums");
     if (threadIdx.x == 0)
-      for (int t = t0; t + 1 < t1; t += 2)
-        pf_finish_norm(S, r, a.tasks[t].node, sums[t - t0], sums[t + 1 - t0]);
+      for (int t = 0; t + 1 < nl; t += 2) pf_finish_norm(S, r, tk[t0 + t].node, sums[t], sums[t + 1]);
     __syncthreads();
+    PF_TRACE("finish");
     pf_stage_post(level, k, P, S, a.C, cx, cnt, threadIdx.x, blockDim.x);
+    PF_TRACE("post");
     t0 = t1;
   }
   if (cx.err) atomicMin(&r->norm_error, cx.err);
   pf_cnt_flush(cnt, a.clamp);
+  __syncthreads();
+  double* gS = a.S + (pf_u64)k * PF_SS;
+  double* gP = (double*)a.P + (pf_u64)k * PF_NP;
+  for (int i = threadIdx.x; i < PF_SS; i += blockDim.x) gS[i] = S[i];
+  for (int i = threadIdx.x; i < PF_NP; i += blockDim.x) gP[i] = P[i];
+  PF_TRACE("store");
+#ifdef PF_SETUP_TRACE
+  if (threadIdx.x == 0 && blockIdx.x == 0)
+    for (int i = 0; i < ntr; ++i) printf("setup %-8s %lld\n", trn[i], trs[i]);
+#endif
 }
 
 // ---------------------------------------------------------------------------
 // pre (large grids): parameters, call records and the pre stage.
-extern "C" __global__ void __launch_bounds__(PF_THREADS) pf_pre_kernel(pf_args a) {
+extern "C" __global__ void __launch_bounds__(PF_THREADS) pf_pre_kernel(const __grid_constant__ pf_args a) {
   pf_math_init();
   const int k = blockIdx.x;
   pf_krec* r = a.rec + k;
@@ -139,7 +199,7 @@ extern "C" __global__ void __launch_bounds__(PF_THREADS) pf_pre_kernel(pf_args a
 // norm (large grids): one level, many blocks per midpoint sum; the last
 // block to arrive combines the block partials, applies Richardson and runs
 // the post stage.
-extern "C" __global__ void __launch_bounds__(PF_THREADS) pf_norm_kernel(pf_args a) {
+extern "C" __global__ void __launch_bounds__(PF_THREADS) pf_norm_kernel(const __grid_constant__ pf_args a) {
   __shared__ pf_dd sm[PF_THREADS];
   __shared__ int s_last;
   __shared__ double sums[64];
@@ -346,6 +406,70 @@ __device__ __forceinline__ pf_dd pf_stage_terms(const pf_args& a, int k, pf_u64 
 #endif
 }
 
+// Publish from ONE warp (the warp that closed the last group).
+__device__ void pf_publish_warp(const pf_args& a, int k, pf_dd r) {
+  const int lane = threadIdx.x & 31;
+  const pf_krec* rc = a.rec + k;
+  pf_out* o = a.hout + k;
+  if (lane == 0) {
+    o->result_hi = r.hi;
+    o->result_lo = r.lo;
+    o->floor_count = rc->floor_count;
+    o->first_nonfinite = rc->first_nonfinite;
+    o->first_event_error = rc->first_event_error;
+    o->norm_error = rc->norm_error;
+  }
+  const double* S = a.S + (pf_u64)k * PF_SS;
+  for (int i = lane; i < 3 * a.n_nodes; i += 32) a.hnorms[(pf_u64)k * 3 * a.n_nodes + i] = S[i];
+#if PF_NPOLY > 0
+  if (k == a.K - 1)
+    for (int i = lane; i < PF_NPOLY; i += 32) a.hclamp[i] = a.clamp[i];
+#endif
+}
+
+// Reduction above the chunks, inside the event pass (no final kernel):
+//   group  = 32 consecutive chunks, a complete binary tree over 32 slots
+//            with (2i, 2i+1) siblings, closed by the last warp to finish one
+//            of its chunks (ticket counter, self-resetting);
+//   top    = the reference's pairwise tree (engine.hpp:63-68) over groups,
+//            run by the warp that closes the last group, which publishes.
+// Shards are whole subtrees of the top tree, so the value is independent of
+// the number of devices.
+__device__ void pf_close_chunk(const pf_args& a, int c) {
+  const int lane = threadIdx.x & 31;
+  const int g = c >> 5;
+  const int n_groups = (a.n_chunks + 31) >> 5;
+  const int gsize = min(32, a.n_chunks - 32 * g);
+  unsigned last = 0;
+  __threadfence();
+  if (lane == 0) last = atomicAdd(a.gcount + g, 1u) == (unsigned)(gsize - 1);
+  last = __shfl_sync(0xffffffffu, last, 0);
+  if (!last) return;
+  __threadfence();
+  if (lane == 0) a.gcount[g] = 0u;
+  for (int k = 0; k < a.K; ++k) {
+    const int cc = 32 * g + lane;
+    pf_dd x = cc < a.n_chunks ? a.partials[(pf_u64)k * a.n_chunks + cc] : pf_dd_zero();
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const pf_dd o = pf_shfl_down_dd(x, d);
+      if ((lane & (2 * d - 1)) == 0) x = pf_dd_add(x, o);
+    }
+    if (lane == 0) a.gpartials[(pf_u64)k * n_groups + g] = x;
+  }
+  __threadfence();
+  unsigned final_warp = 0;
+  if (lane == 0) final_warp = atomicAdd(a.done, 1u) == (unsigned)(n_groups - 1);
+  final_warp = __shfl_sync(0xffffffffu, final_warp, 0);
+  if (!final_warp) return;
+  __threadfence();
+  if (lane == 0) *a.done = 0u;
+  for (int k = 0; k < a.K; ++k) {
+    const pf_dd r = pf_pairwise_warp(a.gpartials + (pf_u64)k * n_groups, (pf_u64)n_groups);
+    pf_publish_warp(a, k, r);
+  }
+}
+
 __device__ __forceinline__ pf_dd pf_warp_tree(pf_dd v) {
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) v = pf_dd_add(v, pf_shfl_down_dd(v, d));
@@ -355,7 +479,7 @@ __device__ __forceinline__ pf_dd pf_warp_tree(pf_dd v) {
 #ifndef PF_EVENT_MIN_BLOCKS
 #define PF_EVENT_MIN_BLOCKS 12
 #endif
-extern "C" __global__ void __launch_bounds__(PF_EV_THREADS, PF_EVENT_MIN_BLOCKS) pf_event_kernel(pf_args a) {
+extern "C" __global__ void __launch_bounds__(PF_EV_THREADS, PF_EVENT_MIN_BLOCKS) pf_event_kernel(const __grid_constant__ pf_args a) {
   extern __shared__ __align__(16) unsigned char pf_dyn[];
   __shared__ __align__(8) pf_u64 bars[PF_EV_WARPS * PF_NST];
   double* stages = reinterpret_cast<double*>(pf_dyn);
@@ -410,15 +534,15 @@ extern "C" __global__ void __launch_bounds__(PF_EV_THREADS, PF_EVENT_MIN_BLOCKS)
         pf_dd t = pf_warp_tree(accs[k * PF_EV_THREADS + threadIdx.x]);
         if (lane == 0) a.partials[(pf_u64)k * a.n_chunks + c] = t;
       }
+      pf_close_chunk(a, (int)c);
     }
   }
-  pf_pdl_trigger();
 }
 
 // ---------------------------------------------------------------------------
 // final: the reference's pairwise tree over chunk partials (engine.hpp:
 // 63-68), one block per parameter set, then publish to the host.
-extern "C" __global__ void __launch_bounds__(PF_FINAL_THREADS) pf_final_kernel(pf_args a) {
+extern "C" __global__ void __launch_bounds__(PF_FINAL_THREADS) pf_final_kernel(const __grid_constant__ pf_args a) {
   __shared__ pf_dd sm[PF_FINAL_THREADS];
   pf_pdl_wait();
   const int k = blockIdx.x;
@@ -431,6 +555,6 @@ extern "C" __global__ void __launch_bounds__(PF_FINAL_THREADS) pf_final_kernel(p
 
 // ---------------------------------------------------------------------------
 // publish only (a shard without events)
-extern "C" __global__ void __launch_bounds__(PF_THREADS) pf_publish_kernel(pf_args a) {
+extern "C" __global__ void __launch_bounds__(PF_THREADS) pf_publish_kernel(const __grid_constant__ pf_args a) {
   pf_publish(a, blockIdx.x, 0.0, 0.0);
 }

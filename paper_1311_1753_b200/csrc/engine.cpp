@@ -183,7 +183,7 @@ Model::Model(const pf_graph& g, const pf_data& d, uint32_t grid_points, const pf
   build_tasks(grid_points);
   double norm_work = 0;
   for (const Task& t : tasks_) norm_work += static_cast<double>(t.points) * subtree_cost(pg_, t.node);
-  small_norms_ = norm_work <= kSmallNormWork;
+  small_norms_ = norm_work <= kSmallNormWork && setup_smem_bytes() <= 48 * 1024 && tasks_.size() <= 16;
 
   ck(cudaSetDevice(opt.device), "cudaSetDevice");
   // parameters and results live in mapped (zero-copy) pinned memory: the
@@ -199,7 +199,12 @@ Model::Model(const pf_graph& g, const pf_data& d, uint32_t grid_points, const pf
     Shard& sh = shards_[s];
     sh.device = opt.device + s;
     int part = shard_count_ > 1 ? shard_index_ : s;
-    subtree_range(n_chunks_total_, groups, part, &sh.chunk_lo, &sh.chunk_hi);
+    // shards are whole subtrees of the top tree over groups of 32 chunks
+    const uint64_t n_groups_total = (n_chunks_total_ + 31) / 32;
+    uint64_t glo = 0, ghi = 0;
+    subtree_range(n_groups_total, groups, part, &glo, &ghi);
+    sh.chunk_lo = std::min(glo * 32, n_chunks_total_);
+    sh.chunk_hi = std::min(ghi * 32, n_chunks_total_);
     sh.n_chunks = static_cast<int>(sh.chunk_hi - sh.chunk_lo);
     sh.event_offset = std::min(sh.chunk_lo * chunk_, n_events_);
     uint64_t end = std::min(sh.chunk_hi * chunk_, n_events_);
@@ -225,6 +230,10 @@ Model::Model(const pf_graph& g, const pf_data& d, uint32_t grid_points, const pf
     size_t part_elems = static_cast<size_t>(kMaxBatch) *
                         std::max<size_t>(std::max<size_t>(sh.n_chunks, max_norm_blocks_), 1);
     ck(cudaMalloc(&sh.d_partials, 16 * part_elems), "cudaMalloc partials");
+    const size_t n_groups = (static_cast<size_t>(sh.n_chunks) + 31) / 32;
+    ck(cudaMalloc(&sh.d_gpartials, 16 * kMaxBatch * std::max<size_t>(n_groups, 1)), "cudaMalloc gpartials");
+    ck(cudaMalloc(&sh.d_gcount, sizeof(uint32_t) * (n_groups + 1)), "cudaMalloc gcount");
+    ck(cudaMemset(sh.d_gcount, 0, sizeof(uint32_t) * (n_groups + 1)), "memset gcount");
     ck(cudaMalloc(&sh.d_rec, sizeof(KRec) * kMaxBatch), "cudaMalloc rec");
     ck(cudaMalloc(&sh.d_clamp, sizeof(uint64_t) * 2 * std::max(L_.n_poly, 1)), "cudaMalloc clamp");
     ck(cudaMemset(sh.d_clamp, 0, sizeof(uint64_t) * 2 * std::max(L_.n_poly, 1)), "memset clamp");
@@ -264,6 +273,7 @@ Model::~Model() {
   for (Shard& sh : shards_) {
     cudaSetDevice(sh.device);
     for (auto& kv : sh.graphs) cudaGraphExecDestroy(kv.second);
+    if (sh.graph1) cudaGraphDestroy(sh.graph1);
     if (sh.stream) cudaStreamDestroy(sh.stream);
     cudaFree(sh.d_data);
     cudaFree(sh.d_P);
@@ -271,6 +281,8 @@ Model::~Model() {
     cudaFree(sh.d_C);
     cudaFree(sh.d_tasks);
     cudaFree(sh.d_partials);
+    cudaFree(sh.d_gpartials);
+    cudaFree(sh.d_gcount);
     cudaFree(sh.d_rec);
     cudaFree(sh.d_clamp);
     cudaFreeHost(sh.h_out);
@@ -363,6 +375,9 @@ Args Model::base_args(Shard& sh, int K) {
   a.tasks = sh.d_tasks;
   a.n_tasks = static_cast<int>(tasks_.size());
   a.partials = sh.d_partials;
+  a.gpartials = sh.d_gpartials;
+  a.gcount = sh.d_gcount;
+  a.done = sh.d_gcount + (sh.n_chunks + 31) / 32;
   a.rec = sh.d_rec;
   a.total_content = total_content_;
   // norm-stage clamps are counted once (shard 0); the others discard them
@@ -382,7 +397,7 @@ cudaGraphExec_t Model::graph_for(Shard& sh, int K) {
   cudaGraph_t graph;
   ck(cudaStreamBeginCapture(sh.stream, cudaStreamCaptureModeThreadLocal), "begin capture");
   if (small_norms_) {
-    launch(sh.mod->setup, dim3(K), dim3(1024), 0, sh.stream, a);
+    launch(sh.mod->setup, dim3(K), dim3(512), setup_smem_bytes(), sh.stream, a);
     ++kernels;
   } else {
     launch(sh.mod->pre, dim3(K), dim3(256), 0, sh.stream, a);
@@ -402,9 +417,9 @@ cudaGraphExec_t Model::graph_for(Shard& sh, int K) {
     // one warp per chunk, 2-warp blocks: the block scheduler balances SMs
     const int grid = std::max(1, (sh.n_chunks + kEventWarps - 1) / kEventWarps);
     const size_t smem = event_smem(L_, K);
+    // the event pass closes its own reduction tree and publishes the results
     launch(sh.mod->event, dim3(grid), dim3(32 * kEventWarps), smem, sh.stream, e, /*pdl=*/true);
-    launch(sh.mod->final, dim3(K), dim3(1024), 0, sh.stream, e, /*pdl=*/true);
-    kernels += 2;
+    kernels += 1;
     if (K == 1) {
       sh.event_args = e;
       sh.event_grid = grid;
@@ -416,7 +431,16 @@ cudaGraphExec_t Model::graph_for(Shard& sh, int K) {
   ck(cudaStreamEndCapture(sh.stream, &graph), "end capture");
   cudaGraphExec_t exec;
   ck(cudaGraphInstantiate(&exec, graph, 0), "cudaGraphInstantiate");
-  cudaGraphDestroy(graph);
+  if (K == 1 && L_.np <= 64) {
+    // keep the template: its root kernel node receives the parameters inline
+    // (cudaGraphExecKernelNodeSetParams) on every call
+    size_t n_roots = 1;
+    ck(cudaGraphGetRootNodes(graph, &sh.first_node, &n_roots), "cudaGraphGetRootNodes");
+    sh.graph1 = graph;
+    sh.first_args = a;
+  } else {
+    cudaGraphDestroy(graph);
+  }
   sh.kernels_per_graph = kernels;
   sh.graphs.emplace(K, exec);
   return exec;
@@ -466,6 +490,21 @@ void Model::run(const double* params, int K, std::vector<Raw>& out, bool partial
   for (Shard& sh : shards_) {
     cudaGraphExec_t g = graph_for(sh, K);
     ck(cudaSetDevice(sh.device), "cudaSetDevice");
+    if (K == 1 && sh.graph1) {
+      cudaKernelNodeParams kp = {};
+      const bool setup = small_norms_;
+      kp.func = reinterpret_cast<void*>(setup ? sh.mod->setup : sh.mod->pre);
+      kp.gridDim = dim3(1);
+      kp.blockDim = dim3(setup ? 512 : 256);
+      kp.sharedMemBytes = setup ? static_cast<unsigned>(setup_smem_bytes()) : 0u;
+      Args inl = sh.first_args;
+      inl.npin = L_.np;
+      std::memcpy(inl.pin, params, sizeof(double) * L_.np);
+      void* ptrs[] = {&inl};
+      kp.kernelParams = ptrs;
+      kp.extra = nullptr;
+      ck(cudaGraphExecKernelNodeSetParams(g, sh.first_node, &kp), "cudaGraphExecKernelNodeSetParams");
+    }
     ck(cudaGraphLaunch(g, sh.stream), "cudaGraphLaunch");
     g_launches += sh.kernels_per_graph;
   }

@@ -74,6 +74,12 @@ struct Args {
   KRec* rec;
   uint64_t* clamp;
   double total_content;
+  void* gpartials;
+  uint32_t* gcount;
+  uint32_t* done;
+  int npin;
+  int pad1;
+  double pin[64];
 };
 
 struct Module {
@@ -98,6 +104,8 @@ struct Shard {
   double* d_C = nullptr;
   Task* d_tasks = nullptr;  // all levels, concatenated
   void* d_partials = nullptr;
+  void* d_gpartials = nullptr;  // K x groups of 32 chunks
+  uint32_t* d_gcount = nullptr; // groups + 1 (last: closed-group counter)
   KRec* d_rec = nullptr;
   uint64_t* d_clamp = nullptr;  // [n_poly counted | n_poly discarded]
   Out* h_out = nullptr;         // mapped, kMaxBatch
@@ -106,6 +114,9 @@ struct Shard {
   std::map<int, cudaGraphExec_t> graphs;
   int kernels_per_graph = 0;
   Args event_args{};  // K = 1 event-pass arguments (timing)
+  Args first_args{};  // K = 1 arguments of the first kernel (params inline)
+  cudaGraph_t graph1 = nullptr;       // K = 1 template graph (kept for node updates)
+  cudaGraphNode_t first_node = nullptr;
   int event_grid = 1;
   void* d_scratch = nullptr;  // L2 flush buffer (bench only)
 };
@@ -154,6 +165,9 @@ class Model {
   Args base_args(Shard& s, int K);
   void build_tasks(uint32_t grid_points);
   std::string error_message(uint32_t code_node) const;
+  size_t setup_smem_bytes() const {
+    return sizeof(double) * (std::max(L_.np, 1) + std::max(L_.ss, 1));
+  }
 
   Program pg_;
   Layout L_;
