@@ -244,14 +244,14 @@ def main():
         if world == 1:
             return bm.eval_metric(p)
         import torch
-        hi, lo, pen = bm.eval_partial(p)
-        t = torch.tensor([hi, lo, 1.0 if pen else 0.0], dtype=torch.float64, device=f"cuda:{local}")
+        fx, pen = bm.eval_partial(p)
+        t = torch.tensor(fx + [1 if pen else 0], dtype=torch.int64, device=f"cuda:{local}")
         out = [torch.empty_like(t) for _ in range(world)]
-        dist.all_gather(out, t)
-        parts = [(o[0].item(), o[1].item()) for o in out]
-        if any(o[2].item() for o in out):
+        dist.all_gather(out, t)  # 56 bytes per rank over NCCL
+        rows = [o.tolist() for o in out]
+        if any(r[-1] for r in rows):
             return pf.kPenaltyValue
-        return pf.combine_partials(parts)
+        return pf.combine_partials([r[:-1] for r in rows])
 
     for _ in range(args.warmup):
         step_value(params)
@@ -287,7 +287,7 @@ def main():
         ms_step = dt.item() / args.steps * 1e3
         ev_ms = None
         launches = pf.kernel_launches() - launches0
-        h2d, d2h = 8 * params.size, 16
+        h2d, d2h = 8 * params.size, 88
 
     # e2e: the public API call (pf_eval_metric via BoundModel.eval_metric) with
     # host parameters in and the host scalar out, host wall clock, L2 flushed

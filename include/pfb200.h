@@ -115,9 +115,9 @@ typedef struct pf_data {
  *   device:        CUDA ordinal of the first device.
  *   n_devices:     >1 shards events over devices device..device+n-1 in this
  *                  process (contiguous subtrees of the reduction tree).
- *   shard_index/shard_count: this process evaluates only subtree
- *                  shard_index of shard_count (power of two) of the global
- *                  reduction tree; pf_eval_partial returns its partial and
+ *   shard_index/shard_count: this process evaluates only the contiguous
+ *                  chunk range shard_index of shard_count (power of two);
+ *                  pf_eval_partial returns its exact accumulator and
  *                  pf_combine_partials reproduces the global value.
  *                  shard_count = 1: whole data set. */
 typedef struct pf_options {
@@ -196,14 +196,19 @@ PF_API int pf_eval_metric(pf_model* model, const double* params, size_t n_params
 PF_API int pf_eval_metric_batch(pf_model* model, const double* params, size_t k, size_t n_params,
                          int32_t metric, double* out, pf_status* status);
 
-/* Shard partial (double-double hi, lo) of this process's subtree, for
- * multi-process sharding; *penalty set when the 1e300 penalty applies. */
-PF_API int pf_eval_partial(pf_model* model, const double* params, size_t n_params, int32_t metric,
-                    double* partial_hi_lo, int32_t* penalty, pf_status* status);
+/* The metric is accumulated EXACTLY in a fixed-point superaccumulator of
+ * PF_FX_DIGITS signed 64-bit digits (value = sum_i d_i 2^(32 i - 128)) and
+ * rounded once, so it does not depend on summation order or sharding. */
+#define PF_FX_DIGITS 6
 
-/* Fixed-order combine of shard_count partials (hi, lo pairs in shard order)
- * into the global metric; identical to the single-device value. */
-PF_API double pf_combine_partials(const double* partials_hi_lo, int32_t shard_count);
+/* This process's shard accumulator (PF_FX_DIGITS digits), for multi-process
+ * sharding; *penalty set when the 1e300 penalty applies. */
+PF_API int pf_eval_partial(pf_model* model, const double* params, size_t n_params, int32_t metric,
+                           int64_t* partial_fx, int32_t* penalty, pf_status* status);
+
+/* Exact combine of shard_count accumulators (shard_count x PF_FX_DIGITS) and
+ * the correctly rounded metric: bitwise the single-device value. */
+PF_API double pf_combine_partials(const int64_t* partials_fx, int32_t shard_count);
 
 /* PdfNode::cached_norm / norm_error_estimate (pdf.hpp:88-92) for every node
  * in pre-order; valid[i] = 0 where the reference would throw

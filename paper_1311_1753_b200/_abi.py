@@ -14,6 +14,7 @@ LIB_PATH = os.path.join(_HERE, "libpfb200.so")
 PF_EXPONENTIAL, PF_GAUSSIAN, PF_BREIT_WIGNER, PF_POLYNOMIAL = 0, 1, 2, 3
 PF_PRODUCT, PF_SUM, PF_COMPOSITE, PF_MAPPED, PF_CONVOLUTION, PF_ARGUS = 4, 5, 6, 7, 8, 9
 PF_NLL, PF_CHISQ = 0, 1
+PF_FX_DIGITS = 6
 PF_OBSERVABLE, PF_PARAMETER = 0, 1
 
 
@@ -101,8 +102,8 @@ _SIGNATURES = {
     "pf_eval_metric_batch": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.c_size_t, C.c_size_t,
                                        C.c_int32, C.POINTER(C.c_double), C.POINTER(pf_status)]),
     "pf_eval_partial": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.c_size_t, C.c_int32,
-                                  C.POINTER(C.c_double), C.POINTER(C.c_int32), C.POINTER(pf_status)]),
-    "pf_combine_partials": (C.c_double, [C.POINTER(C.c_double), C.c_int32]),
+                                  C.POINTER(C.c_int64), C.POINTER(C.c_int32), C.POINTER(pf_status)]),
+    "pf_combine_partials": (C.c_double, [C.POINTER(C.c_int64), C.c_int32]),
     "pf_node_norms": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                 C.POINTER(C.c_int32), C.c_int32]),
     "pf_log_floor_count": (C.c_uint64, [C.c_void_p]),

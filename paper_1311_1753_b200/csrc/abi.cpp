@@ -43,34 +43,6 @@ int guarded(pf_status* st, F&& f) {
   return st ? st->code : 1;
 }
 
-// DD add identical to pf_dd_add on the device (pf_device.cuh)
-struct DD {
-  double hi, lo;
-};
-DD two_sum(double a, double b) {
-  double s = a + b;
-  double bb = s - a;
-  return {s, (a - (s - bb)) + (b - bb)};
-}
-DD fast_two_sum(double a, double b) {
-  double s = a + b;
-  return {s, b - (s - a)};
-}
-DD dd_add(DD a, DD b) {
-  DD s = two_sum(a.hi, b.hi);
-  DD t = two_sum(a.lo, b.lo);
-  double lo = s.lo + t.hi;
-  DD u = fast_two_sum(s.hi, lo);
-  lo = u.lo + t.lo;
-  return fast_two_sum(u.hi, lo);
-}
-DD pairwise(const DD* v, int n) {  // engine.hpp:63-68 shape
-  if (n == 0) return {0.0, 0.0};
-  if (n == 1) return v[0];
-  int half = n / 2;
-  return dd_add(pairwise(v, half), pairwise(v + half, n - half));
-}
-
 pfb::Config to_config(const pf_fit_config* c) {
   pfb::Config cfg;
   if (c) {
@@ -188,20 +160,20 @@ int pf_eval_metric_batch(pf_model* model, const double* params, size_t k, size_t
 }
 
 int pf_eval_partial(pf_model* model, const double* params, size_t n_params, int32_t metric,
-                    double* partial_hi_lo, int32_t* penalty, pf_status* status) {
+                    int64_t* partial_fx, int32_t* penalty, pf_status* status) {
   return guarded(status, [&] {
-    if (!model || !partial_hi_lo || !penalty) throw pfb::Error("bad-model", "null argument");
+    if (!model || !partial_fx || !penalty) throw pfb::Error("bad-model", "null argument");
     int pen = 0;
-    model->impl->eval_partial(params, n_params, metric, partial_hi_lo, &pen);
+    model->impl->eval_partial(params, n_params, metric, partial_fx, &pen);
     *penalty = pen;
   });
 }
 
-double pf_combine_partials(const double* partials_hi_lo, int32_t shard_count) {
-  std::vector<DD> v(static_cast<size_t>(std::max(shard_count, 0)));
-  for (int32_t i = 0; i < shard_count; ++i) v[i] = {partials_hi_lo[2 * i], partials_hi_lo[2 * i + 1]};
-  DD r = pairwise(v.data(), shard_count);
-  return r.hi + r.lo;
+double pf_combine_partials(const int64_t* partials_fx, int32_t shard_count) {
+  int64_t fx[PF_FX_DIGITS] = {0, 0, 0, 0, 0, 0};
+  for (int32_t s = 0; s < shard_count; ++s)
+    for (int i = 0; i < PF_FX_DIGITS; ++i) fx[i] += partials_fx[s * PF_FX_DIGITS + i];
+  return pfb::fx_round(fx);
 }
 
 int pf_node_norms(pf_model* model, double* norms, double* errs, int32_t* valid, int32_t n_nodes) {

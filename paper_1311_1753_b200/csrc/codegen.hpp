@@ -28,7 +28,8 @@ struct Layout {
   int nc = 0;                 // model constant doubles
   int nc_total_slot = -1;     // C index of N_tot (binned)
   bool binned = false;
-  int ept = 16;               // events per thread (chunk = 256 * ept)
+  int ept = 8;                // events per lane per sub-chunk (32 * ept events)
+  int nsub = 2;               // sub-chunks per chunk (chunk = nsub * 32 * ept events)
   std::vector<int> load_cols; // data columns read per event
   std::vector<int> poly_index; // node -> clamp counter index (-1 otherwise)
   int n_poly = 0;

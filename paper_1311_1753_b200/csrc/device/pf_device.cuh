@@ -41,7 +41,7 @@ struct pf_krec {
   pf_u64 first_event_error;  // min (index << 24 | node << 8 | code) raised in the event pass
   pf_u32 norm_error;         // min (node << 8 | code) raised while normalising
   pf_u32 arrive[PF_MAX_LEVELS + 1];  // last-block arrival counters
-  double result_hi, result_lo;
+  long long fx[6];           // exact superaccumulator of the metric (pf_fx_add)
 };
 
 struct pf_task {  // one midpoint sum: node, n points per box dimension
@@ -56,9 +56,10 @@ struct pf_task {  // one midpoint sum: node, n points per box dimension
 // Per-call result record, written by the device straight into mapped
 // (zero-copy) host memory: no memcpy nodes in the per-call graph.
 struct pf_out {
-  double result_hi, result_lo;
+  double result;  // correctly rounded metric of this shard
   pf_u64 floor_count, first_nonfinite, first_event_error;
   pf_u32 norm_error, pad;
+  long long fx[6];  // exact digits (combined across shards on the host)
 };
 
 struct pf_args {
@@ -86,9 +87,7 @@ struct pf_args {
   pf_krec* rec;         // K records
   pf_u64* clamp;        // cumulative PolynomialPdf clamp counters per node
   double total_content; // binned: N_tot (engine.hpp:153)
-  pf_dd* gpartials;     // K x n_groups (groups of 32 chunks)
-  pf_u32* gcount;       // per-group ticket counters (self-resetting)
-  pf_u32* done;         // closed-group counter (self-resetting)
+  pf_u32* done;         // finished-block counter of the event pass (self-resetting)
   int npin;             // K = 1: parameters passed inline (pin[0..npin))
   int pad1;
   double pin[PF_MAX_INLINE];
@@ -191,6 +190,145 @@ __device__ __forceinline__ pf_dd pf_block_reduce(pf_dd v, pf_dd* sm) {
     for (int d = 16; d > 0; d >>= 1) v = pf_dd_add(v, pf_shfl_down_dd(v, d));
   }
   return v;
+}
+
+// ----------------------------------------------------------------------------
+// Exact fixed-point superaccumulator: value = sum_i d_i 2^(32 i - 128), six
+// signed 64-bit digit accumulators, every contribution < 2^32 in magnitude
+// per digit.  Adding a double is exact for |x| in [2^-128, 2^64) (bits below
+// 2^-128 are truncated toward zero); additions commute, so the total does not
+// depend on order, chunking or the number of devices, and the final rounding
+// to double is correct (pf_fx_round).  The reference sums in x87 long double
+// (engine.hpp:57-87); this is at least as accurate.
+#define PF_FX_DIGITS 6
+
+__device__ __forceinline__ void pf_fx_add(long long* acc, double x) {
+  if (x == 0.0) return;
+  const pf_u64 bits = (pf_u64)__double_as_longlong(x);
+  const int be = (int)((bits >> 52) & 0x7ff);
+  if (be == 0x7ff || be >= 1023 + 63) {  // non-finite or |x| >= 2^63: poison the sum
+    atomicAdd((unsigned long long*)(acc + PF_FX_DIGITS - 1), 0x4000000000000000ull);
+    return;
+  }
+  pf_u64 m = bits & 0xfffffffffffffull;
+  int e;
+  if (be == 0) {
+    e = -1074;
+  } else {
+    m |= 0x10000000000000ull;
+    e = be - 1075;
+  }
+  int p = e + 128;  // bit position of m's LSB above 2^-128
+  if (p < 0) {
+    if (p <= -53) return;
+    m >>= -p;
+    p = 0;
+  }
+  const int q = p >> 5, s = p & 31;
+  // m << s spans up to 85 bits: three 32-bit digits starting at q
+  const pf_u64 d0 = (m << s) & 0xffffffffull;
+  const pf_u64 d1 = (s ? (m >> (32 - s)) : (m >> 32)) & 0xffffffffull;
+  const pf_u64 d2 = s ? (m >> (64 - s)) : 0ull;
+  const bool neg = (bits >> 63) != 0;
+  const long long v[3] = {(long long)d0, (long long)d1, (long long)d2};
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+    if (v[i] && q + i < PF_FX_DIGITS)
+      atomicAdd((unsigned long long*)(acc + q + i), (unsigned long long)(neg ? -v[i] : v[i]));
+}
+
+// Register-resident superaccumulator of one lane (same digit layout): exact
+// integer adds with branch-free digit placement; no atomics, no shuffles.
+struct pf_fxl {
+  long long d[PF_FX_DIGITS];
+};
+
+__device__ __forceinline__ void pf_fxl_init(pf_fxl& A) {
+#pragma unroll
+  for (int i = 0; i < PF_FX_DIGITS; ++i) A.d[i] = 0;
+}
+
+__device__ __forceinline__ void pf_fxl_add(pf_fxl& A, double x) {
+  const pf_u64 bits = (pf_u64)__double_as_longlong(x);
+  const int be = (int)((bits >> 52) & 0x7ff);
+  const bool poison = be >= 1023 + 63;  // non-finite or |x| >= 2^63
+  pf_u64 m = (bits & 0xfffffffffffffull) | (be ? 0x10000000000000ull : 0ull);
+  int p = (be ? be : 1) - 1075 + 128;  // LSB position above 2^-128
+  if (p < 0) {
+    m = p <= -53 ? 0ull : (m >> -p);
+    p = 0;
+  }
+  const int q = p >> 5, s = p & 31;
+  const long long d0 = (long long)((m << s) & 0xffffffffull);
+  const long long d1 = (long long)((s ? (m >> (32 - s)) : (m >> 32)) & 0xffffffffull);
+  const long long d2 = (long long)(s ? (m >> (64 - s)) : 0ull);
+  const long long sg = (bits >> 63) ? -1ll : 1ll;
+#pragma unroll
+  for (int i = 0; i < PF_FX_DIGITS; ++i) {
+    const long long v = (i == q ? d0 : 0ll) + (i == q + 1 ? d1 : 0ll) + (i == q + 2 ? d2 : 0ll);
+    A.d[i] += sg * v;
+  }
+  if (poison) A.d[PF_FX_DIGITS - 1] += 0x4000000000000000ll;
+}
+
+// Warp-wide integer sum of the lanes' accumulators into the global one.
+__device__ __forceinline__ void pf_fxl_flush(pf_fxl& A, long long* acc) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int i = 0; i < PF_FX_DIGITS; ++i) {
+    long long v = A.d[i];
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) v += __shfl_down_sync(0xffffffffu, v, d);
+    if (lane == 0 && v) atomicAdd((unsigned long long*)(acc + i), (unsigned long long)v);
+  }
+}
+
+// Correctly rounded double of the accumulator (host twin: pfb::fx_round).
+__device__ __forceinline__ double pf_fx_round(const long long* acc) {
+  unsigned dig[PF_FX_DIGITS];
+  long long carry = 0;
+  for (int i = 0; i < PF_FX_DIGITS; ++i) {  // carry-normalise to 32-bit digits
+    const long long v = acc[i] + carry;
+    dig[i] = (unsigned)(v & 0xffffffffll);
+    carry = v >> 32;
+  }
+  if (carry > 0 || carry < -1) return __longlong_as_double(0x7ff8000000000000ll);  // poisoned
+  const bool neg = carry < 0;
+  if (neg) {  // magnitude of the 192-bit two's complement value
+    unsigned c = 1;
+    for (int i = 0; i < PF_FX_DIGITS; ++i) {
+      const unsigned long long t = (unsigned long long)(~dig[i]) + c;
+      dig[i] = (unsigned)t;
+      c = (unsigned)(t >> 32);
+    }
+  }
+  int top = PF_FX_DIGITS - 1;
+  while (top >= 0 && dig[top] == 0) --top;
+  if (top < 0) return 0.0;
+  const int lz = __clz(dig[top]);
+  const pf_u64 hi = dig[top];
+  const pf_u64 mid = top >= 1 ? dig[top - 1] : 0u;
+  const pf_u64 lo = top >= 2 ? dig[top - 2] : 0u;
+  bool sticky = false;
+  for (int i = top - 3; i >= 0; --i) sticky |= dig[i] != 0;
+  // 64-bit window with the leading one at bit 63, the rest into `sticky`
+  pf_u64 win = (hi << (32 + lz)) | (mid << lz);
+  if (lz) {
+    win |= lo >> (32 - lz);
+    sticky |= (lo & ((1ull << (32 - lz)) - 1)) != 0;
+  } else {
+    sticky |= lo != 0;
+  }
+  pf_u64 mant = win >> 11;  // 53 significant bits
+  const pf_u64 rem = win & 0x7ffull;
+  if ((rem & 0x400ull) && ((rem & 0x3ffull) || sticky || (mant & 1ull))) ++mant;  // nearest even
+  int msb = 32 * top + 31 - lz;
+  if (mant >> 53) {
+    mant >>= 1;
+    ++msb;
+  }
+  const double r = ldexp((double)mant, msb - 52 - 128);
+  return neg ? -r : r;
 }
 
 // ----------------------------------------------------------------------------

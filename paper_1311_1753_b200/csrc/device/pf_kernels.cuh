@@ -27,8 +27,7 @@ __device__ __forceinline__ void pf_rec_init(pf_krec* r) {
   r->first_event_error = ~0ull;
   r->norm_error = ~0u;
   for (int i = 0; i <= PF_MAX_LEVELS; ++i) r->arrive[i] = 0u;
-  r->result_hi = 0.0;
-  r->result_lo = 0.0;
+  for (int i = 0; i < PF_FX_DIGITS; ++i) r->fx[i] = 0ll;
 }
 
 __device__ __forceinline__ void pf_load_params(const pf_args& a, int k) {
@@ -48,27 +47,30 @@ __device__ __forceinline__ void pf_finish_norm(double* S, pf_krec* r, int node, 
     atomicMin(&r->norm_error, ((pf_u32)node << 8) | PF_E_ZERO_INTEGRAL);
 }
 
-// Results of parameter set k into mapped host memory.
-__device__ void pf_publish(const pf_args& a, int k, double hi, double lo) {
+// Results of parameter set k into mapped host memory (one thread writes the
+// record; the calling threads copy the norms).
+__device__ void pf_publish(const pf_args& a, int k, int tid, int nt) {
   const pf_krec* r = a.rec + k;
   pf_out* o = a.hout + k;
-  if (threadIdx.x == 0) {
-    o->result_hi = hi;
-    o->result_lo = lo;
-    o->floor_count = r->floor_count;
-    o->first_nonfinite = r->first_nonfinite;
-    o->first_event_error = r->first_event_error;
-    o->norm_error = r->norm_error;
+  if (tid == 0) {
+    long long fx[PF_FX_DIGITS];
+    for (int i = 0; i < PF_FX_DIGITS; ++i) fx[i] = (long long)__ldcg((const unsigned long long*)(r->fx + i));
+    o->result = pf_fx_round(fx);
+    for (int i = 0; i < PF_FX_DIGITS; ++i) o->fx[i] = fx[i];
+    o->floor_count = __ldcg(&r->floor_count);
+    o->first_nonfinite = __ldcg(&r->first_nonfinite);
+    o->first_event_error = __ldcg(&r->first_event_error);
+    o->norm_error = __ldcg(&r->norm_error);
   }
   const double* S = a.S + (pf_u64)k * PF_SS;
-  for (int i = threadIdx.x; i < 3 * a.n_nodes; i += blockDim.x)
-    a.hnorms[(pf_u64)k * 3 * a.n_nodes + i] = S[i];
+  for (int i = tid; i < 3 * a.n_nodes; i += nt) a.hnorms[(pf_u64)k * 3 * a.n_nodes + i] = S[i];
 #if PF_NPOLY > 0
   if (k == a.K - 1)
-    for (int i = threadIdx.x; i < PF_NPOLY; i += blockDim.x) a.hclamp[i] = a.clamp[i];
+    for (int i = tid; i < PF_NPOLY; i += nt) a.hclamp[i] = __ldcg(a.clamp + i);
 #endif
 }
 
+// ---------------------------------------------------------------------------
 #define PF_SETUP_THREADS 512  // 128 registers: the level's 8 reductions interleave unspilled
 
 // ---------------------------------------------------------------------------
@@ -273,7 +275,12 @@ extern "C" __global__ void __launch_bounds__(PF_THREADS) pf_norm_kernel(const __
 // issued BEFORE waiting on the setup grid (PDL).
 
 #define PF_SUB (32 * PF_EPT)
-#define PF_NSUB 8  // sub-chunks per chunk: chunk = 256 * PF_EPT events
+#ifndef PF_NSUB
+#define PF_NSUB 8  // sub-chunks per chunk: chunk = PF_NSUB * 32 * PF_EPT events
+#endif
+#ifndef PF_UNROLL
+#define PF_UNROLL 4  // events interleaved per lane in the event loop
+#endif
 #ifndef PF_NST
 #define PF_NST 3
 #endif
@@ -347,13 +354,47 @@ __device__ __forceinline__ pf_dd pf_stage_terms(const pf_args& a, int k, pf_u64 
   bool bad = false;
 #if PF_BINNED
   pf_dd acc = pf_dd_zero();
+#elif PF_LOGFORM
+  double lsum = 0.0, fprod = 1.0;
 #else
   pf_prod acc;
   pf_prod_init(acc);
 #endif
-#pragma unroll 2
+#pragma unroll PF_UNROLL
   for (int j = 0; j < PF_EPT; ++j) {
     const int i = 32 * j + lane;
+#if !PF_BINNED && PF_LOGFORM
+    {
+      // log domain: -log v = -(L + log F) with no per-event log; events near
+      // the floor / overflow / subnormal range take the exact linear path
+      double ev[PF_NCOLS];
+#pragma unroll
+      for (int q = 0; q < PF_NCOLS; ++q) ev[q] = 0.0;
+#pragma unroll
+      for (int q = 0; q < PF_NLOAD; ++q) ev[pf_load_col(q)] = st[q * PF_SUB + i];
+      double Lv, Fv;
+      bool ok = pf_eval_event_log(ev, P, S, Lv, Fv);
+      if (!FULL && i >= n_valid) {
+        ok = true;
+        Lv = 0.0;
+        Fv = 1.0;
+      }
+      if (!ok) {
+        double v = pf_eval_event(ev, P, S, a.C, cx, cnt);
+        if (v < PF_LOG_FLOOR) {  // engine.hpp:190-193
+          v = PF_LOG_FLOOR;
+          ++floors;
+        } else if (!(v <= 1.7976931348623157e308)) {
+          bad = true;
+          v = 1.0;
+        }
+        Lv = pf_log(v);
+        Fv = 1.0;
+      }
+      lsum += Lv;
+      fprod *= Fv;
+    }
+#else
     double ev[PF_NCOLS];
 #pragma unroll
     for (int q = 0; q < PF_NCOLS; ++q) ev[q] = 0.0;
@@ -394,6 +435,7 @@ __device__ __forceinline__ pf_dd pf_stage_terms(const pf_args& a, int k, pf_u64 
     }
     pf_prod_mul(acc, v);
 #endif
+#endif  // log domain
   }
   if (cx.err) pf_rescan(a, k, base, lane, st, FULL ? PF_SUB : n_valid, true);
   if (bad) pf_rescan(a, k, base, lane, st, FULL ? PF_SUB : n_valid, false);
@@ -401,73 +443,11 @@ __device__ __forceinline__ pf_dd pf_stage_terms(const pf_args& a, int k, pf_u64 
   pf_cnt_flush(cnt, a.clamp);
 #if PF_BINNED
   return acc;
+#elif PF_LOGFORM
+  return pf_two_sum(-lsum, -pf_log(fprod));
 #else
   return pf_prod_neglog(acc);
 #endif
-}
-
-// Publish from ONE warp (the warp that closed the last group).
-__device__ void pf_publish_warp(const pf_args& a, int k, pf_dd r) {
-  const int lane = threadIdx.x & 31;
-  const pf_krec* rc = a.rec + k;
-  pf_out* o = a.hout + k;
-  if (lane == 0) {
-    o->result_hi = r.hi;
-    o->result_lo = r.lo;
-    o->floor_count = rc->floor_count;
-    o->first_nonfinite = rc->first_nonfinite;
-    o->first_event_error = rc->first_event_error;
-    o->norm_error = rc->norm_error;
-  }
-  const double* S = a.S + (pf_u64)k * PF_SS;
-  for (int i = lane; i < 3 * a.n_nodes; i += 32) a.hnorms[(pf_u64)k * 3 * a.n_nodes + i] = S[i];
-#if PF_NPOLY > 0
-  if (k == a.K - 1)
-    for (int i = lane; i < PF_NPOLY; i += 32) a.hclamp[i] = a.clamp[i];
-#endif
-}
-
-// Reduction above the chunks, inside the event pass (no final kernel):
-//   group  = 32 consecutive chunks, a complete binary tree over 32 slots
-//            with (2i, 2i+1) siblings, closed by the last warp to finish one
-//            of its chunks (ticket counter, self-resetting);
-//   top    = the reference's pairwise tree (engine.hpp:63-68) over groups,
-//            run by the warp that closes the last group, which publishes.
-// Shards are whole subtrees of the top tree, so the value is independent of
-// the number of devices.
-__device__ void pf_close_chunk(const pf_args& a, int c) {
-  const int lane = threadIdx.x & 31;
-  const int g = c >> 5;
-  const int n_groups = (a.n_chunks + 31) >> 5;
-  const int gsize = min(32, a.n_chunks - 32 * g);
-  unsigned last = 0;
-  __threadfence();
-  if (lane == 0) last = atomicAdd(a.gcount + g, 1u) == (unsigned)(gsize - 1);
-  last = __shfl_sync(0xffffffffu, last, 0);
-  if (!last) return;
-  __threadfence();
-  if (lane == 0) a.gcount[g] = 0u;
-  for (int k = 0; k < a.K; ++k) {
-    const int cc = 32 * g + lane;
-    pf_dd x = cc < a.n_chunks ? a.partials[(pf_u64)k * a.n_chunks + cc] : pf_dd_zero();
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const pf_dd o = pf_shfl_down_dd(x, d);
-      if ((lane & (2 * d - 1)) == 0) x = pf_dd_add(x, o);
-    }
-    if (lane == 0) a.gpartials[(pf_u64)k * n_groups + g] = x;
-  }
-  __threadfence();
-  unsigned final_warp = 0;
-  if (lane == 0) final_warp = atomicAdd(a.done, 1u) == (unsigned)(n_groups - 1);
-  final_warp = __shfl_sync(0xffffffffu, final_warp, 0);
-  if (!final_warp) return;
-  __threadfence();
-  if (lane == 0) *a.done = 0u;
-  for (int k = 0; k < a.K; ++k) {
-    const pf_dd r = pf_pairwise_warp(a.gpartials + (pf_u64)k * n_groups, (pf_u64)n_groups);
-    pf_publish_warp(a, k, r);
-  }
 }
 
 __device__ __forceinline__ pf_dd pf_warp_tree(pf_dd v) {
@@ -477,13 +457,15 @@ __device__ __forceinline__ pf_dd pf_warp_tree(pf_dd v) {
 }
 
 #ifndef PF_EVENT_MIN_BLOCKS
-#define PF_EVENT_MIN_BLOCKS 12
+#define PF_EVENT_MIN_BLOCKS 8
 #endif
 extern "C" __global__ void __launch_bounds__(PF_EV_THREADS, PF_EVENT_MIN_BLOCKS) pf_event_kernel(const __grid_constant__ pf_args a) {
   extern __shared__ __align__(16) unsigned char pf_dyn[];
   __shared__ __align__(8) pf_u64 bars[PF_EV_WARPS * PF_NST];
   double* stages = reinterpret_cast<double*>(pf_dyn);
   pf_dd* accs = reinterpret_cast<pf_dd*>(stages + PF_EV_WARPS * PF_NST * PF_STAGE);  // [k][thread]
+  long long* fxs = reinterpret_cast<long long*>(accs + a.K * PF_EV_THREADS);  // [k][digit][thread]
+  for (int i = threadIdx.x; i < a.K * PF_FX_DIGITS * PF_EV_THREADS; i += PF_EV_THREADS) fxs[i] = 0;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   double* my = stages + warp * PF_NST * PF_STAGE;
@@ -530,31 +512,44 @@ extern "C" __global__ void __launch_bounds__(PF_EV_THREADS, PF_EVENT_MIN_BLOCKS)
     __syncwarp();
     if (w + PF_NST - 1 < W) issue(w + PF_NST - 1);  // refills the stage read at w - 1
     if ((w % PF_NSUB) == PF_NSUB - 1) {
+      // chunk done: each lane adds its double-double chunk value EXACTLY into
+      // its own fixed-point accumulator (integer adds, no shuffles/atomics)
       for (int k = 0; k < a.K; ++k) {
-        pf_dd t = pf_warp_tree(accs[k * PF_EV_THREADS + threadIdx.x]);
-        if (lane == 0) a.partials[(pf_u64)k * a.n_chunks + c] = t;
+        const pf_dd t = accs[k * PF_EV_THREADS + threadIdx.x];
+        pf_fxl A;
+#pragma unroll
+        for (int i = 0; i < PF_FX_DIGITS; ++i) A.d[i] = fxs[(k * PF_FX_DIGITS + i) * PF_EV_THREADS + threadIdx.x];
+        pf_fxl_add(A, t.hi);
+        pf_fxl_add(A, t.lo);
+#pragma unroll
+        for (int i = 0; i < PF_FX_DIGITS; ++i) fxs[(k * PF_FX_DIGITS + i) * PF_EV_THREADS + threadIdx.x] = A.d[i];
       }
-      pf_close_chunk(a, (int)c);
     }
   }
+  // warp totals (integer shuffles) into the call's accumulators
+  for (int k = 0; k < a.K; ++k) {
+    pf_fxl A;
+#pragma unroll
+    for (int i = 0; i < PF_FX_DIGITS; ++i) A.d[i] = fxs[(k * PF_FX_DIGITS + i) * PF_EV_THREADS + threadIdx.x];
+    pf_fxl_flush(A, a.rec[k].fx);
+  }
+  // the last block to finish publishes every parameter set
+  __shared__ int s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(a.done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (threadIdx.x == 0) *a.done = 0u;  // self-resetting (bench relaunches)
+  for (int k = 0; k < a.K; ++k) pf_publish(a, k, threadIdx.x, blockDim.x);
 }
 
 // ---------------------------------------------------------------------------
-// final: the reference's pairwise tree over chunk partials (engine.hpp:
-// 63-68), one block per parameter set, then publish to the host.
-extern "C" __global__ void __launch_bounds__(PF_FINAL_THREADS) pf_final_kernel(const __grid_constant__ pf_args a) {
-  __shared__ pf_dd sm[PF_FINAL_THREADS];
-  pf_pdl_wait();
-  const int k = blockIdx.x;
-  pf_dd t = pf_dd_zero();
-  if (a.n_chunks > 0)
-    t = pf_pairwise_block(a.partials + (pf_u64)k * a.n_chunks, (pf_u64)a.n_chunks, sm,
-                          PF_FINAL_THREADS);
-  pf_publish(a, k, t.hi, t.lo);
-}
-
-// ---------------------------------------------------------------------------
-// publish only (a shard without events)
+// publish only (a shard without events: the metric is 0)
 extern "C" __global__ void __launch_bounds__(PF_THREADS) pf_publish_kernel(const __grid_constant__ pf_args a) {
-  pf_publish(a, blockIdx.x, 0.0, 0.0);
+  pf_pdl_wait();
+  pf_publish(a, blockIdx.x, threadIdx.x, blockDim.x);
 }

@@ -12,8 +12,10 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
+#include <limits>
 #include <mutex>
 #include <sstream>
 #include <unordered_map>
@@ -51,7 +53,9 @@ ModuleCache& cache() {
 size_t event_smem(const Layout& L, int K) {
   const size_t stages = static_cast<size_t>(kEventWarps) * kEventStages * L.load_cols.size() * 32 *
                         static_cast<size_t>(L.ept) * sizeof(double);
-  return stages + static_cast<size_t>(K) * 32 * kEventWarps * 16;
+  // per lane and parameter set: a double-double chunk accumulator (16 B)
+  // and an exact fixed-point accumulator (6 x 8 B)
+  return stages + static_cast<size_t>(K) * 32 * kEventWarps * (16 + 48);
 }
 
 namespace {
@@ -76,7 +80,6 @@ const Module* load_module(const Layout& L, int device) {
   ck(cudaLibraryGetKernel(&m->pre, m->lib, "pf_pre_kernel"), "get pf_pre_kernel");
   ck(cudaLibraryGetKernel(&m->norm, m->lib, "pf_norm_kernel"), "get pf_norm_kernel");
   ck(cudaLibraryGetKernel(&m->event, m->lib, "pf_event_kernel"), "get pf_event_kernel");
-  ck(cudaLibraryGetKernel(&m->final, m->lib, "pf_final_kernel"), "get pf_final_kernel");
   ck(cudaKernelSetAttributeForDevice(m->event, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(event_smem(L, kMaxBatch)), device),
      "event kernel smem attribute");
@@ -122,6 +125,15 @@ void subtree_range(uint64_t n, int shard_count, int index, uint64_t* lo, uint64_
 }
 
 uint64_t kernel_launch_count() { return g_launches.load(); }
+
+int sm_count(int device) {
+  static int cached[64] = {0};
+  if (device >= 0 && device < 64 && cached[device]) return cached[device];
+  int n = 148;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device);
+  if (device >= 0 && device < 64) cached[device] = n;
+  return n;
+}
 
 std::vector<char> compile_cubin(const Layout& L, std::string* log) {
   nvrtcProgram prog;
@@ -177,7 +189,7 @@ Model::Model(const pf_graph& g, const pf_data& d, uint32_t grid_points, const pf
   if (shard_index_ < 0 || shard_index_ >= shard_count_)
     throw Error("bad-backend", "shard_index out of range");
 
-  chunk_ = 256ull * static_cast<uint64_t>(L_.ept);
+  chunk_ = 32ull * static_cast<uint64_t>(L_.ept) * static_cast<uint64_t>(L_.nsub);
   n_chunks_total_ = (n_events_ + chunk_ - 1) / chunk_;
   const int n_cols_data = d.n_obs + (binned_ ? 2 : 0);
   build_tasks(grid_points);
@@ -199,12 +211,9 @@ Model::Model(const pf_graph& g, const pf_data& d, uint32_t grid_points, const pf
     Shard& sh = shards_[s];
     sh.device = opt.device + s;
     int part = shard_count_ > 1 ? shard_index_ : s;
-    // shards are whole subtrees of the top tree over groups of 32 chunks
-    const uint64_t n_groups_total = (n_chunks_total_ + 31) / 32;
-    uint64_t glo = 0, ghi = 0;
-    subtree_range(n_groups_total, groups, part, &glo, &ghi);
-    sh.chunk_lo = std::min(glo * 32, n_chunks_total_);
-    sh.chunk_hi = std::min(ghi * 32, n_chunks_total_);
+    // balanced contiguous chunk ranges; the exact accumulator makes the sum
+    // independent of where the shards split
+    subtree_range(n_chunks_total_, groups, part, &sh.chunk_lo, &sh.chunk_hi);
     sh.n_chunks = static_cast<int>(sh.chunk_hi - sh.chunk_lo);
     sh.event_offset = std::min(sh.chunk_lo * chunk_, n_events_);
     uint64_t end = std::min(sh.chunk_hi * chunk_, n_events_);
@@ -230,10 +239,8 @@ Model::Model(const pf_graph& g, const pf_data& d, uint32_t grid_points, const pf
     size_t part_elems = static_cast<size_t>(kMaxBatch) *
                         std::max<size_t>(std::max<size_t>(sh.n_chunks, max_norm_blocks_), 1);
     ck(cudaMalloc(&sh.d_partials, 16 * part_elems), "cudaMalloc partials");
-    const size_t n_groups = (static_cast<size_t>(sh.n_chunks) + 31) / 32;
-    ck(cudaMalloc(&sh.d_gpartials, 16 * kMaxBatch * std::max<size_t>(n_groups, 1)), "cudaMalloc gpartials");
-    ck(cudaMalloc(&sh.d_gcount, sizeof(uint32_t) * (n_groups + 1)), "cudaMalloc gcount");
-    ck(cudaMemset(sh.d_gcount, 0, sizeof(uint32_t) * (n_groups + 1)), "memset gcount");
+    ck(cudaMalloc(&sh.d_done, sizeof(uint32_t)), "cudaMalloc done");
+    ck(cudaMemset(sh.d_done, 0, sizeof(uint32_t)), "memset done");
     ck(cudaMalloc(&sh.d_rec, sizeof(KRec) * kMaxBatch), "cudaMalloc rec");
     ck(cudaMalloc(&sh.d_clamp, sizeof(uint64_t) * 2 * std::max(L_.n_poly, 1)), "cudaMalloc clamp");
     ck(cudaMemset(sh.d_clamp, 0, sizeof(uint64_t) * 2 * std::max(L_.n_poly, 1)), "memset clamp");
@@ -281,8 +288,7 @@ Model::~Model() {
     cudaFree(sh.d_C);
     cudaFree(sh.d_tasks);
     cudaFree(sh.d_partials);
-    cudaFree(sh.d_gpartials);
-    cudaFree(sh.d_gcount);
+    cudaFree(sh.d_done);
     cudaFree(sh.d_rec);
     cudaFree(sh.d_clamp);
     cudaFreeHost(sh.h_out);
@@ -375,9 +381,7 @@ Args Model::base_args(Shard& sh, int K) {
   a.tasks = sh.d_tasks;
   a.n_tasks = static_cast<int>(tasks_.size());
   a.partials = sh.d_partials;
-  a.gpartials = sh.d_gpartials;
-  a.gcount = sh.d_gcount;
-  a.done = sh.d_gcount + (sh.n_chunks + 31) / 32;
+  a.done = sh.d_done;
   a.rec = sh.d_rec;
   a.total_content = total_content_;
   // norm-stage clamps are counted once (shard 0); the others discard them
@@ -415,7 +419,12 @@ cudaGraphExec_t Model::graph_for(Shard& sh, int K) {
   e.clamp = sh.d_clamp;
   if (sh.n_local > 0) {
     // one warp per chunk, 2-warp blocks: the block scheduler balances SMs
-    const int grid = std::max(1, (sh.n_chunks + kEventWarps - 1) / kEventWarps);
+    // persistent grid: one wave of 2-warp blocks; every warp strides over
+    // many chunks, so its TMA ring streams without restarts
+    int per_sm = kEventBlocksPerSM;
+    if (const char* env = std::getenv("PFB200_EV_BLOCKS")) per_sm = std::max(1, std::atoi(env));
+    const int grid = std::max(1, std::min((sh.n_chunks + kEventWarps - 1) / kEventWarps,
+                                          sm_count(sh.device) * per_sm));
     const size_t smem = event_smem(L_, K);
     // the event pass closes its own reduction tree and publishes the results
     launch(sh.mod->event, dim3(grid), dim3(32 * kEventWarps), smem, sh.stream, e, /*pdl=*/true);
@@ -536,22 +545,16 @@ void Model::run(const double* params, int K, std::vector<Raw>& out, bool partial
     }
     if (ev_err != ~0ull) throw Error("event-error", error_message(static_cast<uint32_t>(ev_err & 0xffffff)));
     for (Shard& sh : shards_) floor_total_ += sh.h_out[k].floor_count;
-    // shard partials combined by the top levels of the pairwise tree
-    std::vector<double> parts;
-    for (Shard& sh : shards_) {
-      parts.push_back(sh.n_local > 0 ? sh.h_out[k].result_hi : 0.0);
-      parts.push_back(sh.n_local > 0 ? sh.h_out[k].result_lo : 0.0);
+    // shard accumulators are exact: summing their digits and rounding once
+    // gives the single-device value bit for bit
+    for (int i = 0; i < 6; ++i) {
+      int64_t s = 0;
+      for (Shard& sh : shards_) s += sh.h_out[k].fx[i];
+      out[k].fx[i] = s;
     }
-    if (partial_only || shards_.size() == 1) {
-      out[k].hi = parts[0];
-      out[k].lo = parts[1];
-    } else {
-      double r = pf_combine_partials(parts.data(), static_cast<int32_t>(shards_.size()));
-      out[k].hi = r;
-      out[k].lo = 0.0;
-    }
+    out[k].value = shards_.size() == 1 ? shards_[0].h_out[k].result : fx_round(out[k].fx);
     if (!partial_only) {
-      double r = out[k].hi + out[k].lo;
+      double r = out[k].value;
       if (!std::isfinite(r)) {
         if (nonfinite != ~0ull)
           throw Error("non-finite-metric", "first offending event index " + std::to_string(nonfinite));
@@ -586,7 +589,7 @@ double Model::eval(const double* params, size_t n, int metric, pf_eval_info* inf
     if (info) info->penalty = 1;
     return kPenaltyValue;
   }
-  return out[0].hi + out[0].lo;
+  return out[0].value;
 }
 
 void Model::eval_batch(const double* params, size_t K, size_t n, int metric, double* result) {
@@ -608,14 +611,14 @@ void Model::eval_batch(const double* params, size_t K, size_t n, int metric, dou
       std::memcpy(packed.data() + j * n, params + live[first + j] * n, sizeof(double) * n);
     run(packed.data(), static_cast<int>(cnt), out, false);
     for (size_t j = 0; j < cnt; ++j)
-      result[live[first + j]] = out[j].penalty ? kPenaltyValue : out[j].hi + out[j].lo;
+      result[live[first + j]] = out[j].penalty ? kPenaltyValue : out[j].value;
   }
 }
 
-void Model::eval_partial(const double* params, size_t n, int metric, double* hi_lo, int* penalty) {
+void Model::eval_partial(const double* params, size_t n, int metric, int64_t* fx, int* penalty) {
   check_call(n, metric);
   *penalty = 0;
-  hi_lo[0] = hi_lo[1] = 0.0;
+  for (int i = 0; i < 6; ++i) fx[i] = 0;
   if (!params_valid(params)) {
     *penalty = 1;
     return;
@@ -626,8 +629,7 @@ void Model::eval_partial(const double* params, size_t n, int metric, double* hi_
     *penalty = 1;
     return;
   }
-  hi_lo[0] = out[0].hi;
-  hi_lo[1] = out[0].lo;
+  for (int i = 0; i < 6; ++i) fx[i] = out[0].fx[i];
 }
 
 uint64_t Model::clamp_count(int node) const {
@@ -701,6 +703,57 @@ BenchResult Model::bench(const double* params, size_t n, int metric, int steps, 
   r.h2d_bytes = sizeof(double) * std::max(L_.np, 1);
   r.d2h_bytes = sizeof(Out) + sizeof(double) * 3 * pg_.nodes.size() + sizeof(uint64_t) * L_.n_poly;
   return r;
+}
+
+}  // namespace pfb
+
+namespace pfb {
+
+double fx_round(const int64_t* acc) {
+  constexpr int D = 6;
+  uint32_t dig[D];
+  int64_t carry = 0;
+  for (int i = 0; i < D; ++i) {
+    const int64_t v = acc[i] + carry;
+    dig[i] = static_cast<uint32_t>(v & 0xffffffffll);
+    carry = v >> 32;
+  }
+  if (carry > 0 || carry < -1) return std::numeric_limits<double>::quiet_NaN();
+  const bool neg = carry < 0;
+  if (neg) {
+    uint32_t c = 1;
+    for (int i = 0; i < D; ++i) {
+      const uint64_t t = static_cast<uint64_t>(static_cast<uint32_t>(~dig[i])) + c;
+      dig[i] = static_cast<uint32_t>(t);
+      c = static_cast<uint32_t>(t >> 32);
+    }
+  }
+  int top = D - 1;
+  while (top >= 0 && dig[top] == 0) --top;
+  if (top < 0) return 0.0;
+  const int lz = __builtin_clz(dig[top]);
+  const uint64_t hi = dig[top];
+  const uint64_t mid = top >= 1 ? dig[top - 1] : 0u;
+  const uint64_t lo = top >= 2 ? dig[top - 2] : 0u;
+  bool sticky = false;
+  for (int i = top - 3; i >= 0; --i) sticky |= dig[i] != 0;
+  uint64_t win = (hi << (32 + lz)) | (mid << lz);
+  if (lz) {
+    win |= lo >> (32 - lz);
+    sticky |= (lo & ((1ull << (32 - lz)) - 1)) != 0;
+  } else {
+    sticky |= lo != 0;
+  }
+  uint64_t mant = win >> 11;
+  const uint64_t rem = win & 0x7ffull;
+  if ((rem & 0x400ull) && ((rem & 0x3ffull) || sticky || (mant & 1ull))) ++mant;
+  int msb = 32 * top + 31 - lz;
+  if (mant >> 53) {
+    mant >>= 1;
+    ++msb;
+  }
+  const double r = std::ldexp(static_cast<double>(mant), msb - 52 - 128);
+  return neg ? -r : r;
 }
 
 }  // namespace pfb

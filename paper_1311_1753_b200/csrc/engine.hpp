@@ -16,9 +16,10 @@
 namespace pfb {
 
 constexpr double kPenaltyValue = 1e300;  // engine.hpp:52
-constexpr int kMaxBatch = 32;            // parameter sets per launch
+constexpr int kMaxBatch = 16;            // parameter sets per launch
 constexpr int kEventWarps = 2;           // warps per event-pass block (PF_EV_WARPS)
 constexpr int kEventStages = 3;          // TMA stages per warp (PF_NST)
+constexpr int kEventBlocksPerSM = 8;     // resident event blocks per SM (PF_EVENT_MIN_BLOCKS)
 constexpr double kSmallNormWork = 65536; // raw evaluations: single-CTA setup path
 
 // host mirrors of the device structs (pf_device.cuh); layouts must match
@@ -28,9 +29,9 @@ struct KRec {
   uint64_t first_event_error;
   uint32_t norm_error;
   uint32_t arrive[15];
-  double result_hi, result_lo;
+  int64_t fx[6];
 };
-static_assert(sizeof(KRec) == 104, "pf_krec layout");
+static_assert(sizeof(KRec) == 136, "pf_krec layout");
 
 struct Task {
   int node, n, dims, first_block;
@@ -43,11 +44,16 @@ struct Task {
 static_assert(sizeof(Task) == 184, "pf_task layout");
 
 struct Out {
-  double result_hi, result_lo;
+  double result;
   uint64_t floor_count, first_nonfinite, first_event_error;
   uint32_t norm_error, pad;
+  int64_t fx[6];
 };
-static_assert(sizeof(Out) == 48, "pf_out layout");
+static_assert(sizeof(Out) == 88, "pf_out layout");
+
+// Correctly rounded double of a superaccumulator (digits d_i 2^(32 i - 128));
+// host twin of pf_fx_round (pf_device.cuh).  NaN when poisoned.
+double fx_round(const int64_t* fx);
 
 struct Args {
   const double* hP;
@@ -74,8 +80,6 @@ struct Args {
   KRec* rec;
   uint64_t* clamp;
   double total_content;
-  void* gpartials;
-  uint32_t* gcount;
   uint32_t* done;
   int npin;
   int pad1;
@@ -104,8 +108,7 @@ struct Shard {
   double* d_C = nullptr;
   Task* d_tasks = nullptr;  // all levels, concatenated
   void* d_partials = nullptr;
-  void* d_gpartials = nullptr;  // K x groups of 32 chunks
-  uint32_t* d_gcount = nullptr; // groups + 1 (last: closed-group counter)
+  uint32_t* d_done = nullptr;   // finished-block counter of the event pass
   KRec* d_rec = nullptr;
   uint64_t* d_clamp = nullptr;  // [n_poly counted | n_poly discarded]
   Out* h_out = nullptr;         // mapped, kMaxBatch
@@ -128,6 +131,7 @@ struct BenchResult {
 
 void subtree_range(uint64_t n, int shard_count, int index, uint64_t* lo, uint64_t* hi);
 size_t event_smem(const Layout& L, int K);
+int sm_count(int device);
 
 class Model {
  public:
@@ -141,7 +145,7 @@ class Model {
   // K independent evaluations, bitwise equal to K eval() calls
   void eval_batch(const double* params, size_t K, size_t n, int metric, double* out);
   // this process's shard partial (shard_count > 1)
-  void eval_partial(const double* params, size_t n, int metric, double* hi_lo, int* penalty);
+  void eval_partial(const double* params, size_t n, int metric, int64_t* fx, int* penalty);
   BenchResult bench(const double* params, size_t n, int metric, int steps, bool flush);
 
   const Program& program() const { return pg_; }
@@ -156,7 +160,8 @@ class Model {
  private:
   struct Raw {  // per-k outcome of one device pass
     bool penalty = false;
-    double hi = 0, lo = 0;
+    double value = 0;
+    int64_t fx[6] = {0, 0, 0, 0, 0, 0};
   };
   void check_call(size_t n, int metric) const;
   bool params_valid(const double* p) const;

@@ -839,20 +839,20 @@ class BoundModel:
         return out
 
     def eval_partial(self, params, metric=MetricKind.NegLogLikelihood):
-        """(hi, lo, penalty) of this process's shard subtree"""
+        """(exact accumulator digits, penalty) of this process's shard"""
         p = np.ascontiguousarray(np.asarray(params, dtype=np.float64).ravel())
-        part = (C.c_double * 2)()
+        part = (C.c_int64 * _abi.PF_FX_DIGITS)()
         pen = C.c_int32()
         st = _abi.pf_status()
         if lib.pf_eval_partial(self._h, p.ctypes.data_as(C.POINTER(C.c_double)), p.size, int(metric),
                                part, C.byref(pen), C.byref(st)):
             _raise(st)
-        return part[0], part[1], bool(pen.value)
+        return list(part), bool(pen.value)
 
 
 def combine_partials(parts) -> float:
-    """fixed-order combine of shard partials [(hi, lo), ...] (pfb200.h)"""
-    flat = (C.c_double * (2 * len(parts)))(*[v for hl in parts for v in hl[:2]])
+    """exact combine of shard accumulators [[d0..d5], ...] (pfb200.h)"""
+    flat = (C.c_int64 * (_abi.PF_FX_DIGITS * len(parts)))(*[int(v) for fx in parts for v in fx])
     return lib.pf_combine_partials(flat, len(parts))
 
 
