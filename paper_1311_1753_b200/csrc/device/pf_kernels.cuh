@@ -281,6 +281,7 @@ extern "C" __global__ void __launch_bounds__(PF_THREADS) pf_norm_kernel(const __
 #ifndef PF_UNROLL
 #define PF_UNROLL 4  // events interleaved per lane in the event loop
 #endif
+constexpr int pf_unroll = PF_UNROLL;
 #ifndef PF_NST
 #define PF_NST 3
 #endif
@@ -360,7 +361,7 @@ __device__ __forceinline__ pf_dd pf_stage_terms(const pf_args& a, int k, pf_u64 
   pf_prod acc;
   pf_prod_init(acc);
 #endif
-#pragma unroll PF_UNROLL
+#pragma unroll pf_unroll
   for (int j = 0; j < PF_EPT; ++j) {
     const int i = 32 * j + lane;
 #if !PF_BINNED && PF_LOGFORM
