@@ -200,10 +200,10 @@ int pf_bench(pf_model* model, const double* params, size_t n_params, int32_t met
 
 void pf_shard_events(uint64_t n_events, uint64_t chunk, int32_t shard_count, int32_t shard_index,
                      uint64_t* first, uint64_t* count) {
-  // shards are subtrees of the top tree over groups of 32 chunks
-  uint64_t chunks = chunk ? (n_events + chunk - 1) / chunk : 0, glo = 0, ghi = 0;
-  pfb::subtree_range((chunks + 31) / 32, shard_count, shard_index, &glo, &ghi);
-  const uint64_t lo = std::min(glo * 32, chunks), hi = std::min(ghi * 32, chunks);
+  // balanced contiguous chunk ranges (the exact accumulator makes any split
+  // give the same metric)
+  uint64_t chunks = chunk ? (n_events + chunk - 1) / chunk : 0, lo = 0, hi = 0;
+  pfb::subtree_range(chunks, shard_count, shard_index, &lo, &hi);
   uint64_t a = std::min(lo * chunk, n_events), b = std::min(hi * chunk, n_events);
   if (first) *first = a;
   if (count) *count = b - a;
