@@ -554,12 +554,11 @@ void Model::run(const double* params, int K, std::vector<Raw>& out, bool partial
     }
     out[k].value = shards_.size() == 1 ? shards_[0].h_out[k].result : fx_round(out[k].fx);
     if (!partial_only) {
-      double r = out[k].value;
-      if (!std::isfinite(r)) {
-        if (nonfinite != ~0ull)
-          throw Error("non-finite-metric", "first offending event index " + std::to_string(nonfinite));
-        throw Error("non-finite-metric", "non-finite reduction");
-      }
+      // any non-finite term makes the reference's sum non-finite
+      // (engine.hpp:210-216); the device neutralised it and kept its index
+      if (nonfinite != ~0ull)
+        throw Error("non-finite-metric", "first offending event index " + std::to_string(nonfinite));
+      if (!std::isfinite(out[k].value)) throw Error("non-finite-metric", "non-finite reduction");
     }
   }
   if (L_.n_poly > 0) {
