@@ -132,6 +132,30 @@ def peaks():
         return 6650.0, "fallback"
 
 
+NCU_SUMMARY = os.path.join(ROOT, "profiles", "r1_event_kernel_ncu.txt")
+
+
+def ncu_metric(name):
+    """one metric of the committed ncu --set full capture of pf_event_kernel
+    (profiles/r1_event_kernel_ncu.txt, written by tools/ncu_summary.py), or None"""
+    try:
+        with open(NCU_SUMMARY) as fh:
+            for line in fh:
+                parts = line.split()
+                if len(parts) == 2 and parts[0] == name:
+                    return float(parts[1])
+    except (OSError, ValueError):
+        pass
+    return None
+
+
+def ncu_traffic():
+    """dram read+write bytes per launch (ncu reports Mbyte)"""
+    r = ncu_metric("dram__bytes_read.sum")
+    w = ncu_metric("dram__bytes_write.sum")
+    return None if r is None or w is None else (r + w) * 1e6
+
+
 def cpu_baseline(pdf, x, xs, steps=4):
     """The reference (oracle/_ref) on a bounded sample, all host threads."""
     import oracle
@@ -334,10 +358,19 @@ def main():
         algo_bytes = 8.0 * n_per  # one f64 column per event (EventTable layout)
         achieved = algo_bytes / (ev_ms * 1e-3) / 1e9
         line["roofline"] = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                            "frac": achieved / hbm_peak, "traffic": None,
+                            "frac": achieved / hbm_peak, "traffic": ncu_traffic(),
+                            "traffic_source": "profiles/r1_event_kernel_ncu.txt (ncu --set full, 1 launch)",
                             "kernel": "pf_event_kernel", "kernel_ms": ev_ms,
                             "algorithmic_bytes_per_launch": algo_bytes,
                             "kernel_share_of_step": ev_ms / ms_step, "peak_kind": peak_kind}
+        # the event pass is issue/FP64-pipe limited, not HBM limited: report
+        # the ncu-measured pipe utilisation of the same capture beside it
+        fp64 = ncu_metric("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active")
+        issue = ncu_metric("smsp__issue_active.avg.pct_of_peak_sustained_active")
+        if fp64 is not None:
+            line["roofline"]["fp64_pipe_active_frac_ncu"] = fp64 / 100.0
+        if issue is not None:
+            line["roofline"]["issue_active_frac_ncu"] = issue / 100.0
     if world == 1 and not args.no_cpu_baseline:
         try:
             line["cpu_baseline"] = cpu_baseline(pdf, x, xs)
