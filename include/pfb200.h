@@ -138,7 +138,9 @@ typedef struct pf_status {
 typedef struct pf_eval_info {
   uint64_t log_floor_delta; /* events floored at 1e-300 in this call */
   int32_t penalty;          /* 1 when the 1e300 penalty was returned */
-  int32_t norms_recomputed; /* 0 when the parameter fingerprint matched */
+  int32_t norms_recomputed; /* always 1: norms are recomputed every call on
+                               the device (the reference's fingerprint,
+                               pdf.hpp:40-51, misses on any param change) */
 } pf_eval_info;
 
 typedef struct pf_model pf_model;
@@ -224,8 +226,9 @@ PF_API uint64_t pf_clamp_count(const pf_model* model, int32_t node);
 
 /* Device-side timing of the hot path with CUDA events on the model's own
  * stream (the stream every graph and kernel of the model is launched on).
- *   step_ms_*:            one full pf_eval_metric graph (params H2D, pre,
- *                         norm levels, event pass, final tree, result D2H)
+ *   step_ms_*:            one full pf_eval_metric graph (setup kernel with
+ *                         validity + normalisation, event pass; params and
+ *                         result through mapped host memory)
  *   event_kernel_ms_mean: the event-pass kernel alone (roofline numerator)
  * flush_l2 != 0 writes a 256 MiB scratch buffer before every timed launch,
  * outside the timed window, so no step starts with a warm L2. */
@@ -249,7 +252,8 @@ PF_API int pf_bench(pf_model* model, const double* params, size_t n_params, int3
 PF_API void pf_shard_events(uint64_t n_events, uint64_t chunk, int32_t shard_count,
                             int32_t shard_index, uint64_t* first, uint64_t* count);
 
-/* Events per reduction chunk of a bound model (256 x events per thread). */
+/* Events per reduction chunk of a bound model (warp sub-chunks x 32 lanes x
+ * events per lane); shard boundaries fall on whole chunks. */
 PF_API uint64_t pf_model_chunk(const pf_model* model);
 
 /* ---- fit-manager --------------------------------------------------------- */
