@@ -236,6 +236,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--events", type=int, default=EVENTS_PER_GPU)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--diag-no-flush", action="store_true",
+                    help="diagnostics only: keep L2 warm between steps (never a reported number)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
@@ -288,7 +290,7 @@ def main():
         st = _abi.pf_status()
         with sampler:
             rc = pf.lib.pf_bench(bm._h, params.ctypes.data_as(C.POINTER(C.c_double)), params.size, 0,
-                                 args.steps, 1, C.byref(res), C.byref(st))
+                                 args.steps, 0 if args.diag_no_flush else 1, C.byref(res), C.byref(st))
         if rc:
             raise RuntimeError(st.message.decode())
         launches = (res.kernels_per_step * args.steps)

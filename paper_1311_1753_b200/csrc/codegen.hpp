@@ -30,6 +30,9 @@ struct Layout {
   bool binned = false;
   int ept = 8;                // events per lane per sub-chunk (32 * ept events)
   int nsub = 2;               // sub-chunks per chunk (chunk = nsub * 32 * ept events)
+  int setup_cluster = 8;      // CTAs of the setup kernel's thread-block cluster
+  int nst = 3;                // TMA stages per event warp (PF_NST)
+  int setup_maxq = 8;         // most midpoint sums in one level (PF_SETUP_MAXQ)
   std::vector<int> load_cols; // data columns read per event
   std::vector<int> poly_index; // node -> clamp counter index (-1 otherwise)
   int n_poly = 0;

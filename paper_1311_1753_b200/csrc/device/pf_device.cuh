@@ -88,6 +88,7 @@ struct pf_args {
   pf_u64* clamp;        // cumulative PolynomialPdf clamp counters per node
   double total_content; // binned: N_tot (engine.hpp:153)
   pf_u32* done;         // finished-block counter of the event pass (self-resetting)
+  long long* fxbins;    // K x PF_FX_BINS x 16: binned block digits (self-resetting)
   int npin;             // K = 1: parameters passed inline (pin[0..npin))
   int pad1;
   double pin[PF_MAX_INLINE];
@@ -101,6 +102,28 @@ struct pf_ctx {
 
 __device__ __forceinline__ void pf_fail(pf_ctx& cx, int node, int code) {
   if (!cx.err) cx.err = ((pf_u32)node << 8) | (pf_u32)code;
+}
+
+// Richardson combination of a node's (coarse, fine) midpoint sums
+// (pdf.hpp:178-188) into S: norm, error estimate, 1 / norm; the sums are kept
+// (PF_SUMS_BASE) for AddPdf nodes normalised from their children's sums.
+// Returns true when the integral is zero or non-finite (pdf.hpp:186-187).
+__device__ __forceinline__ bool pf_finish_norm_s(double* S, int node, double coarse, double fine) {
+  const double norm = fine + (fine - coarse) / 3.0;
+  const double err = fabs(fine - coarse) / 3.0;
+  S[3 * node + 0] = norm;
+  S[3 * node + 1] = err;
+  S[3 * node + 2] = 1.0 / norm;
+#ifdef PF_SUMS_BASE
+  S[PF_SUMS_BASE + 2 * node] = coarse;
+  S[PF_SUMS_BASE + 2 * node + 1] = fine;
+#endif
+  return !(norm > 0.0) || !isfinite(norm);
+}
+
+__device__ __forceinline__ void pf_finish_norm_cx(double* S, pf_ctx& cx, int node, double coarse,
+                                                  double fine) {
+  if (pf_finish_norm_s(S, node, coarse, fine)) pf_fail(cx, node, PF_E_ZERO_INTEGRAL);
 }
 
 // ----------------------------------------------------------------------------
@@ -272,16 +295,21 @@ __device__ __forceinline__ void pf_fxl_add(pf_fxl& A, double x) {
 }
 
 // Warp-wide integer sum of the lanes' accumulators into the global one.
-__device__ __forceinline__ void pf_fxl_flush(pf_fxl& A, long long* acc) {
-  const int lane = threadIdx.x & 31;
+// warp total of the lanes' digits (integer shuffles; exact), valid in lane 0
+__device__ __forceinline__ void pf_fxl_warp_sum(pf_fxl& A) {
 #pragma unroll
   for (int i = 0; i < PF_FX_DIGITS; ++i) {
     long long v = A.d[i];
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) v += __shfl_down_sync(0xffffffffu, v, d);
-    if (lane == 0 && v) atomicAdd((unsigned long long*)(acc + i), (unsigned long long)v);
+    A.d[i] = v;
   }
 }
+
+// Same-address atomics serialise in one L2 slice (~1 op/clk): the event pass
+// spreads its blocks' digits over PF_FX_BINS 128-byte slots
+#define PF_FX_BINS 32
+#define PF_FX_BIN_STRIDE 16
 
 // Correctly rounded double of the accumulator (host twin: pfb::fx_round).
 __device__ __forceinline__ double pf_fx_round(const long long* acc) {
@@ -478,6 +506,34 @@ __device__ __forceinline__ double pf_exp_core(double x) {
   const int e1 = e >> 1;
   const double sc = __hiloint2double(__double2hiint(s) + (e1 << 20), __double2loint(s));
   return sc * __hiloint2double((e - e1 + 1023) << 20, 0);
+}
+
+// F = 1 + e^x for x <= 0: the mixture factor of the log-sum-exp NLL form
+// (codegen.cpp emit_event_log), multiplied per lane and logged once per chunk.
+// Only F matters, not e^x: below x = -40, e^x < 2^-57 vanishes in 1 + e^x, so
+// the exponent is clamped at -60 on the integer pipe instead of clamping x
+// (x is finite and |x| < 2^40 whenever the caller keeps F).  Degree-4
+// polynomial on the 2^(j/128) table: |r| <= 0.00272, truncation r^5/120 <=
+// 1.3e-15 relative in e^x, i.e. < 1.3e-15 absolute in log F per event
+// (per-term budget, far inside the 1e-12 relative NLL bar).
+// Constants whose low 32 bits are zero become SASS immediates (no registers).
+#define PF_F_INVLN2N 0x1.71547p+7            // ~128/ln2: only picks k
+#define PF_F_LN2N_HI 0x1.62e42p-8            // 21 significant bits: k * hi exact
+#define PF_F_LN2N_LO 0x1.fdf473de6af28p-29   // ln2/128 - hi
+__device__ __forceinline__ double pf_one_plus_exp_neg(double x) {
+  const double kd = fma(x, PF_F_INVLN2N, 0x1.8p52);
+  const int ki = __double2loint(kd);
+  const double k = kd - 0x1.8p52;
+  double r = fma(k, -PF_F_LN2N_HI, x);
+  r = fma(k, -PF_F_LN2N_LO, r);
+  const double2 t = pf_exp_tab[ki & 127];
+  double q = fma(r, 0x1.55555p-5, 1.0 / 6.0);
+  q = fma(q, r, 0.5);
+  q = fma(q, r, 1.0);
+  const double p = r * q;                    // e^r - 1
+  const double s = fma(t.x, p, t.y) + t.x;   // 2^(j/128) e^r, in [0.99, 2.01)
+  const int e = max(ki >> 7, -60);
+  return 1.0 + __hiloint2double(__double2hiint(s) + (e << 20), __double2loint(s));
 }
 
 // ----------------------------------------------------------------------------

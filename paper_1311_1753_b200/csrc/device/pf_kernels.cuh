@@ -38,12 +38,7 @@ __device__ __forceinline__ void pf_load_params(const pf_args& a, int k) {
 // Richardson combination of a node's (coarse, fine) sums (pdf.hpp:178-188)
 __device__ __forceinline__ void pf_finish_norm(double* S, pf_krec* r, int node, double coarse,
                                                double fine) {
-  const double norm = fine + (fine - coarse) / 3.0;
-  const double err = fabs(fine - coarse) / 3.0;
-  S[3 * node + 0] = norm;
-  S[3 * node + 1] = err;
-  S[3 * node + 2] = 1.0 / norm;
-  if (!(norm > 0.0) || !isfinite(norm))
+  if (pf_finish_norm_s(S, node, coarse, fine))
     atomicMin(&r->norm_error, ((pf_u32)node << 8) | PF_E_ZERO_INTEGRAL);
 }
 
@@ -72,19 +67,46 @@ __device__ void pf_publish(const pf_args& a, int k, int tid, int nt) {
 
 // ---------------------------------------------------------------------------
 #define PF_SETUP_THREADS 512  // 128 registers: the level's 8 reductions interleave unspilled
+#ifndef PF_SETUP_CLUSTER
+#define PF_SETUP_CLUSTER 1    // CTAs (one thread-block cluster) per parameter set
+#endif
+#ifndef PF_SETUP_MAXQ
+#define PF_SETUP_MAXQ 8       // most midpoint sums in one level (2 per node)
+#endif
+
+// thread-block cluster helpers (distributed shared memory, sm_90+)
+__device__ __forceinline__ unsigned pf_cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void pf_cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ pf_dd pf_dsmem_load_dd(const pf_dd* p, unsigned rank) {
+  unsigned ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(pf_smem_addr(p)), "r"(rank));
+  double hi, lo;
+  asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];" : "=d"(hi), "=d"(lo) : "r"(ra) : "memory");
+  return pf_dd{hi, lo};
+}
 
 // ---------------------------------------------------------------------------
-// setup: parameters H2D, call records, pre stage and EVERY normalisation
-// level in one CTA per parameter set (small grids).  Midpoint sums at n and
-// 2n (pdf.hpp:148-176): thread t sums points t, t + 1024, ... in double-
-// double; a fixed-shape block reduction combines the 1024 partials.
+// setup: call records, pre stage and EVERY normalisation level for one
+// parameter set in one thread-block cluster of PF_SETUP_CLUSTER CTAs (small
+// grids).  Midpoint sums at n and 2n (pdf.hpp:148-176): thread t of CTA c
+// sums points c * 512 + t, + 512 * PF_SETUP_CLUSTER, ... in double-double; a
+// fixed-shape block reduction gives each CTA's partial, and every CTA adds
+// the partials of all ranks (read over DSMEM) in rank order, so all CTAs hold
+// identical norms and stage constants for the next level.  Rank 0 writes the
+// per-call state to global memory for the event pass.
 extern "C" __global__ void __launch_bounds__(PF_SETUP_THREADS) pf_setup_kernel(const __grid_constant__ pf_args a) {
   // parameters and the per-call state live in shared memory while the CTA
   // works (every S read/write is an LDS/STS, not an L2 round trip); the task
   // table is staged too.  The state is written to global memory at the end.
   extern __shared__ __align__(16) double pf_sdyn[];
-  __shared__ pf_dd wsum[8][32];
-  __shared__ double sums[8];
+  // this CTA's warp partials per task, double-buffered by level parity
+  __shared__ pf_dd wpart[2][PF_SETUP_MAXQ][PF_SETUP_THREADS / 32];
   __shared__ pf_task tk[16];
   pf_pdl_trigger();  // let the event kernel start streaming its data now
 #ifdef PF_SETUP_TRACE
@@ -96,7 +118,8 @@ extern "C" __global__ void __launch_bounds__(PF_SETUP_THREADS) pf_setup_kernel(c
 #else
 #define PF_TRACE(tag)
 #endif
-  const int k = blockIdx.x;
+  const unsigned rank = PF_SETUP_CLUSTER > 1 ? pf_cluster_rank() : 0u;
+  const int k = blockIdx.x / PF_SETUP_CLUSTER;
   double* P = pf_sdyn;
   double* S = pf_sdyn + PF_NP;
   // K = 1: parameters arrive inline in the kernel arguments (constant bank,
@@ -108,74 +131,101 @@ extern "C" __global__ void __launch_bounds__(PF_SETUP_THREADS) pf_setup_kernel(c
   for (int i = threadIdx.x; i < nt * (int)(sizeof(pf_task) / 8); i += blockDim.x)
     reinterpret_cast<pf_u64*>(tk)[i] = reinterpret_cast<const pf_u64*>(a.tasks)[i];
   pf_krec* r = a.rec + k;
-  if (threadIdx.x == 0) pf_rec_init(r);
+  if (threadIdx.x == 0 && rank == 0) pf_rec_init(r);
   pf_math_init();  // includes __syncthreads
+  // the record is initialised before any CTA of the cluster reports into it
+  if (PF_SETUP_CLUSTER > 1) pf_cluster_sync();
   PF_TRACE("init");
   pf_ctx cx;
   cx.err = 0;
-  pf_cnt cnt;
+  pf_cnt cnt;        // clamps met on this CTA's grid points
   pf_cnt_init(cnt);
-  pf_stage_pre(k, P, S, a.C, cx, cnt, threadIdx.x, blockDim.x);
+  pf_cnt cnt_stage;  // clamps met in the pre/post stages (every CTA runs them; rank 0 reports)
+  pf_cnt_init(cnt_stage);
+  pf_stage_pre(k, P, S, a.C, cx, cnt_stage, threadIdx.x, blockDim.x);
   PF_TRACE("pre");
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int t0 = 0;
   for (int level = 0; level < a.n_levels; ++level) {
     int t1 = t0;
     while (t1 < nt && tk[t1].level == level) ++t1;
-    const int nl = min(t1 - t0, 8);
-    // every midpoint sum of the level first (thread t: points t, t + 1024, ...)
-    pf_dd accl[8];
+    const int nl = min(t1 - t0, PF_SETUP_MAXQ);  // (coarse, fine) task pairs of the level's nodes
+    // every midpoint sum of the level first (this CTA's share of the points)
+    pf_dd x[PF_SETUP_MAXQ];
+#pragma unroll
+    for (int q = 0; q < PF_SETUP_MAXQ; ++q) x[q] = pf_dd_zero();
     for (int q = 0; q < nl; ++q) {
       const pf_task& T = tk[t0 + q];
       pf_dd acc = pf_dd_zero();
-      for (pf_u64 i = threadIdx.x; i < T.points; i += PF_SETUP_THREADS)
+      for (pf_u64 i = rank * PF_SETUP_THREADS + threadIdx.x; i < T.points;
+           i += PF_SETUP_THREADS * PF_SETUP_CLUSTER)
         acc = pf_dd_add_d(acc, pf_norm_point(T.node, i, T, P, S, a.C, cx, cnt));
-      accl[q] = acc;
+      x[q] = acc;
     }
-    // then all of the level's fixed-shape block reductions together, so
-    // their double-double latency chains overlap (warp trees, then one
-    // warp per sum over the 32 warp results)
-    pf_dd x[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) x[q] = q < nl ? accl[q] : pf_dd_zero();
+    PF_TRACE("points");
+    // warp trees of all the level's sums together (their latency chains overlap)
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) {
 #pragma unroll
-      for (int q = 0; q < 8; ++q)
-        if (q < nl) x[q] = pf_dd_add(x[q], pf_shfl_down_dd(x[q], d));
+      for (int q = 0; q < PF_SETUP_MAXQ; ++q) x[q] = pf_dd_add(x[q], pf_shfl_down_dd(x[q], d));
     }
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (lane == 0)
-      for (int q = 0; q < nl; ++q) wsum[q][warp] = x[q];
-    __syncthreads();
-    if (warp < nl) {
-      pf_dd y = lane < PF_SETUP_THREADS / 32 ? wsum[warp][lane] : pf_dd_zero();
 #pragma unroll
-      for (int d = 16; d > 0; d >>= 1) y = pf_dd_add(y, pf_shfl_down_dd(y, d));
+      for (int q = 0; q < PF_SETUP_MAXQ; ++q) wpart[level & 1][q][warp] = x[q];
+    PF_TRACE("wtree");
+    // warp partials of every rank visible cluster-wide (double-buffered by
+    // level parity: a rank cannot overwrite a buffer another rank may still
+    // read without first passing the next level's barrier)
+    if (PF_SETUP_CLUSTER > 1)
+      pf_cluster_sync();
+    else
+      __syncthreads();
+    PF_TRACE("csync");
+    // one warp per node: lanes 0-15 its coarse sum, lanes 16-31 its fine sum;
+    // lane l holds warp partial (l & 15) of every rank, combined over ranks by
+    // a fixed tree, then a 16-lane tree; lane 0 finishes the node
+    if (2 * warp < nl) {
+      const int q = 2 * warp + (lane >> 4);
+      const pf_dd* src = &wpart[level & 1][q][lane & 15];
+      pf_dd v[PF_SETUP_CLUSTER];
+#pragma unroll
+      for (int rk = 0; rk < PF_SETUP_CLUSTER; ++rk)
+        v[rk] = PF_SETUP_CLUSTER > 1 ? pf_dsmem_load_dd(src, (unsigned)rk) : *src;
+#pragma unroll
+      for (int w = 1; w < PF_SETUP_CLUSTER; w <<= 1)
+#pragma unroll
+        for (int rk = 0; rk + w < PF_SETUP_CLUSTER; rk += 2 * w) v[rk] = pf_dd_add(v[rk], v[rk + w]);
+      pf_dd y = v[0];
+#pragma unroll
+      for (int d = 8; d > 0; d >>= 1) y = pf_dd_add(y, pf_shfl_down_dd(y, d));
       // midpoint_sum returns static_cast<double>(sum) * vol (pdf.hpp:173-175)
-      if (lane == 0) sums[warp] = __dmul_rn(pf_dd_to_double(y), tk[t0 + warp].vol);
+      const double sum = __dmul_rn(pf_dd_to_double(y), tk[t0 + q].vol);
+      const double fine = __shfl_down_sync(0xffffffffu, sum, 16);
+      if (lane == 0) pf_finish_norm(S, r, tk[t0 + q].node, sum, fine);
     }
-    __syncthreads();
-    PF_TRACE("sums");
-    if (threadIdx.x == 0)
-      for (int t = 0; t + 1 < nl; t += 2) pf_finish_norm(S, r, tk[t0 + t].node, sums[t], sums[t + 1]);
     __syncthreads();
     PF_TRACE("finish");
-    pf_stage_post(level, k, P, S, a.C, cx, cnt, threadIdx.x, blockDim.x);
+    pf_stage_post(level, k, P, S, a.C, cx, cnt_stage, threadIdx.x, blockDim.x);
     PF_TRACE("post");
     t0 = t1;
   }
   if (cx.err) atomicMin(&r->norm_error, cx.err);
   pf_cnt_flush(cnt, a.clamp);
+  if (rank == 0) pf_cnt_flush(cnt_stage, a.clamp);
   __syncthreads();
-  double* gS = a.S + (pf_u64)k * PF_SS;
-  double* gP = (double*)a.P + (pf_u64)k * PF_NP;
-  for (int i = threadIdx.x; i < PF_SS; i += blockDim.x) gS[i] = S[i];
-  for (int i = threadIdx.x; i < PF_NP; i += blockDim.x) gP[i] = P[i];
+  if (rank == 0) {
+    double* gS = a.S + (pf_u64)k * PF_SS;
+    double* gP = (double*)a.P + (pf_u64)k * PF_NP;
+    for (int i = threadIdx.x; i < PF_SS; i += blockDim.x) gS[i] = S[i];
+    for (int i = threadIdx.x; i < PF_NP; i += blockDim.x) gP[i] = P[i];
+  }
   PF_TRACE("store");
 #ifdef PF_SETUP_TRACE
   if (threadIdx.x == 0 && blockIdx.x == 0)
     for (int i = 0; i < ntr; ++i) printf("setup %-8s %lld\n", trn[i], trs[i]);
 #endif
+  // no CTA leaves while another may still read its shared memory
+  if (PF_SETUP_CLUSTER > 1) pf_cluster_sync();
 }
 
 // ---------------------------------------------------------------------------
@@ -268,18 +318,19 @@ extern "C" __global__ void __launch_bounds__(PF_THREADS) pf_norm_kernel(const __
 // ring of PF_NST stages (mbarrier completion), PF_NST - 1 copies in flight
 // while the warp computes; the compute loop reads the stage with
 // conflict-free LDS (lane l takes events 32 j + l), so the code stays small
-// and the memory stream never waits on the math.  Per lane: densities are
-// multiplied into a running product (one log per lane and sub-chunk), the
-// -log terms accumulate in double-double, and a fixed shuffle tree finishes
-// each chunk.  No block-level barrier in the main loop.  The first stages are
-// issued BEFORE waiting on the setup grid (PDL).
+// and the memory stream never waits on the math.  Per lane: a chunk
+// accumulator (pf_lacc_*: log-domain sum and mixture-factor product, or a
+// running density product) is carried over the chunk's sub-chunks and turned
+// into -log terms once per chunk, which are added EXACTLY into the lane's
+// fixed-point accumulator.  No block-level barrier in the main loop.  The
+// first stages are issued BEFORE waiting on the setup grid (PDL).
 
 #define PF_SUB (32 * PF_EPT)
 #ifndef PF_NSUB
 #define PF_NSUB 8  // sub-chunks per chunk: chunk = PF_NSUB * 32 * PF_EPT events
 #endif
 #ifndef PF_UNROLL
-#define PF_UNROLL 4  // events interleaved per lane in the event loop
+#define PF_UNROLL 8  // events interleaved per lane in the event loop
 #endif
 constexpr int pf_unroll = PF_UNROLL;
 #ifndef PF_NST
@@ -340,11 +391,48 @@ __device__ __noinline__ void pf_rescan(const pf_args& a, int k, pf_u64 base, int
   }
 }
 
-// this lane's terms over one staged sub-chunk for parameter set k.  FULL:
-// all 32 * PF_EPT events are real (every sub-chunk but the data's last).
-template <bool FULL>
-__device__ __forceinline__ pf_dd pf_stage_terms(const pf_args& a, int k, pf_u64 base, int lane,
-                                                const double* st, int n_valid) {
+// Per-lane chunk accumulator, carried across the PF_NSUB sub-chunks of a
+// chunk (in shared memory, fixed order) and turned into the chunk's sum of
+// -log terms once per chunk (pf_lacc_terms), so the one log per lane is
+// amortised over PF_NSUB * PF_EPT events:
+//   log domain: {sum of L, product of mixture factors F}  (F <= n_children)
+//   linear:     {m, e}: running density product m * 2^e   (pf_prod)
+//   binned:     double-double sum of chi-squared terms
+__device__ __forceinline__ pf_dd pf_lacc_merge(pf_dd x, pf_dd y) {
+#if PF_BINNED
+  return pf_dd_add(x, y);
+#elif PF_LOGFORM
+  return pf_dd{x.hi + y.hi, x.lo * y.lo};
+#else
+  pf_prod p;
+  p.m = x.hi;
+  p.e = (int)x.lo;
+  pf_prod_mul(p, y.hi);  // y.hi is a renormalised mantissa: inside 2^[-400, 400)
+  return pf_dd{p.m, (double)(p.e + (int)y.lo)};
+#endif
+}
+
+__device__ __forceinline__ pf_dd pf_lacc_terms(pf_dd x) {
+#if PF_BINNED
+  return x;
+#elif PF_LOGFORM
+  return pf_two_sum(-x.hi, -pf_log(x.lo));
+#else
+  pf_prod p;
+  p.m = x.hi;
+  p.e = (int)x.lo;
+  return pf_prod_neglog(p);
+#endif
+}
+
+#if !PF_BINNED && PF_LOGFORM
+// Rare path of the log-domain pass, out of line: one of this lane's events
+// in the sub-chunk is near the floor, overflows, is subnormal or NaN (or the
+// log form is unusable, e.g. a negative mixture coefficient).  The lane's
+// sub-chunk is recomputed with the reference's linear form for exactly those
+// events (engine.hpp:186-195: floor 1e-300 counted, non-finite index kept).
+__device__ __noinline__ pf_dd pf_lane_fixup(const pf_args& a, int k, pf_u64 base, int lane,
+                                            const double* st, int n_valid) {
   const double* P = a.P + (pf_u64)k * PF_NP;
   const double* S = a.S + (pf_u64)k * PF_SS;
   pf_ctx cx;
@@ -353,10 +441,82 @@ __device__ __forceinline__ pf_dd pf_stage_terms(const pf_args& a, int k, pf_u64 
   pf_cnt_init(cnt);
   pf_u32 floors = 0;
   bool bad = false;
+  double lsum = 0.0, fprod = 1.0;
+  for (int j = 0; j < PF_EPT; ++j) {
+    const int i = 32 * j + lane;
+    if (i >= n_valid) continue;
+    double ev[PF_NCOLS];
+#pragma unroll
+    for (int q = 0; q < PF_NCOLS; ++q) ev[q] = 0.0;
+#pragma unroll
+    for (int q = 0; q < PF_NLOAD; ++q) ev[pf_load_col(q)] = st[q * PF_SUB + i];
+    double Lv, Fv;
+    if (!pf_eval_event_log(ev, P, S, Lv, Fv)) {
+      double v = pf_eval_event(ev, P, S, a.C, cx, cnt);
+      if (v < PF_LOG_FLOOR) {
+        v = PF_LOG_FLOOR;
+        ++floors;
+      } else if (!(v <= 1.7976931348623157e308)) {
+        bad = true;
+        v = 1.0;
+      }
+      Lv = pf_log(v);
+      Fv = 1.0;
+    }
+    lsum += Lv;
+    fprod *= Fv;
+  }
+  if (cx.err) pf_rescan(a, k, base, lane, st, n_valid, true);
+  if (bad) pf_rescan(a, k, base, lane, st, n_valid, false);
+  if (floors) atomicAdd(&a.rec[k].floor_count, (pf_u64)floors);
+  pf_cnt_flush(cnt, a.clamp);
+  return pf_dd{lsum, fprod};
+}
+#endif
+
+// this lane's accumulator over one staged sub-chunk for parameter set k.
+// FULL: all 32 * PF_EPT events are real (every sub-chunk but the data's last).
+template <bool FULL>
+__device__ __forceinline__ pf_dd pf_stage_terms(const pf_args& a, int k, pf_u64 base, int lane,
+                                                const double* st, int n_valid) {
+  const double* P = a.P + (pf_u64)k * PF_NP;
+  const double* S = a.S + (pf_u64)k * PF_SS;
+#if !PF_BINNED && PF_LOGFORM
+  // log domain, optimistic: -log v = -(L + log F) with no per-event log and
+  // no per-event branch; the lane's sub-chunk is redone exactly (above) when
+  // any of its events fails the log-domain test
+  double lsum = 0.0, fprod = 1.0;
+  bool allok = true;
+#pragma unroll pf_unroll
+  for (int j = 0; j < PF_EPT; ++j) {
+    const int i = 32 * j + lane;
+    double ev[PF_NCOLS];
+#pragma unroll
+    for (int q = 0; q < PF_NCOLS; ++q) ev[q] = 0.0;
+#pragma unroll
+    for (int q = 0; q < PF_NLOAD; ++q) ev[pf_load_col(q)] = st[q * PF_SUB + i];
+    double Lv, Fv;
+    bool ok = pf_eval_event_log(ev, P, S, Lv, Fv);
+    if (!FULL && i >= n_valid) {
+      ok = true;
+      Lv = 0.0;
+      Fv = 1.0;
+    }
+    allok = allok && ok;
+    lsum += Lv;
+    fprod *= Fv;
+  }
+  if (!allok) return pf_lane_fixup(a, k, base, lane, st, FULL ? PF_SUB : n_valid);
+  return pf_dd{lsum, fprod};
+#else
+  pf_ctx cx;
+  cx.err = 0;
+  pf_cnt cnt;
+  pf_cnt_init(cnt);
+  pf_u32 floors = 0;
+  bool bad = false;
 #if PF_BINNED
   pf_dd acc = pf_dd_zero();
-#elif PF_LOGFORM
-  double lsum = 0.0, fprod = 1.0;
 #else
   pf_prod acc;
   pf_prod_init(acc);
@@ -364,38 +524,6 @@ __device__ __forceinline__ pf_dd pf_stage_terms(const pf_args& a, int k, pf_u64 
 #pragma unroll pf_unroll
   for (int j = 0; j < PF_EPT; ++j) {
     const int i = 32 * j + lane;
-#if !PF_BINNED && PF_LOGFORM
-    {
-      // log domain: -log v = -(L + log F) with no per-event log; events near
-      // the floor / overflow / subnormal range take the exact linear path
-      double ev[PF_NCOLS];
-#pragma unroll
-      for (int q = 0; q < PF_NCOLS; ++q) ev[q] = 0.0;
-#pragma unroll
-      for (int q = 0; q < PF_NLOAD; ++q) ev[pf_load_col(q)] = st[q * PF_SUB + i];
-      double Lv, Fv;
-      bool ok = pf_eval_event_log(ev, P, S, Lv, Fv);
-      if (!FULL && i >= n_valid) {
-        ok = true;
-        Lv = 0.0;
-        Fv = 1.0;
-      }
-      if (!ok) {
-        double v = pf_eval_event(ev, P, S, a.C, cx, cnt);
-        if (v < PF_LOG_FLOOR) {  // engine.hpp:190-193
-          v = PF_LOG_FLOOR;
-          ++floors;
-        } else if (!(v <= 1.7976931348623157e308)) {
-          bad = true;
-          v = 1.0;
-        }
-        Lv = pf_log(v);
-        Fv = 1.0;
-      }
-      lsum += Lv;
-      fprod *= Fv;
-    }
-#else
     double ev[PF_NCOLS];
 #pragma unroll
     for (int q = 0; q < PF_NCOLS; ++q) ev[q] = 0.0;
@@ -436,7 +564,6 @@ __device__ __forceinline__ pf_dd pf_stage_terms(const pf_args& a, int k, pf_u64 
     }
     pf_prod_mul(acc, v);
 #endif
-#endif  // log domain
   }
   if (cx.err) pf_rescan(a, k, base, lane, st, FULL ? PF_SUB : n_valid, true);
   if (bad) pf_rescan(a, k, base, lane, st, FULL ? PF_SUB : n_valid, false);
@@ -444,17 +571,10 @@ __device__ __forceinline__ pf_dd pf_stage_terms(const pf_args& a, int k, pf_u64 
   pf_cnt_flush(cnt, a.clamp);
 #if PF_BINNED
   return acc;
-#elif PF_LOGFORM
-  return pf_two_sum(-lsum, -pf_log(fprod));
 #else
-  return pf_prod_neglog(acc);
+  return pf_dd{acc.m, (double)acc.e};
 #endif
-}
-
-__device__ __forceinline__ pf_dd pf_warp_tree(pf_dd v) {
-#pragma unroll
-  for (int d = 16; d > 0; d >>= 1) v = pf_dd_add(v, pf_shfl_down_dd(v, d));
-  return v;
+#endif
 }
 
 #ifndef PF_EVENT_MIN_BLOCKS
@@ -476,6 +596,8 @@ extern "C" __global__ void __launch_bounds__(PF_EV_THREADS, PF_EVENT_MIN_BLOCKS)
     pf_fence_mbar_init();
   }
   pf_math_init();  // includes __syncthreads (barrier inits visible)
+  // static chunk assignment: warp gw takes chunks gw, gw + nw, ... (a
+  // dynamic ticket was measured no faster and slower to start)
   const int gw = blockIdx.x * PF_EV_WARPS + warp;
   const int nw = gridDim.x * PF_EV_WARPS;
   const int my_chunks = gw < a.n_chunks ? (a.n_chunks - 1 - gw) / nw + 1 : 0;
@@ -508,15 +630,15 @@ extern "C" __global__ void __launch_bounds__(PF_EV_THREADS, PF_EVENT_MIN_BLOCKS)
       pf_dd t = full ? pf_stage_terms<true>(a, k, base, lane, my + s * PF_STAGE, n_valid)
                      : pf_stage_terms<false>(a, k, base, lane, my + s * PF_STAGE, n_valid);
       pf_dd* slot = accs + k * PF_EV_THREADS + threadIdx.x;
-      *slot = first ? t : pf_dd_add(*slot, t);
+      *slot = first ? t : pf_lacc_merge(*slot, t);
     }
     __syncwarp();
     if (w + PF_NST - 1 < W) issue(w + PF_NST - 1);  // refills the stage read at w - 1
     if ((w % PF_NSUB) == PF_NSUB - 1) {
-      // chunk done: each lane adds its double-double chunk value EXACTLY into
-      // its own fixed-point accumulator (integer adds, no shuffles/atomics)
+      // chunk done: each lane adds its chunk value EXACTLY into its own
+      // fixed-point accumulator (integer adds, no shuffles/atomics)
       for (int k = 0; k < a.K; ++k) {
-        const pf_dd t = accs[k * PF_EV_THREADS + threadIdx.x];
+        const pf_dd t = pf_lacc_terms(accs[k * PF_EV_THREADS + threadIdx.x]);
         pf_fxl A;
 #pragma unroll
         for (int i = 0; i < PF_FX_DIGITS; ++i) A.d[i] = fxs[(k * PF_FX_DIGITS + i) * PF_EV_THREADS + threadIdx.x];
@@ -527,16 +649,31 @@ extern "C" __global__ void __launch_bounds__(PF_EV_THREADS, PF_EVENT_MIN_BLOCKS)
       }
     }
   }
-  // warp totals (integer shuffles) into the call's accumulators
+  // block totals: warp shuffles, the block's warps through shared memory,
+  // then ONE binned atomic set per block (exact integer digits)
+  __shared__ long long bfx[PF_EV_WARPS][PF_FX_DIGITS];
   for (int k = 0; k < a.K; ++k) {
     pf_fxl A;
 #pragma unroll
     for (int i = 0; i < PF_FX_DIGITS; ++i) A.d[i] = fxs[(k * PF_FX_DIGITS + i) * PF_EV_THREADS + threadIdx.x];
-    pf_fxl_flush(A, a.rec[k].fx);
+    pf_fxl_warp_sum(A);
+    if (lane == 0)
+#pragma unroll
+      for (int i = 0; i < PF_FX_DIGITS; ++i) bfx[warp][i] = A.d[i];
+    __syncthreads();
+    if (threadIdx.x < PF_FX_DIGITS) {
+      long long v = 0;
+#pragma unroll
+      for (int w = 0; w < PF_EV_WARPS; ++w) v += bfx[w][threadIdx.x];
+      if (v)
+        atomicAdd((unsigned long long*)(a.fxbins + ((pf_u64)k * PF_FX_BINS + blockIdx.x % PF_FX_BINS) *
+                                                       PF_FX_BIN_STRIDE + threadIdx.x),
+                  (unsigned long long)v);
+    }
+    __syncthreads();
   }
   // the last block to finish publishes every parameter set
   __shared__ int s_last;
-  __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
     s_last = atomicAdd(a.done, 1u) == gridDim.x - 1;
@@ -545,6 +682,19 @@ extern "C" __global__ void __launch_bounds__(PF_EV_THREADS, PF_EVENT_MIN_BLOCKS)
   if (!s_last) return;
   __threadfence();
   if (threadIdx.x == 0) *a.done = 0u;  // self-resetting (bench relaunches)
+  for (int k = 0; k < a.K; ++k) {
+    if (threadIdx.x < PF_FX_DIGITS) {
+      long long* bins = a.fxbins + (pf_u64)k * PF_FX_BINS * PF_FX_BIN_STRIDE + threadIdx.x;
+      long long v = 0;
+#pragma unroll 8
+      for (int b = 0; b < PF_FX_BINS; ++b) {
+        v += (long long)__ldcg((const unsigned long long*)(bins + b * PF_FX_BIN_STRIDE));
+        bins[b * PF_FX_BIN_STRIDE] = 0ll;  // self-resetting
+      }
+      a.rec[k].fx[threadIdx.x] = v;
+    }
+  }
+  __syncthreads();
   for (int k = 0; k < a.K; ++k) pf_publish(a, k, threadIdx.x, blockDim.x);
 }
 

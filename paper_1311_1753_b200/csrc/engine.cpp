@@ -3,9 +3,12 @@
 // setData (engine.hpp:139-154 of the reference): finalize the graph, upload
 // the EventTable once into HBM (column-major, one shard per device), compile
 // the fused evaluator with NVRTC for sm_100a and capture one CUDA graph per
-// batch width:  H2D params -> pre -> norm levels -> event -> final -> D2H.
+// batch width:  setup (validity + normalisation; or pre + norm levels for big
+// grids) -PDL-> event pass, which publishes the result itself.  Parameters
+// and results travel through mapped host memory (K = 1: parameters inline in
+// the kernel arguments), so there are no memcpy nodes.
 // eval_metric (engine.hpp:165-218): host-side contract checks and penalty
-// rules, one graph launch per shard, one synchronisation, one small D2H.
+// rules, one graph launch per shard, one synchronisation.
 #include "engine.hpp"
 
 #include <nvrtc.h>
@@ -49,11 +52,11 @@ ModuleCache& cache() {
 }  // namespace
 
 // TMA stage ring (PF_EV_WARPS x PF_NST stages x PF_NLOAD x 32 PF_EPT doubles)
-// plus the per-lane double-double accumulators of K parameter sets
+// plus the per-lane chunk and fixed-point accumulators of K parameter sets
 size_t event_smem(const Layout& L, int K) {
-  const size_t stages = static_cast<size_t>(kEventWarps) * kEventStages * L.load_cols.size() * 32 *
+  const size_t stages = static_cast<size_t>(kEventWarps) * L.nst * L.load_cols.size() * 32 *
                         static_cast<size_t>(L.ept) * sizeof(double);
-  // per lane and parameter set: a double-double chunk accumulator (16 B)
+  // per lane and parameter set: a chunk accumulator (16 B, pf_lacc_*)
   // and an exact fixed-point accumulator (6 x 8 B)
   return stages + static_cast<size_t>(K) * 32 * kEventWarps * (16 + 48);
 }
@@ -88,19 +91,26 @@ const Module* load_module(const Layout& L, int device) {
 }
 
 void launch(cudaKernel_t k, dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args& a,
-            bool pdl = false) {
+            bool pdl = false, int cluster = 1) {
   void* args[] = {&a};
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
+  cfg.attrs = attr;
   if (pdl) {  // programmatic dependent launch: overlaps this grid's start with its predecessor
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    attr[cfg.numAttrs].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[cfg.numAttrs].val.programmaticStreamSerializationAllowed = 1;
+    ++cfg.numAttrs;
+  }
+  if (cluster > 1) {  // thread-block cluster (distributed shared memory)
+    attr[cfg.numAttrs].id = cudaLaunchAttributeClusterDimension;
+    attr[cfg.numAttrs].val.clusterDim.x = static_cast<unsigned>(cluster);
+    attr[cfg.numAttrs].val.clusterDim.y = 1;
+    attr[cfg.numAttrs].val.clusterDim.z = 1;
+    ++cfg.numAttrs;
   }
   ck(cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(k), args), "cudaLaunchKernelEx");
 }
@@ -195,7 +205,10 @@ Model::Model(const pf_graph& g, const pf_data& d, uint32_t grid_points, const pf
   build_tasks(grid_points);
   double norm_work = 0;
   for (const Task& t : tasks_) norm_work += static_cast<double>(t.points) * subtree_cost(pg_, t.node);
-  small_norms_ = norm_work <= kSmallNormWork && setup_smem_bytes() <= 48 * 1024 && tasks_.size() <= 16;
+  int most_in_level = 0;
+  for (int n : level_n_tasks_) most_in_level = std::max(most_in_level, n);
+  small_norms_ = norm_work <= kSmallNormWork && setup_smem_bytes() <= 48 * 1024 && tasks_.size() <= 16 &&
+                 most_in_level <= L_.setup_maxq;
 
   ck(cudaSetDevice(opt.device), "cudaSetDevice");
   // parameters and results live in mapped (zero-copy) pinned memory: the
@@ -241,6 +254,9 @@ Model::Model(const pf_graph& g, const pf_data& d, uint32_t grid_points, const pf
     ck(cudaMalloc(&sh.d_partials, 16 * part_elems), "cudaMalloc partials");
     ck(cudaMalloc(&sh.d_done, sizeof(uint32_t)), "cudaMalloc done");
     ck(cudaMemset(sh.d_done, 0, sizeof(uint32_t)), "memset done");
+    const size_t bins = sizeof(int64_t) * kMaxBatch * kFxBins * 16;
+    ck(cudaMalloc(&sh.d_fxbins, bins), "cudaMalloc fxbins");
+    ck(cudaMemset(sh.d_fxbins, 0, bins), "memset fxbins");
     ck(cudaMalloc(&sh.d_rec, sizeof(KRec) * kMaxBatch), "cudaMalloc rec");
     ck(cudaMalloc(&sh.d_clamp, sizeof(uint64_t) * 2 * std::max(L_.n_poly, 1)), "cudaMalloc clamp");
     ck(cudaMemset(sh.d_clamp, 0, sizeof(uint64_t) * 2 * std::max(L_.n_poly, 1)), "memset clamp");
@@ -289,6 +305,7 @@ Model::~Model() {
     cudaFree(sh.d_tasks);
     cudaFree(sh.d_partials);
     cudaFree(sh.d_done);
+    cudaFree(sh.d_fxbins);
     cudaFree(sh.d_rec);
     cudaFree(sh.d_clamp);
     cudaFreeHost(sh.h_out);
@@ -382,6 +399,7 @@ Args Model::base_args(Shard& sh, int K) {
   a.n_tasks = static_cast<int>(tasks_.size());
   a.partials = sh.d_partials;
   a.done = sh.d_done;
+  a.fxbins = sh.d_fxbins;
   a.rec = sh.d_rec;
   a.total_content = total_content_;
   // norm-stage clamps are counted once (shard 0); the others discard them
@@ -398,10 +416,19 @@ cudaGraphExec_t Model::graph_for(Shard& sh, int K) {
   ck(cudaSetDevice(sh.device), "cudaSetDevice");
   Args a = base_args(sh, K);
   int kernels = 0;
+  // never more event blocks per SM than are co-resident (wide stages or a big
+  // K need more shared memory): a persistent grid with a second partial wave
+  // would leave SMs idle at the end
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, reinterpret_cast<const void*>(sh.mod->event),
+                                                    32 * kEventWarps, event_smem(L_, K)) != cudaSuccess ||
+      occ < 1)
+    occ = kEventBlocksPerSM;
   cudaGraph_t graph;
   ck(cudaStreamBeginCapture(sh.stream, cudaStreamCaptureModeThreadLocal), "begin capture");
   if (small_norms_) {
-    launch(sh.mod->setup, dim3(K), dim3(512), setup_smem_bytes(), sh.stream, a);
+    launch(sh.mod->setup, dim3(K * L_.setup_cluster), dim3(512), setup_smem_bytes(), sh.stream, a, false,
+           L_.setup_cluster);
     ++kernels;
   } else {
     launch(sh.mod->pre, dim3(K), dim3(256), 0, sh.stream, a);
@@ -423,9 +450,10 @@ cudaGraphExec_t Model::graph_for(Shard& sh, int K) {
     // many chunks, so its TMA ring streams without restarts
     int per_sm = kEventBlocksPerSM;
     if (const char* env = std::getenv("PFB200_EV_BLOCKS")) per_sm = std::max(1, std::atoi(env));
+    const size_t smem = event_smem(L_, K);
+    per_sm = std::min(per_sm, occ);
     const int grid = std::max(1, std::min((sh.n_chunks + kEventWarps - 1) / kEventWarps,
                                           sm_count(sh.device) * per_sm));
-    const size_t smem = event_smem(L_, K);
     // the event pass closes its own reduction tree and publishes the results
     launch(sh.mod->event, dim3(grid), dim3(32 * kEventWarps), smem, sh.stream, e, /*pdl=*/true);
     kernels += 1;
@@ -503,7 +531,7 @@ void Model::run(const double* params, int K, std::vector<Raw>& out, bool partial
       cudaKernelNodeParams kp = {};
       const bool setup = small_norms_;
       kp.func = reinterpret_cast<void*>(setup ? sh.mod->setup : sh.mod->pre);
-      kp.gridDim = dim3(1);
+      kp.gridDim = dim3(setup ? L_.setup_cluster : 1);
       kp.blockDim = dim3(setup ? 512 : 256);
       kp.sharedMemBytes = setup ? static_cast<unsigned>(setup_smem_bytes()) : 0u;
       Args inl = sh.first_args;

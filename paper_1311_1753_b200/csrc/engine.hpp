@@ -18,8 +18,8 @@ namespace pfb {
 constexpr double kPenaltyValue = 1e300;  // engine.hpp:52
 constexpr int kMaxBatch = 16;            // parameter sets per launch
 constexpr int kEventWarps = 2;           // warps per event-pass block (PF_EV_WARPS)
-constexpr int kEventStages = 3;          // TMA stages per warp (PF_NST)
 constexpr int kEventBlocksPerSM = 8;     // resident event blocks per SM (PF_EVENT_MIN_BLOCKS)
+constexpr int kFxBins = 32;               // PF_FX_BINS (x 16 int64 per bin)
 constexpr double kSmallNormWork = 65536; // raw evaluations: single-CTA setup path
 
 // host mirrors of the device structs (pf_device.cuh); layouts must match
@@ -81,6 +81,7 @@ struct Args {
   uint64_t* clamp;
   double total_content;
   uint32_t* done;
+  int64_t* fxbins;
   int npin;
   int pad1;
   double pin[64];
@@ -109,6 +110,7 @@ struct Shard {
   Task* d_tasks = nullptr;  // all levels, concatenated
   void* d_partials = nullptr;
   uint32_t* d_done = nullptr;   // finished-block counter of the event pass
+  int64_t* d_fxbins = nullptr;  // kMaxBatch x kFxBins x 16 binned digits of the event pass
   KRec* d_rec = nullptr;
   uint64_t* d_clamp = nullptr;  // [n_poly counted | n_poly discarded]
   Out* h_out = nullptr;         // mapped, kMaxBatch

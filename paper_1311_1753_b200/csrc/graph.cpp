@@ -312,7 +312,22 @@ Program finalize(const pf_graph& g, int n_data_obs, const int32_t* data_obs, int
   for (auto& node : pg.nodes)
     if (node.kind == PF_SUM)
       for (int c : node.children) pg.nodes[c].normalised = true;
-  // levels: 1 + max level of normalised strict descendants
+  // An AddPdf whose children are all normalised over its own box needs no
+  // grid of its own: midpoint_sum (pdf.hpp:148-176) is linear and AddPdf::raw
+  // (pdf.hpp:368-379) is sum_i c_i raw_i / norm_i, so its coarse and fine sums
+  // are the children's sums weighted by c_i / norm_i (equal up to rounding,
+  // ~1e-16 relative).  It completes in its children's level (no extra level).
+  for (auto& node : pg.nodes) {
+    if (node.kind != PF_SUM || !node.normalised) continue;
+    bool same = true;
+    for (int c : node.children) {
+      const Node& ch = pg.nodes[c];
+      same = same && ch.normalised && ch.box.size() == node.box.size();
+      for (size_t d = 0; same && d < node.box.size(); ++d) same = ch.box[d].var == node.box[d].var;
+    }
+    node.folded = same;
+  }
+  // levels: 1 + max level of normalised strict descendants (folded: their max)
   std::function<int(int)> max_desc_level = [&](int id) -> int {
     int best = -1;
     for (int c : pg.nodes[id].children) {
@@ -320,7 +335,7 @@ Program finalize(const pf_graph& g, int n_data_obs, const int32_t* data_obs, int
       if (pg.nodes[c].normalised) sub = std::max(sub, pg.nodes[c].level);
       best = std::max(best, sub);
     }
-    if (pg.nodes[id].normalised) pg.nodes[id].level = best + 1;
+    if (pg.nodes[id].normalised) pg.nodes[id].level = pg.nodes[id].folded ? std::max(best, 0) : best + 1;
     return best;
   };
   max_desc_level(0);

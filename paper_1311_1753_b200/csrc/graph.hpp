@@ -55,6 +55,7 @@ struct Node {
   std::vector<BoxDim> box;      // resolve_box (pdf.hpp:562-607)
   bool normalised = false;      // root or child of an AddPdf (pdf.hpp:107-132)
   int level = -1;               // normalisation level (0 = no normalised descendants)
+  bool folded = false;          // AddPdf normalised from its children's grid sums (no grid)
   int parent = -1;
 };
 
