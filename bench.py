@@ -1,20 +1,23 @@
 #!/usr/bin/env python3
 """bench.py — NLL evaluation throughput of the B200 engine (BASELINE.json metric).
 
-Workload (N=1): BASELINE config 2 — AddPdf(GaussianPdf, ExpPdf) unbinned NLL
-on 1e7 synthetic toy events in one observable x in [0, 10], grid 1024.
-One step = one full eval_metric call (parameter H2D, normalisation integrals,
-fused per-event pass, deterministic reduction, result D2H).
+Workload (default, N=1): BASELINE config 2 — AddPdf(GaussianPdf, ExpPdf)
+unbinned NLL on 1e7 synthetic events per GPU, x in [0, 10], grid 1024.
+One step = one full eval_metric call (validity, normalisation integrals,
+fused per-event pass, exact reduction, result on the host).
+--config C1|C3|C4 selects the other BASELINE configurations
+(paper_1311_1753_b200/workloads.py).
 
-  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+  python bench.py [--gpus N --steps K --warmup W] [--config C2] [--impl reference]
 
-N > 1 (torchrun, one rank per GPU): weak scaling — every rank owns a 1e7-event
-shard (a subtree of the global reduction tree) of an N x 1e7-event data set;
-the 16-byte double-double partials are all-gathered over NCCL and combined in
-a fixed order, so the global NLL is bitwise identical for every N.
+N > 1 (torchrun, one rank per GPU): every rank owns its own events (weak
+scaling: 1e7 per GPU for C2; strong: the C3 total split N ways); each rank's
+exact fixed-point digits (48 bytes) are all-gathered over NCCL and combined
+exactly, so the global value does not depend on the combine order.
 
 --impl reference: the reference's own BoundModel::eval_metric (oracle/_ref,
-compiled from /root/reference's unmodified headers) on the host cores.
+compiled from /root/reference's unmodified headers) on the host cores; for
+ArgusPdf (C3), which the reference lacks, the C restatement (oracle port).
 """
 from __future__ import annotations
 
@@ -32,38 +35,19 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-EVENTS_PER_GPU = 10_000_000
-GRID = 1024
-TRUTH = dict(m=5.0, s=0.8, a=-0.6, f=0.3)
-START = dict(m=4.8, s=1.0, a=-0.5, f=0.4)
+from paper_1311_1753_b200.workloads import WORKLOADS  # noqa: E402
+
+# C2 (the default workload), kept importable for tools/
+START = WORKLOADS["C2"].start
 
 
 def make_events(n: int, seed: int = 11) -> np.ndarray:
-    """Toy events of the C2 shape: f * Gauss(5, 0.8) + (1-f) * Exp(-0.6),
-    truncated to [0, 10] (exact inverse-CDF sampling, numpy PCG64)."""
-    rng = np.random.default_rng(seed)
-    u = rng.random(n)
-    sig = rng.random(n) < TRUTH["f"]
-    a = TRUTH["a"]
-    # truncated exponential on [0, 10]
-    xe = np.log1p(u * np.expm1(a * 10.0)) / a
-    # truncated gaussian by rejection-free clipping of a wide draw
-    xg = rng.normal(TRUTH["m"], TRUTH["s"], n)
-    bad = (xg < 0) | (xg > 10)
-    while bad.any():
-        xg[bad] = rng.normal(TRUTH["m"], TRUTH["s"], int(bad.sum()))
-        bad = (xg < 0) | (xg > 10)
-    return np.where(sig, xg, xe)
+    return WORKLOADS["C2"].columns(n, seed)
 
 
 def build_model(pf):
-    x = pf.new_observable("x", 0.0, 10.0)
-    m = pf.new_parameter("m", START["m"], 0.1, 0.0, 10.0)
-    s = pf.new_parameter("s", START["s"], 0.1, 0.1, 5.0)
-    a = pf.new_parameter("a", START["a"], 0.1, -5.0, 5.0)
-    f = pf.new_parameter("f", START["f"], 0.01, 0.0, 1.0)
-    pdf = pf.add_pdf("sigbkg", [pf.gaussian_pdf("sig", x, m, s), pf.exp_pdf("bkg", x, a)], [f])
-    return x, pdf
+    obs, pdf = WORKLOADS["C2"].build(pf)
+    return obs[0], pdf
 
 
 class ClockSampler:
@@ -156,23 +140,27 @@ def ncu_traffic():
     return None if r is None or w is None else (r + w) * 1e6
 
 
-def cpu_baseline(pdf, x, xs, steps=4):
-    """The reference (oracle/_ref) on a bounded sample, all host threads."""
+def cpu_side(W, pf, obs, pdf, cols, metric, fit=True, steps=3):
+    """The reference (oracle/_ref, all host threads) — or, for ArgusPdf
+    models it cannot express, the C restatement (oracle port, one thread) —
+    on a bounded sample of the same workload: per-call throughput and one
+    full fit from the start point."""
     import oracle
-    from paper_1311_1753_b200 import parfit as pf
     threads = os.cpu_count() or 1
-    sample = min(len(xs), 2_000_000)
-    ds = pf.UnbinnedDataSet.from_columns([x], xs[:sample])
-    if oracle.Reference.available():
-        kind, ev = "reference", oracle.Reference(pdf, ds, GRID)
-        call = lambda p: ev.eval(p, 0, threads)  # noqa: E731
+    if W.unit == "bins":
+        sample = min(cols.shape[-1], 100_000)
+        ds = W.data(pf, obs, sample)
     else:
-        kind, ev = "port", oracle.Oracle(pdf, ds, GRID)
-        threads = 1
-        call = lambda p: ev.eval(p, 0)  # noqa: E731
-    p0 = [START["f"], START["m"], START["s"], START["a"]]
-    names = ev.param_names()
-    p0 = [dict(f=START["f"], m=START["m"], s=START["s"], a=START["a"])[n] for n in names]
+        sample = min(cols.shape[-1], 2_000_000)
+        ds = pf.UnbinnedDataSet.from_columns(obs, cols[..., :sample])
+    use_ref = oracle.Reference.available() and W.name != "C3"
+    if use_ref:
+        kind, ev = "reference", oracle.Reference(pdf, ds, W.grid)
+        call = lambda p: ev.eval(p, metric, threads)  # noqa: E731
+    else:
+        kind, ev, threads = "port", oracle.Oracle(pdf, ds, W.grid), 1
+        call = lambda p: ev.eval(p, metric)  # noqa: E731
+    p0 = [W.start[n] for n in ev.param_names()]
     call(p0)
     t = time.perf_counter()
     for k in range(steps):
@@ -180,10 +168,43 @@ def cpu_baseline(pdf, x, xs, steps=4):
         p[0] += 1e-9 * (k + 1)  # jitter: the normalisation recomputes, as in FD probes
         call(p)
     dt = (time.perf_counter() - t) / steps
-    return {"value": sample / dt, "unit": "events/s", "cores": threads, "kind": kind,
-            "sample": f"{sample} events of the same toy data, {steps} eval_metric calls "
-                      f"(C2 model, grid {GRID}), params jittered 1e-9 per call",
-            "nll_evals_per_s": 1.0 / dt, "ms_per_eval": dt * 1e3}
+    out = {"value": sample / dt, "unit": f"{W.unit}/s", "cores": threads, "kind": kind,
+           "sample": f"{sample} {W.unit} of the same synthetic data, {steps} eval_metric calls "
+                     f"({W.name}, grid {W.grid}), params jittered 1e-9 per call",
+           "evals_per_s": 1.0 / dt, "ms_per_eval": dt * 1e3}
+    if fit and use_ref:
+        r = ev.fit(metric, threads)
+        out["fit"] = {"wall_s": r["wall_time_s"], "calls": int(r["calls"]), "status": int(r["status"]),
+                      "units": sample}
+    return out, ds
+
+
+def fit_leg(W, pf, obs, pdf, cols, device):
+    """GPU fit and reference fit (all host threads) of the same sample"""
+    import oracle
+    n = W.fit_n
+    if cols is None:
+        ds = W.data(pf, obs, n)
+    else:
+        n = min(n, cols.shape[-1])
+        ds = pf.UnbinnedDataSet.from_columns(obs, np.ascontiguousarray(cols[..., :n]))
+    bm = pf.BoundModel(pdf, ds, pf.GridSpec(W.grid), pf.Backend.gpus(1, device))
+    for p in bm.registry().parameters():  # start point
+        p.value = W.start[p.name]
+    r = pf.fit(bm, pf.MetricKind(W.metric))
+    out = {"units": n, "gpu_wall_s": r.wall_time_s, "gpu_calls": r.n_metric_calls, "gpu_status": int(r.status),
+           "params": dict(zip(r.names, r.params))}
+    if oracle.Reference.available() and W.name != "C3":
+        for p in bm.registry().parameters():  # the fit wrote its result back: same start
+            p.value = W.start[p.name]
+        threads = os.cpu_count() or 1
+        rr = oracle.Reference(pdf, ds, W.grid).fit(W.metric, threads)
+        out.update({"ref_wall_s": rr["wall_time_s"], "ref_calls": int(rr["calls"]),
+                    "ref_status": int(rr["status"]), "ref_threads": threads,
+                    "speedup": rr["wall_time_s"] / r.wall_time_s if r.wall_time_s > 0 else None,
+                    "max_rel_param_diff": float(max(abs(a - b) / max(abs(b), 1e-300)
+                                                    for a, b in zip(r.params, rr["params"])))})
+    return out
 
 
 def run_reference(args):
@@ -193,37 +214,47 @@ def run_reference(args):
         return
     import oracle
     from paper_1311_1753_b200 import parfit as pf
-    if not oracle.Reference.available():
+    W = WORKLOADS[args.config]
+    if not oracle.Reference.available() and W.name != "C3":
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libparfit_ref.so not built"}))
         return
-    x, pdf = build_model(pf)
-    n = EVENTS_PER_GPU
-    xs = make_events(n)
-    ds = pf.UnbinnedDataSet.from_columns([x], xs)
+    obs, pdf = W.build(pf)
+    n = args.events or W.default_n
+    if W.unit == "bins":
+        n = min(n, 100_000)  # one reference chi-squared call on 1e6 bins x Q=1024 takes ~7 s on 8 threads
+    elif W.name == "C3":
+        n = min(n, 2_000_000)
+    ds = W.data(pf, obs, n)
     threads = os.cpu_count() or 1
-    ref = oracle.Reference(pdf, ds, GRID)
-    names = ref.param_names()
-    p0 = [START[nm] for nm in names]
+    if W.name == "C3":  # ArgusPdf: not in the reference; the C restatement stands in
+        kind, ev, threads = "port", oracle.Oracle(pdf, ds, W.grid), 1
+        call = lambda p: ev.eval(p, W.metric)  # noqa: E731
+    else:
+        kind, ev = "reference", oracle.Reference(pdf, ds, W.grid)
+        call = lambda p: ev.eval(p, W.metric, threads)  # noqa: E731
+    p0 = [W.start[nm] for nm in ev.param_names()]
     for _ in range(args.warmup):
-        ref.eval(p0, 0, threads)
+        call(p0)
     t = time.perf_counter()
     for k in range(args.steps):
         p = list(p0)
         p[0] += 1e-9 * (k + 1)
-        ref.eval(p, 0, threads)
+        call(p)
     dt = (time.perf_counter() - t) / args.steps
     val = n / dt
+    metric_name = "NLL events/sec" if W.metric == 0 else "chi2 bins/sec"
     line = {
-        "impl": "reference", "metric": "NLL events/sec", "value": val, "unit": "events/s",
+        "impl": "reference", "metric": metric_name, "value": val, "unit": f"{W.unit}/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (numpy PCG64 seed 11 C2 toy)",
-        "config": {"workload": f"C2: AddPdf(GaussianPdf, ExpPdf) NLL, {n} events, grid {GRID}",
-                   "parallelism": f"{threads} host threads (Backend::with_threads)"},
-        "nll_evals_per_s": 1.0 / dt,
-        "cpu_baseline": {"value": val, "unit": "events/s", "cores": threads, "kind": "reference",
-                         "sample": f"full workload, {args.steps} eval_metric calls"},
-        "e2e": {"value": val, "unit": "events/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "higher_is_better": True, "scaling": W.scaling, "vs_baseline": None, "dtype": "f64",
+        "data": f"synthetic ({W.name}, numpy PCG64 seed 11)",
+        "config": {"workload": f"{W.name}: {W.description}, {n} {W.unit}, grid {W.grid}",
+                   "parallelism": f"{threads} host threads" + (" (Backend::with_threads)" if kind == "reference"
+                                                                else " (C restatement)")},
+        "evals_per_s": 1.0 / dt,
+        "cpu_baseline": {"value": val, "unit": f"{W.unit}/s", "cores": threads, "kind": kind,
+                         "sample": f"{n} {W.unit}, {args.steps} eval_metric calls"},
+        "e2e": {"value": val, "unit": f"{W.unit}/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
 
@@ -234,14 +265,17 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--events", type=int, default=EVENTS_PER_GPU)
+    ap.add_argument("--config", default="C2", choices=sorted(WORKLOADS))
+    ap.add_argument("--events", type=int, default=0, help="events (bins) per GPU; 0: the config's size")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-fit", action="store_true")
     ap.add_argument("--diag-no-flush", action="store_true",
                     help="diagnostics only: keep L2 warm between steps (never a reported number)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
         return
+    W = WORKLOADS[args.config]
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -254,23 +288,32 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     from paper_1311_1753_b200 import parfit as pf
-    x, pdf = build_model(pf)
-    n_per = args.events
-    n_total = n_per * world
-    xs = make_events(n_total)
-    ds = pf.UnbinnedDataSet.from_columns([x], xs)
-    bm = pf.BoundModel(pdf, ds, pf.GridSpec(GRID), pf.Backend.gpus(1, local), shard_index=rank,
-                       shard_count=world)
-    names = [p.name for p in bm.registry().parameters()]
-    params = np.array([START[nm] for nm in names])
+    obs, pdf = W.build(pf)
+    if W.scaling == "weak":
+        n_local = args.events or W.default_n
+        n_total = n_local * world
+    else:
+        n_total = args.events or W.default_n
+        n_local = n_total // world + (1 if rank < n_total % world else 0)
+    # every rank owns its own events (seed per rank); the exact digits of the
+    # ranks' partial sums are combined, so the order of combination is free
+    if W.unit == "bins":
+        ds = W.data(pf, obs, n_local, seed=11 + rank)
+        cols = None
+    else:
+        cols = W.columns(n_local, seed=11 + rank)
+        ds = pf.UnbinnedDataSet.from_columns(obs, cols)
+    bm = pf.BoundModel(pdf, ds, pf.GridSpec(W.grid), pf.Backend.gpus(1, local))
+    params = W.params(bm)
+    metric = pf.MetricKind(W.metric)
     import ctypes as C
     from paper_1311_1753_b200 import _abi
 
     def step_value(p):
         if world == 1:
-            return bm.eval_metric(p)
+            return bm.eval_metric(p, metric)
         import torch
-        fx, pen = bm.eval_partial(p)
+        fx, pen = bm.eval_partial(p, metric)
         t = torch.tensor(fx + [1 if pen else 0], dtype=torch.int64, device=f"cuda:{local}")
         out = [torch.empty_like(t) for _ in range(world)]
         dist.all_gather(out, t)  # 56 bytes per rank over NCCL
@@ -289,14 +332,14 @@ def main():
         res = _abi.pf_bench_result()
         st = _abi.pf_status()
         with sampler:
-            rc = pf.lib.pf_bench(bm._h, params.ctypes.data_as(C.POINTER(C.c_double)), params.size, 0,
+            rc = pf.lib.pf_bench(bm._h, params.ctypes.data_as(C.POINTER(C.c_double)), params.size, W.metric,
                                  args.steps, 0 if args.diag_no_flush else 1, C.byref(res), C.byref(st))
         if rc:
             raise RuntimeError(st.message.decode())
         launches = (res.kernels_per_step * args.steps)
         ms_step = res.step_ms_mean
         ev_ms = res.event_kernel_ms_mean
-        nll = res.metric
+        value = res.metric
         h2d, d2h = res.h2d_bytes_per_step, res.d2h_bytes_per_step
     else:
         import torch
@@ -305,7 +348,7 @@ def main():
             torch.cuda.synchronize()
             t = time.perf_counter()
             for _ in range(args.steps):
-                nll = step_value(params)
+                value = step_value(params)
             torch.cuda.synchronize()
             dist.barrier()
             dt = torch.tensor([time.perf_counter() - t], dtype=torch.float64, device=f"cuda:{local}")
@@ -338,44 +381,54 @@ def main():
             dist.destroy_process_group()
         return
 
-    events_per_s = n_total / (ms_step * 1e-3)
+    metric_name = "NLL events/sec" if W.metric == 0 else "chi2 bins/sec"
     line = {
-        "metric": "NLL events/sec", "value": events_per_s, "unit": "events/s",
+        "metric": metric_name, "value": n_total / (ms_step * 1e-3), "unit": f"{W.unit}/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (numpy PCG64 seed 11 C2 toy: 0.3 Gauss(5,0.8) + 0.7 Exp(-0.6) on [0,10])",
-        "config": {"workload": f"C2: AddPdf(GaussianPdf, ExpPdf) unbinned NLL, {n_per} events/GPU, "
-                               f"grid {GRID}, params at the fit start",
-                   "events_per_gpu": n_per, "global_events": n_total,
+        "higher_is_better": True, "scaling": W.scaling, "vs_baseline": None, "dtype": "f64",
+        "data": f"synthetic ({W.name}, numpy PCG64 seed 11 + rank; {W.description})",
+        "config": {"workload": f"{W.name}: {W.description}, {n_local} {W.unit}/GPU, grid {W.grid}, "
+                               f"params at the fit start",
+                   f"{W.unit}_per_gpu": n_local, f"global_{W.unit}": n_total,
                    "l2": "flushed (256 MiB device write) before every timed step",
                    "parallelism": f"dp{world}"},
-        "nll_evals_per_s": 1e3 / ms_step,
-        "nll": nll,
+        "evals_per_s": 1e3 / ms_step,
+        "metric_value": value,
         "gpu_launches": int(launches),
-        "e2e": {"value": n_total / e2e_s, "unit": "events/s", "h2d_bytes_per_step": int(h2d),
+        "e2e": {"value": n_total / e2e_s, "unit": f"{W.unit}/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_s * 1e3},
         "clocks": sampler.summary() if sampler else None,
     }
     if ev_ms:
-        algo_bytes = 8.0 * n_per  # one f64 column per event (EventTable layout)
+        algo_bytes = W.bytes_per_unit() * n_local  # EventTable columns read per call
         achieved = algo_bytes / (ev_ms * 1e-3) / 1e9
         line["roofline"] = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                            "frac": achieved / hbm_peak, "traffic": ncu_traffic(),
+                            "frac": achieved / hbm_peak,
+                            "traffic": ncu_traffic() if W.name == "C2" else None,
                             "traffic_source": "profiles/r1_event_kernel_ncu.txt (ncu --set full, 1 launch)",
                             "kernel": "pf_event_kernel", "kernel_ms": ev_ms,
                             "algorithmic_bytes_per_launch": algo_bytes,
                             "kernel_share_of_step": ev_ms / ms_step, "peak_kind": peak_kind}
-        # the event pass is issue/FP64-pipe limited, not HBM limited: report
-        # the ncu-measured pipe utilisation of the same capture beside it
-        fp64 = ncu_metric("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active")
-        issue = ncu_metric("smsp__issue_active.avg.pct_of_peak_sustained_active")
-        if fp64 is not None:
-            line["roofline"]["fp64_pipe_active_frac_ncu"] = fp64 / 100.0
-        if issue is not None:
-            line["roofline"]["issue_active_frac_ncu"] = issue / 100.0
+        if W.name == "C2":
+            # the event pass is issue/FP64-pipe limited, not HBM limited: the
+            # ncu-measured pipe utilisation of the same capture beside it
+            fp64 = ncu_metric("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active")
+            issue = ncu_metric("smsp__issue_active.avg.pct_of_peak_sustained_active")
+            if fp64 is not None:
+                line["roofline"]["fp64_pipe_active_frac_ncu"] = fp64 / 100.0
+            if issue is not None:
+                line["roofline"]["issue_active_frac_ncu"] = issue / 100.0
+    if world == 1 and not args.no_fit and W.name != "C3":  # C3: no reference fit to compare with
+        # full fit (fit.hpp:498-581) from the start point, GPU and reference
+        # on the same bounded sample (at 1e7 events the reference's absolute
+        # gradient tolerance is below the NLL's rounding noise and neither
+        # side converges before max_iterations)
+        line["fit"] = fit_leg(W, pf, obs, pdf, cols, local)
     if world == 1 and not args.no_cpu_baseline:
         try:
-            line["cpu_baseline"] = cpu_baseline(pdf, x, xs)
+            if cols is None:
+                cols = np.zeros((1, n_local))  # binned: the sample is regenerated
+            line["cpu_baseline"], _ = cpu_side(W, pf, obs, pdf, cols, W.metric, fit=False)
         except Exception as e:  # the baseline is reported, never required
             line["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
     print(json.dumps(line))

@@ -175,3 +175,55 @@ def test_reference_matches_on_random_points():
     r = oracle.Reference(pdf, ds)
     for p in ([0.4, -0.6, 5, 1], [0.1, -1.5, 4.2, 0.7], [0.9, -0.1, 6.1, 1.9]):
         assert close(bm.eval_metric(p), r.eval(p))
+
+
+# --- BASELINE configurations C3 / C4 at oracle-sized inputs -----------------
+from paper_1311_1753_b200.workloads import WORKLOADS  # noqa: E402
+
+
+def test_c3_gauss_argus_product_vs_oracle():
+    """C3 shape: ProdPdf(Gauss(x), Argus(y)), 2-D normalisation grid 1024 x 1024
+    (the GPU factorises the separable grid; the oracle walks all 5.2M points).
+    ArgusPdf has no reference code: parity is against the C restatement."""
+    W = WORKLOADS["C3"]
+    obs, pdf = W.build(pf)
+    ds = pf.UnbinnedDataSet.from_columns(obs, W.columns(20_011, seed=5))
+    bm = pf.BoundModel(pdf, ds, pf.GridSpec(W.grid))
+    o = oracle.Oracle(pdf, ds, W.grid)
+    names = [p.name for p in bm.registry().parameters()]
+    nodes = pf.GraphDesc(pdf, obs).preorder()
+    for pt in (W.start, W.truth, dict(m=5.3, s=0.8, m0=5.29, c=-35.0, p=1.2)):
+        p = [pt[n] for n in names]
+        got, want = bm.eval_metric(p), o.eval(p)
+        assert close(got, want), (pt, got, want)
+        norms, _, valid = o.norms()
+        assert valid[0] and close(nodes[0].cached_norm(), norms[0])
+
+
+def test_c3_floor_at_the_argus_endpoint():
+    """events at or beyond m0 have raw 0: floored at 1e-300 and counted"""
+    W = WORKLOADS["C3"]
+    obs, pdf = W.build(pf)
+    cols = W.columns(5000, seed=6)
+    cols[1, ::97] = W.truth["m0"]  # exactly at the endpoint
+    ds = pf.UnbinnedDataSet.from_columns(obs, cols)
+    bm = pf.BoundModel(pdf, ds, pf.GridSpec(W.grid))
+    o = oracle.Oracle(pdf, ds, W.grid)
+    p = [W.truth[n.name] for n in bm.registry().parameters()]
+    assert close(bm.eval_metric(p), o.eval(p))
+    assert bm.log_floor_count() == o.floor_count() > 0
+
+
+def test_c4_binned_convolution_vs_reference():
+    """C4 shape: BW (x) Gauss, Q = 1024, binned chi-squared (2000 bins here)"""
+    W = WORKLOADS["C4"]
+    obs, pdf = W.build(pf)
+    ds = W.data(pf, obs, 2000, seed=3)
+    bm = pf.BoundModel(pdf, ds, pf.GridSpec(W.grid))
+    ref = oracle.Reference(pdf, ds, W.grid) if oracle.Reference.available() else oracle.Oracle(pdf, ds, W.grid)
+    names = [p.name for p in bm.registry().parameters()]
+    for pt in (W.start, W.truth, dict(m=2.9, w=0.35, rm=0.01, rs=0.06)):
+        p = [pt[n] for n in names]
+        got = bm.eval_metric(p, pf.MetricKind.ChiSquared)
+        want = ref.eval(p, 1)
+        assert close(got, want), (pt, got, want)
