@@ -33,6 +33,7 @@ struct Layout {
   int setup_cluster = 8;      // CTAs of the setup kernel's thread-block cluster
   int nst = 3;                // TMA stages per event warp (PF_NST)
   int setup_maxq = 8;         // most midpoint sums in one level (PF_SETUP_MAXQ)
+  int lacc_n = 2;             // doubles of the per-lane chunk accumulator (PF_LACC_N)
   std::vector<int> load_cols; // data columns read per event
   std::vector<int> poly_index; // node -> clamp counter index (-1 otherwise)
   int n_poly = 0;

@@ -536,6 +536,21 @@ __device__ __forceinline__ double pf_one_plus_exp_neg(double x) {
   return 1.0 + __hiloint2double(__double2hiint(s) + (e << 20), __double2loint(s));
 }
 
+// A power factor of the log form (codegen.cpp log_factored) is a positive
+// normal in [2^-20, 2^21): its log is within 14.6 in magnitude, which bounds
+// sum_j pow_j log fac_j per call (pf_stage_post) without a per-event log.
+__device__ __forceinline__ bool pf_fac_in_range(double v) {
+  return ((unsigned)__double2hiint(v) >> 20) - 1003u < 41u;
+}
+
+// running product of power factors: mantissas in [1, 2) multiplied, binary
+// exponents summed (so products of any length neither over- nor underflow)
+__device__ __forceinline__ void pf_fac_accum(double& m, int& e, double v) {
+  const int hi = __double2hiint(v);
+  e += (hi >> 20) - 1023;
+  m *= __hiloint2double((hi & 0x000fffff) | 0x3ff00000, __double2loint(v));
+}
+
 // ----------------------------------------------------------------------------
 // TMA bulk copies (cp.async.bulk, global -> shared) completed on mbarriers.
 __device__ __forceinline__ unsigned pf_smem_addr(const void* p) {

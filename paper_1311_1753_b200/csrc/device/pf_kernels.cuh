@@ -393,46 +393,129 @@ __device__ __noinline__ void pf_rescan(const pf_args& a, int k, pf_u64 base, int
 
 // Per-lane chunk accumulator, carried across the PF_NSUB sub-chunks of a
 // chunk (in shared memory, fixed order) and turned into the chunk's sum of
-// -log terms once per chunk (pf_lacc_terms), so the one log per lane is
+// -log terms once per chunk (pf_lacc_terms), so the lane's logs are
 // amortised over PF_NSUB * PF_EPT events:
-//   log domain: {sum of L, product of mixture factors F}  (F <= n_children)
+//   log form 1: {sum of L, per power factor: mantissa product, exponent sum}
+//   log form 2: {sum of L, product of mixture factors F (F <= n_children)}
 //   linear:     {m, e}: running density product m * 2^e   (pf_prod)
 //   binned:     double-double sum of chi-squared terms
-__device__ __forceinline__ pf_dd pf_lacc_merge(pf_dd x, pf_dd y) {
+#ifndef PF_NFAC
+#define PF_NFAC 0
+#endif
+#ifndef PF_FSPLIT
+#define PF_FSPLIT 0
+#endif
+#define PF_NFAC_A (PF_NFAC > 0 ? PF_NFAC : 1)
+#if !PF_BINNED && PF_LOGFORM
+#define PF_LACC_N (1 + (PF_FSPLIT ? 2 : 1) * PF_NFAC)
+#else
+#define PF_LACC_N 2
+#endif
+struct pf_lacc {
+  double v[PF_LACC_N];
+};
+
+__device__ __forceinline__ pf_lacc pf_lacc_merge(pf_lacc x, const pf_lacc& y) {
 #if PF_BINNED
-  return pf_dd_add(x, y);
+  const pf_dd s = pf_dd_add(pf_dd{x.v[0], x.v[1]}, pf_dd{y.v[0], y.v[1]});
+  x.v[0] = s.hi;
+  x.v[1] = s.lo;
 #elif PF_LOGFORM
-  return pf_dd{x.hi + y.hi, x.lo * y.lo};
+  x.v[0] += y.v[0];
+#pragma unroll
+  for (int j = 0; j < PF_NFAC; ++j) {
+    if (PF_FSPLIT) {
+      x.v[1 + 2 * j] *= y.v[1 + 2 * j];  // mantissa products (< 2^64 per chunk lane)
+      x.v[2 + 2 * j] += y.v[2 + 2 * j];  // exponent sums (exact integers)
+    } else {
+      x.v[1 + j] *= y.v[1 + j];
+    }
+  }
 #else
   pf_prod p;
-  p.m = x.hi;
-  p.e = (int)x.lo;
-  pf_prod_mul(p, y.hi);  // y.hi is a renormalised mantissa: inside 2^[-400, 400)
-  return pf_dd{p.m, (double)(p.e + (int)y.lo)};
+  p.m = x.v[0];
+  p.e = (int)x.v[1];
+  pf_prod_mul(p, y.v[0]);  // y's mantissa is renormalised: inside 2^[-400, 400)
+  x.v[0] = p.m;
+  x.v[1] = (double)(p.e + (int)y.v[1]);
 #endif
+  return x;
 }
 
-__device__ __forceinline__ pf_dd pf_lacc_terms(pf_dd x) {
+// the chunk lane's sum of -log terms (double-double)
+__device__ __forceinline__ pf_dd pf_lacc_terms(const pf_lacc& x, const double* __restrict__ P) {
 #if PF_BINNED
-  return x;
+  return pf_dd{x.v[0], x.v[1]};
 #elif PF_LOGFORM
-  return pf_two_sum(-x.hi, -pf_log(x.lo));
+  double f = 0.0;
+#pragma unroll
+  for (int j = 0; j < PF_NFAC; ++j) {
+    if (PF_FSPLIT) {
+      const double e = x.v[2 + 2 * j];
+      f += pf_fac_pow(j, P) * (pf_log(x.v[1 + 2 * j]) + (e * PF_LN2_HI + e * PF_LN2_LO));
+    } else {
+      f += pf_log(x.v[1 + j]);
+    }
+  }
+  return pf_two_sum(-x.v[0], -f);
 #else
   pf_prod p;
-  p.m = x.hi;
-  p.e = (int)x.lo;
+  p.m = x.v[0];
+  p.e = (int)x.v[1];
   return pf_prod_neglog(p);
 #endif
 }
 
 #if !PF_BINNED && PF_LOGFORM
+// log-form event accumulation shared by the fast loop and the fix-up
+struct pf_lform {
+  double lsum;
+  double fm[PF_NFAC_A];
+  int fe[PF_NFAC_A];
+};
+
+__device__ __forceinline__ void pf_lform_init(pf_lform& A) {
+  A.lsum = 0.0;
+#pragma unroll
+  for (int j = 0; j < PF_NFAC_A; ++j) {
+    A.fm[j] = 1.0;
+    A.fe[j] = 0;
+  }
+}
+
+__device__ __forceinline__ void pf_lform_add(pf_lform& A, double Lv, const double* fac) {
+  A.lsum += Lv;
+#pragma unroll
+  for (int j = 0; j < PF_NFAC; ++j) {
+    if (PF_FSPLIT)
+      pf_fac_accum(A.fm[j], A.fe[j], fac[j]);
+    else
+      A.fm[j] *= fac[j];
+  }
+}
+
+__device__ __forceinline__ pf_lacc pf_lform_pack(const pf_lform& A) {
+  pf_lacc x;
+  x.v[0] = A.lsum;
+#pragma unroll
+  for (int j = 0; j < PF_NFAC; ++j) {
+    if (PF_FSPLIT) {
+      x.v[1 + 2 * j] = A.fm[j];
+      x.v[2 + 2 * j] = (double)A.fe[j];
+    } else {
+      x.v[1 + j] = A.fm[j];
+    }
+  }
+  return x;
+}
+
 // Rare path of the log-domain pass, out of line: one of this lane's events
 // in the sub-chunk is near the floor, overflows, is subnormal or NaN (or the
 // log form is unusable, e.g. a negative mixture coefficient).  The lane's
 // sub-chunk is recomputed with the reference's linear form for exactly those
 // events (engine.hpp:186-195: floor 1e-300 counted, non-finite index kept).
-__device__ __noinline__ pf_dd pf_lane_fixup(const pf_args& a, int k, pf_u64 base, int lane,
-                                            const double* st, int n_valid) {
+__device__ __noinline__ pf_lacc pf_lane_fixup(const pf_args& a, int k, pf_u64 base, int lane,
+                                              const double* st, int n_valid) {
   const double* P = a.P + (pf_u64)k * PF_NP;
   const double* S = a.S + (pf_u64)k * PF_SS;
   pf_ctx cx;
@@ -441,7 +524,8 @@ __device__ __noinline__ pf_dd pf_lane_fixup(const pf_args& a, int k, pf_u64 base
   pf_cnt_init(cnt);
   pf_u32 floors = 0;
   bool bad = false;
-  double lsum = 0.0, fprod = 1.0;
+  pf_lform A;
+  pf_lform_init(A);
   for (int j = 0; j < PF_EPT; ++j) {
     const int i = 32 * j + lane;
     if (i >= n_valid) continue;
@@ -450,8 +534,10 @@ __device__ __noinline__ pf_dd pf_lane_fixup(const pf_args& a, int k, pf_u64 base
     for (int q = 0; q < PF_NCOLS; ++q) ev[q] = 0.0;
 #pragma unroll
     for (int q = 0; q < PF_NLOAD; ++q) ev[pf_load_col(q)] = st[q * PF_SUB + i];
-    double Lv, Fv;
-    if (!pf_eval_event_log(ev, P, S, Lv, Fv)) {
+    double Lv, fac[PF_NFAC_A];
+    if (pf_eval_event_log(ev, P, S, Lv, fac)) {
+      pf_lform_add(A, Lv, fac);
+    } else {
       double v = pf_eval_event(ev, P, S, a.C, cx, cnt);
       if (v < PF_LOG_FLOOR) {
         v = PF_LOG_FLOOR;
@@ -460,24 +546,21 @@ __device__ __noinline__ pf_dd pf_lane_fixup(const pf_args& a, int k, pf_u64 base
         bad = true;
         v = 1.0;
       }
-      Lv = pf_log(v);
-      Fv = 1.0;
+      A.lsum += pf_log(v);
     }
-    lsum += Lv;
-    fprod *= Fv;
   }
   if (cx.err) pf_rescan(a, k, base, lane, st, n_valid, true);
   if (bad) pf_rescan(a, k, base, lane, st, n_valid, false);
   if (floors) atomicAdd(&a.rec[k].floor_count, (pf_u64)floors);
   pf_cnt_flush(cnt, a.clamp);
-  return pf_dd{lsum, fprod};
+  return pf_lform_pack(A);
 }
 #endif
 
 // this lane's accumulator over one staged sub-chunk for parameter set k.
 // FULL: all 32 * PF_EPT events are real (every sub-chunk but the data's last).
 template <bool FULL>
-__device__ __forceinline__ pf_dd pf_stage_terms(const pf_args& a, int k, pf_u64 base, int lane,
+__device__ __forceinline__ pf_lacc pf_stage_terms(const pf_args& a, int k, pf_u64 base, int lane,
                                                 const double* st, int n_valid) {
   const double* P = a.P + (pf_u64)k * PF_NP;
   const double* S = a.S + (pf_u64)k * PF_SS;
@@ -485,7 +568,8 @@ __device__ __forceinline__ pf_dd pf_stage_terms(const pf_args& a, int k, pf_u64 
   // log domain, optimistic: -log v = -(L + log F) with no per-event log and
   // no per-event branch; the lane's sub-chunk is redone exactly (above) when
   // any of its events fails the log-domain test
-  double lsum = 0.0, fprod = 1.0;
+  pf_lform A;
+  pf_lform_init(A);
   bool allok = true;
 #pragma unroll pf_unroll
   for (int j = 0; j < PF_EPT; ++j) {
@@ -495,19 +579,19 @@ __device__ __forceinline__ pf_dd pf_stage_terms(const pf_args& a, int k, pf_u64 
     for (int q = 0; q < PF_NCOLS; ++q) ev[q] = 0.0;
 #pragma unroll
     for (int q = 0; q < PF_NLOAD; ++q) ev[pf_load_col(q)] = st[q * PF_SUB + i];
-    double Lv, Fv;
-    bool ok = pf_eval_event_log(ev, P, S, Lv, Fv);
+    double Lv, fac[PF_NFAC_A];
+    bool ok = pf_eval_event_log(ev, P, S, Lv, fac);
     if (!FULL && i >= n_valid) {
       ok = true;
       Lv = 0.0;
-      Fv = 1.0;
+#pragma unroll
+      for (int f = 0; f < PF_NFAC_A; ++f) fac[f] = 1.0;
     }
     allok = allok && ok;
-    lsum += Lv;
-    fprod *= Fv;
+    pf_lform_add(A, Lv, fac);
   }
   if (!allok) return pf_lane_fixup(a, k, base, lane, st, FULL ? PF_SUB : n_valid);
-  return pf_dd{lsum, fprod};
+  return pf_lform_pack(A);
 #else
   pf_ctx cx;
   cx.err = 0;
@@ -569,11 +653,15 @@ __device__ __forceinline__ pf_dd pf_stage_terms(const pf_args& a, int k, pf_u64 
   if (bad) pf_rescan(a, k, base, lane, st, FULL ? PF_SUB : n_valid, false);
   if (floors) atomicAdd(&a.rec[k].floor_count, (pf_u64)floors);
   pf_cnt_flush(cnt, a.clamp);
+  pf_lacc x;
 #if PF_BINNED
-  return acc;
+  x.v[0] = acc.hi;
+  x.v[1] = acc.lo;
 #else
-  return pf_dd{acc.m, (double)acc.e};
+  x.v[0] = acc.m;
+  x.v[1] = (double)acc.e;
 #endif
+  return x;
 #endif
 }
 
@@ -584,8 +672,8 @@ extern "C" __global__ void __launch_bounds__(PF_EV_THREADS, PF_EVENT_MIN_BLOCKS)
   extern __shared__ __align__(16) unsigned char pf_dyn[];
   __shared__ __align__(8) pf_u64 bars[PF_EV_WARPS * PF_NST];
   double* stages = reinterpret_cast<double*>(pf_dyn);
-  pf_dd* accs = reinterpret_cast<pf_dd*>(stages + PF_EV_WARPS * PF_NST * PF_STAGE);  // [k][thread]
-  long long* fxs = reinterpret_cast<long long*>(accs + a.K * PF_EV_THREADS);  // [k][digit][thread]
+  double* accs = stages + PF_EV_WARPS * PF_NST * PF_STAGE;  // [k][PF_LACC_N][thread]
+  long long* fxs = reinterpret_cast<long long*>(accs + a.K * PF_LACC_N * PF_EV_THREADS);  // [k][digit][thread]
   for (int i = threadIdx.x; i < a.K * PF_FX_DIGITS * PF_EV_THREADS; i += PF_EV_THREADS) fxs[i] = 0;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -627,10 +715,17 @@ extern "C" __global__ void __launch_bounds__(PF_EV_THREADS, PF_EVENT_MIN_BLOCKS)
     const bool full = base + PF_SUB <= a.n_local;
     const int n_valid = full ? PF_SUB : (int)(a.n_local > base ? a.n_local - base : 0);
     for (int k = 0; k < a.K; ++k) {
-      pf_dd t = full ? pf_stage_terms<true>(a, k, base, lane, my + s * PF_STAGE, n_valid)
-                     : pf_stage_terms<false>(a, k, base, lane, my + s * PF_STAGE, n_valid);
-      pf_dd* slot = accs + k * PF_EV_THREADS + threadIdx.x;
-      *slot = first ? t : pf_lacc_merge(*slot, t);
+      pf_lacc t = full ? pf_stage_terms<true>(a, k, base, lane, my + s * PF_STAGE, n_valid)
+                       : pf_stage_terms<false>(a, k, base, lane, my + s * PF_STAGE, n_valid);
+      double* slot = accs + k * PF_LACC_N * PF_EV_THREADS + threadIdx.x;
+      if (!first) {
+        pf_lacc prev;
+#pragma unroll
+        for (int j = 0; j < PF_LACC_N; ++j) prev.v[j] = slot[j * PF_EV_THREADS];
+        t = pf_lacc_merge(prev, t);
+      }
+#pragma unroll
+      for (int j = 0; j < PF_LACC_N; ++j) slot[j * PF_EV_THREADS] = t.v[j];
     }
     __syncwarp();
     if (w + PF_NST - 1 < W) issue(w + PF_NST - 1);  // refills the stage read at w - 1
@@ -638,7 +733,10 @@ extern "C" __global__ void __launch_bounds__(PF_EV_THREADS, PF_EVENT_MIN_BLOCKS)
       // chunk done: each lane adds its chunk value EXACTLY into its own
       // fixed-point accumulator (integer adds, no shuffles/atomics)
       for (int k = 0; k < a.K; ++k) {
-        const pf_dd t = pf_lacc_terms(accs[k * PF_EV_THREADS + threadIdx.x]);
+        pf_lacc x;
+#pragma unroll
+        for (int j = 0; j < PF_LACC_N; ++j) x.v[j] = accs[(k * PF_LACC_N + j) * PF_EV_THREADS + threadIdx.x];
+        const pf_dd t = pf_lacc_terms(x, a.P + (pf_u64)k * PF_NP);
         pf_fxl A;
 #pragma unroll
         for (int i = 0; i < PF_FX_DIGITS; ++i) A.d[i] = fxs[(k * PF_FX_DIGITS + i) * PF_EV_THREADS + threadIdx.x];

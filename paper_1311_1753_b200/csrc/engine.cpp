@@ -56,9 +56,9 @@ ModuleCache& cache() {
 size_t event_smem(const Layout& L, int K) {
   const size_t stages = static_cast<size_t>(kEventWarps) * L.nst * L.load_cols.size() * 32 *
                         static_cast<size_t>(L.ept) * sizeof(double);
-  // per lane and parameter set: a chunk accumulator (16 B, pf_lacc_*)
-  // and an exact fixed-point accumulator (6 x 8 B)
-  return stages + static_cast<size_t>(K) * 32 * kEventWarps * (16 + 48);
+  // per lane and parameter set: a chunk accumulator (pf_lacc, lacc_n
+  // doubles) and an exact fixed-point accumulator (6 x 8 B)
+  return stages + static_cast<size_t>(K) * 32 * kEventWarps * (8 * L.lacc_n + 48);
 }
 
 namespace {

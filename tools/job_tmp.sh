@@ -1,4 +1,3 @@
-./paper_1311_1753_b200/_build/drop_in_test 2>&1 | tail -20
-python -m pytest tests -m gpu -q 2>&1 | tail -8
-timeout 600 python bench.py --config C3 --steps 10 --warmup 3 > gpurun_out/c3.json 2> gpurun_out/c3.err; tail -c 1800 gpurun_out/c3.json; tail -3 gpurun_out/c3.err
-timeout 600 python bench.py --steps 20 --warmup 3 --no-cpu-baseline > gpurun_out/c2.json 2> gpurun_out/c2.err; python -c "import json; d=json.load(open('gpurun_out/c2.json')); print(d['ms_per_step'], d['fit'])"; tail -3 gpurun_out/c2.err
+BENCH_ARGS="--config C3" bash tools/variants.sh "" "PFB200_EV_BLOCKS=10 PFB200_DEFINES=PF_EVENT_MIN_BLOCKS=10" "PFB200_NSUB=8" "PFB200_DEFINES=PF_UNROLL=4" 2>&1
+BENCH_ARGS="--config C4" bash tools/variants.sh "" "PFB200_NSUB=4" "PFB200_EV_BLOCKS=4" 2>&1
+bash tools/variants.sh "" 2>&1
