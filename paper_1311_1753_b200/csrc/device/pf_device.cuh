@@ -58,7 +58,7 @@ struct pf_task {  // one midpoint sum: node, n points per box dimension
 struct pf_out {
   double result;  // correctly rounded metric of this shard
   pf_u64 floor_count, first_nonfinite, first_event_error;
-  pf_u32 norm_error, pad;
+  pf_u32 norm_error, pad;  // pad: completion sequence number (pf_publish)
   long long fx[6];  // exact digits (combined across shards on the host)
 };
 
@@ -87,7 +87,7 @@ struct pf_args {
   pf_krec* rec;         // K records
   pf_u64* clamp;        // cumulative PolynomialPdf clamp counters per node
   double total_content; // binned: N_tot (engine.hpp:153)
-  pf_u32* done;         // finished-block counter of the event pass (self-resetting)
+  pf_u32* done;         // [finished-block counter (self-resetting), per-k completion sequence]
   long long* fxbins;    // K x PF_FX_BINS x 16: binned block digits (self-resetting)
   int npin;             // K = 1: parameters passed inline (pin[0..npin))
   int pad1;

@@ -63,6 +63,15 @@ __device__ void pf_publish(const pf_args& a, int k, int tid, int nt) {
   if (k == a.K - 1)
     for (int i = tid; i < PF_NPOLY; i += nt) a.hclamp[i] = __ldcg(a.clamp + i);
 #endif
+  // completion word: the host spins on it instead of synchronising the
+  // stream (every field above is visible to the host first)
+  __syncthreads();
+  if (tid == 0) {
+    const pf_u32 seq = a.done[1 + k] + 1u;
+    a.done[1 + k] = seq;
+    __threadfence_system();
+    *(volatile pf_u32*)&o->pad = seq;
+  }
 }
 
 // ---------------------------------------------------------------------------

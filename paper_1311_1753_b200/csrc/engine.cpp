@@ -204,7 +204,12 @@ Model::Model(const pf_graph& g, const pf_data& d, uint32_t grid_points, const pf
   const int n_cols_data = d.n_obs + (binned_ ? 2 : 0);
   build_tasks(grid_points);
   double norm_work = 0;
-  for (const Task& t : tasks_) norm_work += static_cast<double>(t.points) * subtree_cost(pg_, t.node);
+  for (const Task& t : tasks_) {
+    const Node& nd = pg_.nodes[t.node];
+    const bool pairs = nd.kind == PF_CONVOLUTION && nd.box.size() == 1;
+    norm_work += static_cast<double>(t.points) *
+                 (pairs ? 1.0 + subtree_cost(pg_, nd.children[1]) : subtree_cost(pg_, t.node));
+  }
   int most_in_level = 0;
   for (int n : level_n_tasks_) most_in_level = std::max(most_in_level, n);
   small_norms_ = norm_work <= kSmallNormWork && setup_smem_bytes() <= 48 * 1024 && tasks_.size() <= 16 &&
@@ -252,8 +257,8 @@ Model::Model(const pf_graph& g, const pf_data& d, uint32_t grid_points, const pf
     size_t part_elems = static_cast<size_t>(kMaxBatch) *
                         std::max<size_t>(std::max<size_t>(sh.n_chunks, max_norm_blocks_), 1);
     ck(cudaMalloc(&sh.d_partials, 16 * part_elems), "cudaMalloc partials");
-    ck(cudaMalloc(&sh.d_done, sizeof(uint32_t)), "cudaMalloc done");
-    ck(cudaMemset(sh.d_done, 0, sizeof(uint32_t)), "memset done");
+    ck(cudaMalloc(&sh.d_done, sizeof(uint32_t) * (1 + kMaxBatch)), "cudaMalloc done");
+    ck(cudaMemset(sh.d_done, 0, sizeof(uint32_t) * (1 + kMaxBatch)), "memset done");
     const size_t bins = sizeof(int64_t) * kMaxBatch * kFxBins * 16;
     ck(cudaMalloc(&sh.d_fxbins, bins), "cudaMalloc fxbins");
     ck(cudaMemset(sh.d_fxbins, 0, bins), "memset fxbins");
@@ -262,6 +267,9 @@ Model::Model(const pf_graph& g, const pf_data& d, uint32_t grid_points, const pf
     ck(cudaMemset(sh.d_clamp, 0, sizeof(uint64_t) * 2 * std::max(L_.n_poly, 1)), "memset clamp");
     ck(cudaHostAlloc(reinterpret_cast<void**>(&sh.h_out), sizeof(Out) * kMaxBatch, cudaHostAllocMapped),
        "mapped out");
+    // pinned memory may be recycled from a freed model: clear the completion
+    // words (pad) so no stale value can equal the sequence the host expects
+    std::memset(sh.h_out, 0, sizeof(Out) * kMaxBatch);
     ck(cudaHostAlloc(reinterpret_cast<void**>(&sh.h_norms),
                      sizeof(double) * kMaxBatch * 3 * pg_.nodes.size(), cudaHostAllocMapped),
        "mapped norms");
@@ -332,7 +340,10 @@ void Model::build_tasks(uint32_t grid_points) {
       const Node& nd = pg_.nodes[node];
       const int dims = static_cast<int>(nd.box.size());
       if (dims > 8) throw Error("bad-graph", nd.name + ": more than 8 box dimensions");
-      const double cost = subtree_cost(pg_, node);
+      // a convolution's grid runs over (point, tau_j) pairs (codegen.cpp
+      // emit_norm_point): Q elements per point, each one resolution call
+      const bool pairs = nd.kind == PF_CONVOLUTION && dims == 1;
+      const double cost = pairs ? 1.0 + subtree_cost(pg_, nd.children[1]) : subtree_cost(pg_, node);
       for (int fine = 0; fine < 2; ++fine) {
         Task t;
         std::memset(&t, 0, sizeof t);
@@ -351,6 +362,7 @@ void Model::build_tasks(uint32_t grid_points) {
         double vol = 1.0;
         for (int dd = 0; dd < dims; ++dd) vol *= t.h[dd];
         t.vol = vol;
+        if (pairs) total *= static_cast<uint64_t>(nd.q);
         t.points = total;
         // about 4096 raw evaluations per block, at most 4096 blocks per task
         uint64_t per = static_cast<uint64_t>(std::max(1.0, std::floor(4096.0 / cost)));
@@ -544,8 +556,25 @@ void Model::run(const double* params, int K, std::vector<Raw>& out, bool partial
     }
     ck(cudaGraphLaunch(g, sh.stream), "cudaGraphLaunch");
     g_launches += sh.kernels_per_graph;
+    for (int k = 0; k < K; ++k) ++sh.seq[k];
   }
-  for (Shard& sh : shards_) ck(cudaStreamSynchronize(sh.stream), "cudaStreamSynchronize");
+  // the result is in mapped memory as soon as the publishing block has
+  // written its completion word: spin on it (a stream synchronisation costs
+  // a wake-up); the stream is queried now and then so errors still surface
+  for (Shard& sh : shards_) {
+    for (int k = 0; k < K; ++k) {
+      const volatile uint32_t* word = &sh.h_out[k].pad;
+      for (uint64_t spin = 1; *word != sh.seq[k]; ++spin) {
+        if ((spin & 1023) == 0) {
+          const cudaError_t e = cudaStreamQuery(sh.stream);
+          if (e == cudaSuccess && *word != sh.seq[k])
+            throw Error("device-error", "evaluation finished without publishing its result");
+          if (e != cudaSuccess && e != cudaErrorNotReady) ck(e, "evaluation");
+        }
+      }
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
   (void)np;
   out.assign(K, Raw());
   const size_t nn = pg_.nodes.size();
@@ -725,6 +754,8 @@ BenchResult Model::bench(const double* params, size_t n, int metric, int steps, 
   }
   r.event_ms_mean = steps ? sum / steps : 0;
   r.event_ms_min = steps ? mn : 0;
+  ck(cudaStreamSynchronize(sh.stream), "cudaStreamSynchronize");
+  for (int k = 0; k < kMaxBatch; ++k) sh.seq[k] = sh.h_out[k].pad;  // bench launches published too
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   r.h2d_bytes = sizeof(double) * std::max(L_.np, 1);

@@ -109,7 +109,8 @@ struct Shard {
   double* d_C = nullptr;
   Task* d_tasks = nullptr;  // all levels, concatenated
   void* d_partials = nullptr;
-  uint32_t* d_done = nullptr;   // finished-block counter of the event pass
+  uint32_t* d_done = nullptr;   // [finished-block counter, kMaxBatch completion sequences]
+  uint32_t seq[kMaxBatch] = {};  // completion sequence the host expects next, per k
   int64_t* d_fxbins = nullptr;  // kMaxBatch x kFxBins x 16 binned digits of the event pass
   KRec* d_rec = nullptr;
   uint64_t* d_clamp = nullptr;  // [n_poly counted | n_poly discarded]
