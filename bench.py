@@ -116,67 +116,37 @@ def peaks():
         return 6650.0, "fallback"
 
 
-NCU_SUMMARY = os.path.join(ROOT, "profiles", "r1_event_kernel_ncu.txt")
+def ncu_summary_path(config):
+    """the committed ncu --set full capture of this config's event kernel
+    (tools/ncu_summary.py output under profiles/)"""
+    return os.path.join(ROOT, "profiles", f"r1b_{config.lower()}_event_ncu.txt")
 
 
-def ncu_metric(name):
-    """one metric of the committed ncu --set full capture of pf_event_kernel
-    (profiles/r1_event_kernel_ncu.txt, written by tools/ncu_summary.py), or None"""
+_SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+
+
+def ncu_metric(config, name):
+    """(value, unit) of one metric of the committed capture, or (None, None)"""
     try:
-        with open(NCU_SUMMARY) as fh:
+        with open(ncu_summary_path(config)) as fh:
             for line in fh:
                 parts = line.split()
-                if len(parts) == 2 and parts[0] == name:
-                    return float(parts[1])
+                if len(parts) >= 2 and parts[0] == name:
+                    return float(parts[1]), (parts[2] if len(parts) > 2 else "")
     except (OSError, ValueError):
         pass
-    return None
+    return None, None
 
 
-def ncu_traffic():
-    """dram read+write bytes per launch (ncu reports Mbyte)"""
-    r = ncu_metric("dram__bytes_read.sum")
-    w = ncu_metric("dram__bytes_write.sum")
-    return None if r is None or w is None else (r + w) * 1e6
-
-
-def cpu_side(W, pf, obs, pdf, cols, metric, fit=True, steps=3):
-    """The reference (oracle/_ref, all host threads) — or, for ArgusPdf
-    models it cannot express, the C restatement (oracle port, one thread) —
-    on a bounded sample of the same workload: per-call throughput and one
-    full fit from the start point."""
-    import oracle
-    threads = os.cpu_count() or 1
-    if W.unit == "bins":
-        sample = min(cols.shape[-1], 100_000)
-        ds = W.data(pf, obs, sample)
-    else:
-        sample = min(cols.shape[-1], 2_000_000)
-        ds = pf.UnbinnedDataSet.from_columns(obs, cols[..., :sample])
-    use_ref = oracle.Reference.available() and W.name != "C3"
-    if use_ref:
-        kind, ev = "reference", oracle.Reference(pdf, ds, W.grid)
-        call = lambda p: ev.eval(p, metric, threads)  # noqa: E731
-    else:
-        kind, ev, threads = "port", oracle.Oracle(pdf, ds, W.grid), 1
-        call = lambda p: ev.eval(p, metric)  # noqa: E731
-    p0 = [W.start[n] for n in ev.param_names()]
-    call(p0)
-    t = time.perf_counter()
-    for k in range(steps):
-        p = list(p0)
-        p[0] += 1e-9 * (k + 1)  # jitter: the normalisation recomputes, as in FD probes
-        call(p)
-    dt = (time.perf_counter() - t) / steps
-    out = {"value": sample / dt, "unit": f"{W.unit}/s", "cores": threads, "kind": kind,
-           "sample": f"{sample} {W.unit} of the same synthetic data, {steps} eval_metric calls "
-                     f"({W.name}, grid {W.grid}), params jittered 1e-9 per call",
-           "evals_per_s": 1.0 / dt, "ms_per_eval": dt * 1e3}
-    if fit and use_ref:
-        r = ev.fit(metric, threads)
-        out["fit"] = {"wall_s": r["wall_time_s"], "calls": int(r["calls"]), "status": int(r["status"]),
-                      "units": sample}
-    return out, ds
+def ncu_traffic(config):
+    """DRAM read + write bytes of one event-kernel launch"""
+    total = 0.0
+    for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+        v, u = ncu_metric(config, m)
+        if v is None or u not in _SCALE:
+            return None
+        total += v * _SCALE[u]
+    return total
 
 
 def fit_leg(W, pf, obs, pdf, cols, device):
@@ -404,20 +374,20 @@ def main():
         achieved = algo_bytes / (ev_ms * 1e-3) / 1e9
         line["roofline"] = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                             "frac": achieved / hbm_peak,
-                            "traffic": ncu_traffic() if W.name == "C2" else None,
-                            "traffic_source": "profiles/r1_event_kernel_ncu.txt (ncu --set full, 1 launch)",
+                            "traffic": ncu_traffic(W.name),
+                            "traffic_source": os.path.relpath(ncu_summary_path(W.name), ROOT) +
+                                              " (ncu --set full, 1 launch)",
                             "kernel": "pf_event_kernel", "kernel_ms": ev_ms,
                             "algorithmic_bytes_per_launch": algo_bytes,
                             "kernel_share_of_step": ev_ms / ms_step, "peak_kind": peak_kind}
-        if W.name == "C2":
-            # the event pass is issue/FP64-pipe limited, not HBM limited: the
-            # ncu-measured pipe utilisation of the same capture beside it
-            fp64 = ncu_metric("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active")
-            issue = ncu_metric("smsp__issue_active.avg.pct_of_peak_sustained_active")
-            if fp64 is not None:
-                line["roofline"]["fp64_pipe_active_frac_ncu"] = fp64 / 100.0
-            if issue is not None:
-                line["roofline"]["issue_active_frac_ncu"] = issue / 100.0
+        # the event pass is issue/FP64-pipe limited rather than HBM limited:
+        # the ncu-measured pipe utilisation of the same capture beside it
+        fp64, _ = ncu_metric(W.name, "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active")
+        issue, _ = ncu_metric(W.name, "smsp__issue_active.avg.pct_of_peak_sustained_active")
+        if fp64 is not None:
+            line["roofline"]["fp64_pipe_active_frac_ncu"] = fp64 / 100.0
+        if issue is not None:
+            line["roofline"]["issue_active_frac_ncu"] = issue / 100.0
     if world == 1 and not args.no_fit and W.name != "C3":  # C3: no reference fit to compare with
         # full fit (fit.hpp:498-581) from the start point, GPU and reference
         # on the same bounded sample (at 1e7 events the reference's absolute

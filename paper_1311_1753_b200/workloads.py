@@ -68,9 +68,13 @@ class C1(Workload):
         alpha = pf.new_parameter("alpha", self.start["alpha"], 0.5, -10, 10)
         return [x], pf.exp_pdf("exppdf", x, alpha)
 
-    def data(self, pf, obs, n, seed=11):
+    @classmethod
+    def columns(cls, n, seed=11):
         rng = np.random.default_rng(seed)
-        return pf.UnbinnedDataSet.from_columns(obs, _trunc_exp(rng.random(n), self.truth["alpha"], 21.49))
+        return _trunc_exp(rng.random(n), cls.truth["alpha"], 21.49)
+
+    def data(self, pf, obs, n, seed=11):
+        return pf.UnbinnedDataSet.from_columns(obs, self.columns(n, seed))
 
     def bytes_per_unit(self):
         return 8.0

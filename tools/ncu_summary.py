@@ -8,7 +8,7 @@ import sys
 rep = sys.argv[1]
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 r = list(csv.reader(raw.splitlines()))
-h, v = r[0], r[2]
+h, units, v = r[0], r[1], r[2]
 want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
         "dram__throughput.avg.pct_of_peak_sustained_elapsed",
         "sm__inst_executed_pipe_fp64.avg.pct", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
@@ -20,7 +20,7 @@ want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
 for i, name in enumerate(h):
     if any(name == w or name.startswith(w + ".") or (w.endswith("pct") and name.startswith(w)) or
            (w == "launch__occupancy_limit" and name.startswith(w)) for w in want):
-        print(f"{name:70s} {v[i]}")
+        print(f"{name:70s} {v[i]} {units[i]}".rstrip())
 print("-- stalls per issue --")
 for i, name in enumerate(h):
     if "average_warps_issue_stalled" in name and name.endswith("per_issue_active.ratio"):
