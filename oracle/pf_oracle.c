@@ -614,3 +614,30 @@ void po_mt64_uniform(uint64_t seed, uint64_t n, double* out) {
   mt64_seed(&g, seed);
   for (uint64_t i = 0; i < n; ++i) out[i] = (double)(mt64_next(&g) >> 11) * 0x1.0p-53;
 }
+
+/* Test support for the GPU's ArgusPdf log form (codegen.cpp emit_logterm):
+ * y / m0 there is Markstein's FMA sequence on the correctly rounded
+ * reciprocal, q = y * inv, r = fma(-q, m0, y), q' = fma(r, inv, q).  Counts
+ * the operand pairs (y in [lo, hi), m0 in [mlo, mhi), uniform from a
+ * splitmix64 stream) where q' differs from the IEEE quotient y / m0. */
+static uint64_t po_splitmix(uint64_t* s) {
+  uint64_t z = (*s += 0x9e3779b97f4a7c15ull);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+int64_t po_markstein_mismatches(uint64_t n, uint64_t seed, double lo, double hi, double mlo, double mhi) {
+  int64_t bad = 0;
+  uint64_t s = seed;
+  for (uint64_t i = 0; i < n; ++i) {
+    const double u = (double)(po_splitmix(&s) >> 11) * 0x1.0p-53;
+    const double v = (double)(po_splitmix(&s) >> 11) * 0x1.0p-53;
+    const double y = lo + (hi - lo) * u, m0 = mlo + (mhi - mlo) * v;
+    const double inv = 1.0 / m0;
+    const double q = y * inv;
+    const double r = fma(fma(-q, m0, y), inv, q);
+    if (r != y / m0) ++bad;
+  }
+  return bad;
+}

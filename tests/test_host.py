@@ -231,3 +231,18 @@ def test_shard_partition_covers_events():
             if n > 1024 * g:
                 sizes = [c for _, c in spans]
                 assert max(sizes) - min(sizes) <= 1024
+
+
+def test_markstein_division_is_correctly_rounded():
+    """the GPU ArgusPdf log form divides by Markstein's FMA sequence on the
+    per-call reciprocal: it must equal the IEEE quotient (the oracle's and the
+    linear kernel's y / m0) bit for bit"""
+    import ctypes as C
+    import oracle
+    L = oracle._olib()
+    f = L.po_markstein_mismatches
+    f.restype = C.c_int64
+    f.argtypes = [C.c_uint64, C.c_uint64, C.c_double, C.c_double, C.c_double, C.c_double]
+    assert f(2_000_000, 1, 5.20, 5.29, 5.28, 5.30) == 0       # the C3 range
+    assert f(2_000_000, 2, 1e-3, 1e3, 1e-3, 1e3) == 0         # wide operands
+    assert f(1_000_000, 3, 0.5, 2.0, 1.0 - 1e-15, 1.0 + 1e-15) == 0  # near-1 divisors
