@@ -149,6 +149,45 @@ def ncu_traffic(config):
     return total
 
 
+def cpu_side(W, pf, obs, pdf, cols, metric, fit=True, steps=3):
+    """The reference (oracle/_ref, all host threads) — or, for ArgusPdf
+    models it cannot express, the C restatement (oracle port, one thread) —
+    on a bounded sample of the same workload: per-call throughput and one
+    full fit from the start point."""
+    import oracle
+    threads = os.cpu_count() or 1
+    if W.unit == "bins":
+        sample = min(cols.shape[-1], 100_000)
+        ds = W.data(pf, obs, sample)
+    else:
+        sample = min(cols.shape[-1], 2_000_000)
+        ds = pf.UnbinnedDataSet.from_columns(obs, cols[..., :sample])
+    use_ref = oracle.Reference.available() and W.name != "C3"
+    if use_ref:
+        kind, ev = "reference", oracle.Reference(pdf, ds, W.grid)
+        call = lambda p: ev.eval(p, metric, threads)  # noqa: E731
+    else:
+        kind, ev, threads = "port", oracle.Oracle(pdf, ds, W.grid), 1
+        call = lambda p: ev.eval(p, metric)  # noqa: E731
+    p0 = [W.start[n] for n in ev.param_names()]
+    call(p0)
+    t = time.perf_counter()
+    for k in range(steps):
+        p = list(p0)
+        p[0] += 1e-9 * (k + 1)  # jitter: the normalisation recomputes, as in FD probes
+        call(p)
+    dt = (time.perf_counter() - t) / steps
+    out = {"value": sample / dt, "unit": f"{W.unit}/s", "cores": threads, "kind": kind,
+           "sample": f"{sample} {W.unit} of the same synthetic data, {steps} eval_metric calls "
+                     f"({W.name}, grid {W.grid}), params jittered 1e-9 per call",
+           "evals_per_s": 1.0 / dt, "ms_per_eval": dt * 1e3}
+    if fit and use_ref:
+        r = ev.fit(metric, threads)
+        out["fit"] = {"wall_s": r["wall_time_s"], "calls": int(r["calls"]), "status": int(r["status"]),
+                      "units": sample}
+    return out, ds
+
+
 def fit_leg(W, pf, obs, pdf, cols, device):
     """GPU fit and reference fit (all host threads) of the same sample"""
     import oracle

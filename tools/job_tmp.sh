@@ -1,4 +1,4 @@
-python -m pytest tests -m gpu -q 2>&1 | tail -3
-BENCH_ARGS="--config C3" bash tools/variants.sh "" "PFB200_EV_BLOCKS=10 PFB200_DEFINES=PF_EVENT_MIN_BLOCKS=10" 2>&1
-bash tools/variants.sh "" 2>&1
-python bench.py --config C1 --steps 50 --no-cpu-baseline > gpurun_out/c1.json 2>gpurun_out/c1.err; tail -c 900 gpurun_out/c1.json; tail -2 gpurun_out/c1.err
+python bench.py --config C3 --steps 20 > gpurun_out/r1c_c3.json 2> gpurun_out/r1c_c3.err
+python bench.py --config C1 --steps 50 > gpurun_out/r1c_c1.json 2> gpurun_out/r1c_c1.err
+ncu --set full --clock-control none --import-source on -k regex:"pf_event" -s 3 -c 1 -o gpurun_out/r1c_c3_event --force-overwrite python bench.py --config C3 --steps 2 --warmup 3 --no-cpu-baseline --no-fit > gpurun_out/r1c_ncu3.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"pf_event" -s 3 -c 1 -o gpurun_out/r1c_c1_event --force-overwrite python bench.py --config C1 --steps 2 --warmup 3 --no-cpu-baseline --no-fit > gpurun_out/r1c_ncu1.log 2>&1
