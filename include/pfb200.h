@@ -287,6 +287,12 @@ PF_API int pf_fit(pf_model* model, int32_t metric, const pf_fit_config* config, 
            const int32_t* fixed, const double* lower, const double* upper, const double* step,
            pf_fit_result* result, pf_status* status);
 
+/* Diagnostics: copies up to n of the model's %globaltimer stamps (built with
+ * PFB200_DEFINES=PF_EVENT_TRACE; per event block: entry, prologue, PDL wait,
+ * main loop, done, published; block 4095: setup entry/exit) into out.
+ * Returns the number copied (0 when the module has no trace buffer). */
+PF_API int64_t pf_debug_trace(pf_model* model, uint64_t* out, int64_t n);
+
 /* Library version / number of CUDA kernels launched so far by this process
  * (all models), for the bench's gpu_launches accounting. */
 PF_API int32_t pf_abi_version(void);

@@ -118,6 +118,7 @@ _SIGNATURES = {
     "pf_model_chunk": (C.c_uint64, [C.c_void_p]),
     "pf_abi_version": (C.c_int32, []),
     "pf_kernel_launches": (C.c_uint64, []),
+    "pf_debug_trace": (C.c_int64, [C.c_void_p, C.POINTER(C.c_uint64), C.c_int64]),
 }
 
 

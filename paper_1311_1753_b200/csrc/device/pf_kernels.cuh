@@ -18,6 +18,17 @@
 // independent of the number of devices.
 
 // griddepcontrol (programmatic dependent launch); no-ops without PDL
+#ifdef PF_EVENT_TRACE
+__device__ __forceinline__ unsigned long long pf_gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// per block: [in, prologue done, PDL wait done, main loop done, block done,
+// published]; setup: slot 0 of block 4095 (in), slot 1 (out)
+__device__ unsigned long long pf_trace_buf[4096 * 6];
+#define PF_ETRACE(slot, v) (pf_trace_buf[(pf_u64)blockIdx.x * 6 + (slot)] = (v))
+#endif
 __device__ __forceinline__ void pf_pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
 __device__ __forceinline__ void pf_pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
@@ -129,6 +140,9 @@ extern "C" __global__ void __launch_bounds__(PF_SETUP_THREADS) pf_setup_kernel(c
 #endif
   const unsigned rank = PF_SETUP_CLUSTER > 1 ? pf_cluster_rank() : 0u;
   const int k = blockIdx.x / PF_SETUP_CLUSTER;
+#ifdef PF_EVENT_TRACE
+  if (threadIdx.x == 0 && blockIdx.x == 0) pf_trace_buf[4095 * 6 + 0] = pf_gtime();
+#endif
   double* P = pf_sdyn;
   double* S = pf_sdyn + PF_NP;
   // K = 1: parameters arrive inline in the kernel arguments (constant bank,
@@ -232,6 +246,9 @@ extern "C" __global__ void __launch_bounds__(PF_SETUP_THREADS) pf_setup_kernel(c
 #ifdef PF_SETUP_TRACE
   if (threadIdx.x == 0 && blockIdx.x == 0)
     for (int i = 0; i < ntr; ++i) printf("setup %-8s %lld\n", trn[i], trs[i]);
+#endif
+#ifdef PF_EVENT_TRACE
+  if (threadIdx.x == 0 && blockIdx.x == 0) pf_trace_buf[4095 * 6 + 1] = pf_gtime();
 #endif
   // no CTA leaves while another may still read its shared memory
   if (PF_SETUP_CLUSTER > 1) pf_cluster_sync();
@@ -574,11 +591,35 @@ __device__ __forceinline__ pf_lacc pf_stage_terms(const pf_args& a, int k, pf_u6
   const double* P = a.P + (pf_u64)k * PF_NP;
   const double* S = a.S + (pf_u64)k * PF_SS;
 #if !PF_BINNED && PF_LOGFORM
+  pf_lform A;
+  pf_lform_init(A);
+#ifdef PF_LOG_FAST_SLOT
+  // per-call fast path: interval bounds over the data box (pf_stage_post)
+  // proved every event's terms in range, so no per-event test at all
+  if (S[PF_LOG_FAST_SLOT] != 0.0) {
+#pragma unroll pf_unroll
+    for (int j = 0; j < PF_EPT; ++j) {
+      const int i = 32 * j + lane;
+      double ev[PF_NCOLS];
+#pragma unroll
+      for (int q = 0; q < PF_NCOLS; ++q) ev[q] = 0.0;
+#pragma unroll
+      for (int q = 0; q < PF_NLOAD; ++q) ev[pf_load_col(q)] = st[q * PF_SUB + i];
+      double Lv, fac[PF_NFAC_A];
+      pf_eval_event_log_fast(ev, P, S, Lv, fac);
+      if (!FULL && i >= n_valid) {
+        Lv = 0.0;
+#pragma unroll
+        for (int f = 0; f < PF_NFAC_A; ++f) fac[f] = 1.0;
+      }
+      pf_lform_add(A, Lv, fac);
+    }
+    return pf_lform_pack(A);
+  }
+#endif
   // log domain, optimistic: -log v = -(L + log F) with no per-event log and
   // no per-event branch; the lane's sub-chunk is redone exactly (above) when
   // any of its events fails the log-domain test
-  pf_lform A;
-  pf_lform_init(A);
   bool allok = true;
 #pragma unroll pf_unroll
   for (int j = 0; j < PF_EPT; ++j) {
@@ -680,6 +721,9 @@ __device__ __forceinline__ pf_lacc pf_stage_terms(const pf_args& a, int k, pf_u6
 extern "C" __global__ void __launch_bounds__(PF_EV_THREADS, PF_EVENT_MIN_BLOCKS) pf_event_kernel(const __grid_constant__ pf_args a) {
   extern __shared__ __align__(16) unsigned char pf_dyn[];
   __shared__ __align__(8) pf_u64 bars[PF_EV_WARPS * PF_NST];
+#ifdef PF_EVENT_TRACE
+  const unsigned long long t_in = pf_gtime();
+#endif
   double* stages = reinterpret_cast<double*>(pf_dyn);
   double* accs = stages + PF_EV_WARPS * PF_NST * PF_STAGE;  // [k][PF_LACC_N][thread]
   long long* fxs = reinterpret_cast<long long*>(accs + a.K * PF_LACC_N * PF_EV_THREADS);  // [k][digit][thread]
@@ -714,7 +758,13 @@ extern "C" __global__ void __launch_bounds__(PF_EV_THREADS, PF_EVENT_MIN_BLOCKS)
     }
   };
   for (int w = 0; w < PF_NST - 1 && w < W; ++w) issue(w);
+#ifdef PF_EVENT_TRACE
+  const unsigned long long t_pro = pf_gtime();
+#endif
   pf_pdl_wait();  // norms, constants and records of this call are ready
+#ifdef PF_EVENT_TRACE
+  const unsigned long long t_wait = pf_gtime();
+#endif
   for (int w = 0; w < W; ++w) {
     const int s = w % PF_NST;
     pf_mbar_wait(mybar + s, (unsigned)((w / PF_NST) & 1));
@@ -756,6 +806,9 @@ extern "C" __global__ void __launch_bounds__(PF_EV_THREADS, PF_EVENT_MIN_BLOCKS)
       }
     }
   }
+#ifdef PF_EVENT_TRACE
+  const unsigned long long t_loop = pf_gtime();
+#endif
   // block totals: warp shuffles, the block's warps through shared memory,
   // then ONE binned atomic set per block (exact integer digits)
   __shared__ long long bfx[PF_EV_WARPS][PF_FX_DIGITS];
@@ -786,23 +839,81 @@ extern "C" __global__ void __launch_bounds__(PF_EV_THREADS, PF_EVENT_MIN_BLOCKS)
     s_last = atomicAdd(a.done, 1u) == gridDim.x - 1;
   }
   __syncthreads();
+#ifdef PF_EVENT_TRACE
+  if (threadIdx.x == 0 && blockIdx.x < 4095) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    PF_ETRACE(5, (unsigned long long)smid);
+    PF_ETRACE(0, t_in);
+    PF_ETRACE(1, t_pro);
+    PF_ETRACE(2, t_wait);
+    PF_ETRACE(3, t_loop);
+    PF_ETRACE(4, pf_gtime());
+  }
+#endif
   if (!s_last) return;
+#ifdef PF_EVENT_TRACE
+  if (threadIdx.x == 0) pf_trace_buf[4094 * 6 + 0] = pf_gtime();
+#endif
   __threadfence();
   if (threadIdx.x == 0) *a.done = 0u;  // self-resetting (bench relaunches)
-  for (int k = 0; k < a.K; ++k) {
-    if (threadIdx.x < PF_FX_DIGITS) {
-      long long* bins = a.fxbins + (pf_u64)k * PF_FX_BINS * PF_FX_BIN_STRIDE + threadIdx.x;
-      long long v = 0;
-#pragma unroll 8
-      for (int b = 0; b < PF_FX_BINS; ++b) {
-        v += (long long)__ldcg((const unsigned long long*)(bins + b * PF_FX_BIN_STRIDE));
-        bins[b * PF_FX_BIN_STRIDE] = 0ll;  // self-resetting
+  // warp 0 finishes every parameter set: lane b reads bin b (one round trip,
+  // 32 bins), integer shuffles add the digits, lane 0 rounds and writes the
+  // record straight into mapped host memory; one system fence, then the
+  // completion words
+  static_assert(PF_FX_BINS == 32, "one bin per lane of warp 0");
+  if (warp == 0) {
+    for (int k = 0; k < a.K; ++k) {
+      const pf_krec* r = a.rec + k;
+      long long* bin = a.fxbins + ((pf_u64)k * PF_FX_BINS + lane) * PF_FX_BIN_STRIDE;
+      long long d[PF_FX_DIGITS];
+#pragma unroll
+      for (int i = 0; i < PF_FX_DIGITS; ++i) d[i] = (long long)__ldcg((const unsigned long long*)(bin + i));
+      pf_u64 floors = 0, nonfinite = 0, evterr = 0;
+      pf_u32 normerr = 0;
+      if (lane == 0) {
+        floors = __ldcg(&r->floor_count);
+        nonfinite = __ldcg(&r->first_nonfinite);
+        evterr = __ldcg(&r->first_event_error);
+        normerr = __ldcg(&r->norm_error);
       }
-      a.rec[k].fx[threadIdx.x] = v;
+#pragma unroll
+      for (int i = 0; i < PF_FX_DIGITS; ++i) bin[i] = 0ll;  // self-resetting
+#pragma unroll
+      for (int i = 0; i < PF_FX_DIGITS; ++i) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) d[i] += __shfl_down_sync(0xffffffffu, d[i], off);
+      }
+      pf_out* o = a.hout + k;
+      if (lane == 0) {
+        o->result = pf_fx_round(d);
+#pragma unroll
+        for (int i = 0; i < PF_FX_DIGITS; ++i) o->fx[i] = d[i];
+        o->floor_count = floors;
+        o->first_nonfinite = nonfinite;
+        o->first_event_error = evterr;
+        o->norm_error = normerr;
+      }
+      const double* S = a.S + (pf_u64)k * PF_SS;
+      for (int i = lane; i < 3 * a.n_nodes; i += 32) a.hnorms[(pf_u64)k * 3 * a.n_nodes + i] = S[i];
+#if PF_NPOLY > 0
+      if (k == a.K - 1)
+        for (int i = lane; i < PF_NPOLY; i += 32) a.hclamp[i] = __ldcg(a.clamp + i);
+#endif
+    }
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_system();  // every field above reaches the host first
+      for (int k = 0; k < a.K; ++k) {
+        const pf_u32 seq = a.done[1 + k] + 1u;
+        a.done[1 + k] = seq;
+        *(volatile pf_u32*)&a.hout[k].pad = seq;
+      }
     }
   }
-  __syncthreads();
-  for (int k = 0; k < a.K; ++k) pf_publish(a, k, threadIdx.x, blockDim.x);
+#ifdef PF_EVENT_TRACE
+  if (threadIdx.x == 0) pf_trace_buf[4094 * 6 + 2] = pf_gtime();
+#endif
 }
 
 // ---------------------------------------------------------------------------

@@ -183,6 +183,24 @@ Model::Model(const pf_graph& g, const pf_data& d, uint32_t grid_points, const pf
   pg_ = finalize(g, d.n_obs, d.obs, binned_ ? 2 : 0);
   L_ = generate(pg_, binned_);
   if (binned_) L_.constants[L_.nc_total_slot] = total_content_;
+  if (L_.data_range_base >= 0) {
+    // (min, max) of every data column over ALL events, for the per-call
+    // log-form range proof (a NaN or infinite datum disables the fast path)
+    for (int c = 0; c < d.n_obs; ++c) {
+      double lo = std::numeric_limits<double>::infinity(), hi = -lo;
+      bool finite = d.n_events > 0;
+      const double* col = d.values + static_cast<size_t>(c) * d.n_events;
+      for (uint64_t e = 0; e < d.n_events; ++e) {
+        const double v = col[e];
+        finite = finite && std::isfinite(v);
+        lo = v < lo ? v : lo;
+        hi = v > hi ? v : hi;
+      }
+      if (!finite) lo = hi = std::numeric_limits<double>::quiet_NaN();
+      L_.constants[L_.data_range_base + 2 * c] = lo;
+      L_.constants[L_.data_range_base + 2 * c + 1] = hi;
+    }
+  }
   clamp_total_.assign(pg_.nodes.size(), 0);
   norms_.assign(pg_.nodes.size(), 1.0);  // PdfNode::norm_ default (pdf.hpp:199)
   errs_.assign(pg_.nodes.size(), 0.0);
@@ -706,6 +724,21 @@ void Model::norms(double* norms, double* errs, int32_t* valid, int n) const {
 namespace pfb {
 
 // Device timing with CUDA events on the shard-0 stream (pfb200.h pf_bench).
+int64_t Model::debug_trace(uint64_t* out, int64_t n) {
+  Shard& sh = shards_[0];
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  if (cudaLibraryGetGlobal(&ptr, &bytes, sh.mod->lib, "pf_trace_buf") != cudaSuccess || !ptr) {
+    cudaGetLastError();
+    return 0;
+  }
+  const int64_t m = std::min<int64_t>(n, static_cast<int64_t>(bytes / sizeof(uint64_t)));
+  ck(cudaSetDevice(sh.device), "cudaSetDevice");
+  ck(cudaStreamSynchronize(sh.stream), "cudaStreamSynchronize");
+  ck(cudaMemcpy(out, ptr, sizeof(uint64_t) * m, cudaMemcpyDeviceToHost), "trace D2H");
+  return m;
+}
+
 BenchResult Model::bench(const double* params, size_t n, int metric, int steps, bool flush) {
   BenchResult r;
   r.metric = eval(params, n, metric, nullptr);  // builds the K = 1 graph

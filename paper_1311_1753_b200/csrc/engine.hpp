@@ -149,6 +149,7 @@ class Model {
   void eval_batch(const double* params, size_t K, size_t n, int metric, double* out);
   // this process's shard partial (shard_count > 1)
   void eval_partial(const double* params, size_t n, int metric, int64_t* fx, int* penalty);
+  int64_t debug_trace(uint64_t* out, int64_t n);
   BenchResult bench(const double* params, size_t n, int metric, int steps, bool flush);
 
   const Program& program() const { return pg_; }
