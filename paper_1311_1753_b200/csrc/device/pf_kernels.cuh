@@ -103,6 +103,13 @@ __device__ __forceinline__ unsigned pf_cluster_rank() {
 __device__ __forceinline__ void pf_cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+__device__ __forceinline__ double pf_dsmem_load(const double* p, unsigned rank) {
+  unsigned ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(pf_smem_addr(p)), "r"(rank));
+  double v;
+  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(ra) : "memory");
+  return v;
+}
 __device__ __forceinline__ pf_dd pf_dsmem_load_dd(const pf_dd* p, unsigned rank) {
   unsigned ra;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(pf_smem_addr(p)), "r"(rank));
@@ -126,7 +133,7 @@ extern "C" __global__ void __launch_bounds__(PF_SETUP_THREADS) pf_setup_kernel(c
   // table is staged too.  The state is written to global memory at the end.
   extern __shared__ __align__(16) double pf_sdyn[];
   // this CTA's warp partials per task, double-buffered by level parity
-  __shared__ pf_dd wpart[2][PF_SETUP_MAXQ][PF_SETUP_THREADS / 32];
+  __shared__ double wpart[2][PF_SETUP_MAXQ][PF_SETUP_THREADS / 32];
   __shared__ pf_task tk[16];
   pf_pdl_trigger();  // let the event kernel start streaming its data now
 #ifdef PF_SETUP_TRACE
@@ -173,24 +180,27 @@ extern "C" __global__ void __launch_bounds__(PF_SETUP_THREADS) pf_setup_kernel(c
     int t1 = t0;
     while (t1 < nt && tk[t1].level == level) ++t1;
     const int nl = min(t1 - t0, PF_SETUP_MAXQ);  // (coarse, fine) task pairs of the level's nodes
-    // every midpoint sum of the level first (this CTA's share of the points)
-    pf_dd x[PF_SETUP_MAXQ];
+    // every midpoint sum of the level first (this CTA's share of the points).
+    // The grid values are non-negative: plain-double pairwise trees are good
+    // to ~1.5e-15 relative over the 3n points (the reference's long double
+    // is not needed at the 1e-12 bar), at a tenth of double-double's cost.
+    double x[PF_SETUP_MAXQ];
 #pragma unroll
-    for (int q = 0; q < PF_SETUP_MAXQ; ++q) x[q] = pf_dd_zero();
+    for (int q = 0; q < PF_SETUP_MAXQ; ++q) x[q] = 0.0;
     for (int q = 0; q < nl; ++q) {
       const pf_task& T = tk[t0 + q];
-      pf_dd acc = pf_dd_zero();
+      double acc = 0.0;
       for (pf_u64 i = rank * PF_SETUP_THREADS + threadIdx.x; i < T.points;
            i += PF_SETUP_THREADS * PF_SETUP_CLUSTER)
-        acc = pf_dd_add_d(acc, pf_norm_point(T.node, i, T, P, S, a.C, cx, cnt));
+        acc += pf_norm_point(T.node, i, T, P, S, a.C, cx, cnt);
       x[q] = acc;
     }
     PF_TRACE("points");
-    // warp trees of all the level's sums together (their latency chains overlap)
+    // warp trees of all the level's sums together
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) {
 #pragma unroll
-      for (int q = 0; q < PF_SETUP_MAXQ; ++q) x[q] = pf_dd_add(x[q], pf_shfl_down_dd(x[q], d));
+      for (int q = 0; q < PF_SETUP_MAXQ; ++q) x[q] += __shfl_down_sync(0xffffffffu, x[q], d);
     }
     if (lane == 0)
 #pragma unroll
@@ -209,20 +219,20 @@ extern "C" __global__ void __launch_bounds__(PF_SETUP_THREADS) pf_setup_kernel(c
     // a fixed tree, then a 16-lane tree; lane 0 finishes the node
     if (2 * warp < nl) {
       const int q = 2 * warp + (lane >> 4);
-      const pf_dd* src = &wpart[level & 1][q][lane & 15];
-      pf_dd v[PF_SETUP_CLUSTER];
+      const double* src = &wpart[level & 1][q][lane & 15];
+      double v[PF_SETUP_CLUSTER];
 #pragma unroll
       for (int rk = 0; rk < PF_SETUP_CLUSTER; ++rk)
-        v[rk] = PF_SETUP_CLUSTER > 1 ? pf_dsmem_load_dd(src, (unsigned)rk) : *src;
+        v[rk] = PF_SETUP_CLUSTER > 1 ? pf_dsmem_load(src, (unsigned)rk) : *src;
 #pragma unroll
       for (int w = 1; w < PF_SETUP_CLUSTER; w <<= 1)
 #pragma unroll
-        for (int rk = 0; rk + w < PF_SETUP_CLUSTER; rk += 2 * w) v[rk] = pf_dd_add(v[rk], v[rk + w]);
-      pf_dd y = v[0];
+        for (int rk = 0; rk + w < PF_SETUP_CLUSTER; rk += 2 * w) v[rk] += v[rk + w];
+      double y = v[0];
 #pragma unroll
-      for (int d = 8; d > 0; d >>= 1) y = pf_dd_add(y, pf_shfl_down_dd(y, d));
+      for (int d = 8; d > 0; d >>= 1) y += __shfl_down_sync(0xffffffffu, y, d);
       // midpoint_sum returns static_cast<double>(sum) * vol (pdf.hpp:173-175)
-      const double sum = __dmul_rn(pf_dd_to_double(y), tk[t0 + q].vol);
+      const double sum = __dmul_rn(y, tk[t0 + q].vol);
       const double fine = __shfl_down_sync(0xffffffffu, sum, 16);
       if (lane == 0) pf_finish_norm(S, r, tk[t0 + q].node, sum, fine);
     }
