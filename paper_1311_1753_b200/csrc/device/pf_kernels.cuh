@@ -913,11 +913,19 @@ extern "C" __global__ void __launch_bounds__(PF_EV_THREADS, PF_EVENT_MIN_BLOCKS)
     }
     __syncwarp();
     if (lane == 0) {
+#ifdef PF_PUBLISH_FENCE
       __threadfence_system();  // every field above reaches the host first
+#endif
       for (int k = 0; k < a.K; ++k) {
         const pf_u32 seq = a.done[1 + k] + 1u;
         a.done[1 + k] = seq;
+#ifdef PF_PUBLISH_FENCE
         *(volatile pf_u32*)&a.hout[k].pad = seq;
+#else
+        // system-scope release: every field above (this warp's writes, made
+        // visible to lane 0 by the __syncwarp) reaches the host first
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(&a.hout[k].pad), "r"(seq) : "memory");
+#endif
       }
     }
   }
