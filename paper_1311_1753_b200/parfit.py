@@ -314,6 +314,7 @@ class PdfNode:
         self._norm = 1.0
         self._norm_err = 0.0
         self._norm_valid = False
+        self._owner = None  # the BoundModel that evaluated this node last (norms fetched lazily)
         self._model = None
 
     def name(self):
@@ -331,12 +332,18 @@ class PdfNode:
     def declared_observables(self):
         return list(self._obs)
 
+    def _fresh(self):
+        if self._owner is not None and self._owner._stale:
+            self._owner._sync_norms()
+
     def cached_norm(self) -> float:
+        self._fresh()
         if not self._norm_valid:
             raise Error("stale-normalization", self._name)
         return self._norm
 
     def norm_error_estimate(self) -> float:
+        self._fresh()
         return self._norm_err
 
 
@@ -764,6 +771,8 @@ class BoundModel:
         for i in range(lib.pf_model_n_params(h)):
             self._registry.register_parameter(self._desc.vars[lib.pf_model_param_variable(h, i)])
         self._nodes = self._desc.preorder()
+        self._stale = False
+        self._call = None
         for i, node in enumerate(self._nodes):
             node._id = i
             node._model = self
@@ -800,7 +809,15 @@ class BoundModel:
                                     2 if self._binned else 0)
         return self._table
 
+    def _evaluated(self):
+        """norms are fetched on first use (PdfNode.cached_norm), not per call"""
+        self._stale = True
+        if self._nodes and self._nodes[0]._owner is not self:
+            for node in self._nodes:
+                node._owner = self
+
     def _sync_norms(self):
+        self._stale = False
         n = len(self._nodes)
         norms = (C.c_double * n)()
         errs = (C.c_double * n)()
@@ -813,13 +830,14 @@ class BoundModel:
                 node._norm_valid = True
 
     def eval_metric(self, params, metric=MetricKind.NegLogLikelihood, backend=None) -> float:
-        p = np.ascontiguousarray(np.asarray(params, dtype=np.float64).ravel())
-        out = C.c_double()
-        info = _abi.pf_eval_info()
-        st = _abi.pf_status()
-        rc = lib.pf_eval_metric(self._h, p.ctypes.data_as(C.POINTER(C.c_double)), p.size, int(metric),
-                                C.byref(out), C.byref(info), C.byref(st))
-        self._sync_norms()
+        p = params if (isinstance(params, np.ndarray) and params.dtype == np.float64 and params.ndim == 1
+                       and params.flags.c_contiguous) else np.ascontiguousarray(params, dtype=np.float64).ravel()
+        if self._call is None:  # argument objects reused by every call (the hot path of a fit)
+            out, info, st = C.c_double(), _abi.pf_eval_info(), _abi.pf_status()
+            self._call = (out, info, st, C.byref(out), C.byref(info), C.byref(st))
+        out, info, st, r_out, r_info, r_st = self._call
+        rc = _eval_fast(self._h, p.ctypes.data, p.size, int(metric), r_out, r_info, r_st)
+        self._evaluated()
         if rc:
             _raise(st)
         return out.value
@@ -833,7 +851,7 @@ class BoundModel:
         rc = lib.pf_eval_metric_batch(self._h, p.ctypes.data_as(C.POINTER(C.c_double)), p.shape[0],
                                       p.shape[1], int(metric),
                                       out.ctypes.data_as(C.POINTER(C.c_double)), C.byref(st))
-        self._sync_norms()
+        self._evaluated()
         if rc:
             _raise(st)
         return out
@@ -848,6 +866,13 @@ class BoundModel:
                                part, C.byref(pen), C.byref(st)):
             _raise(st)
         return list(part), bool(pen.value)
+
+
+# pf_eval_metric bound a second time with plain-address arguments: the
+# per-call path of BoundModel.eval_metric skips ctypes pointer conversions
+_eval_fast = lib["pf_eval_metric"]
+_eval_fast.restype = C.c_int
+_eval_fast.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]
 
 
 def combine_partials(parts) -> float:
