@@ -266,10 +266,14 @@ class PdfNode {
   const std::vector<VariablePtr>& declared_parameters() const { return params_; }
   const std::vector<VariablePtr>& declared_observables() const { return obs_; }
   double cached_norm() const {
+    refresh();
     if (!norm_valid_) throw Error("stale-normalization", name_);
     return norm_;
   }
-  double norm_error_estimate() const { return norm_err_; }
+  double norm_error_estimate() const {
+    refresh();
+    return norm_err_;
+  }
   const std::vector<double>& reals() const { return reals_; }
   std::size_t quadrature() const { return q_; }
 
@@ -281,8 +285,10 @@ class PdfNode {
   std::vector<double> reals_;
   std::size_t q_ = 0;
   mutable std::size_t id_ = 0;
-  double norm_ = 1.0, norm_err_ = 0.0;
-  bool norm_valid_ = false;
+  mutable double norm_ = 1.0, norm_err_ = 0.0;
+  mutable bool norm_valid_ = false;
+  mutable BoundModel* owner_ = nullptr;  // the model that evaluated this node last
+  void refresh() const;                  // its norms, fetched on first use
   friend class BoundModel;
   friend IndexTable finalize(ParameterRegistry&, const PdfPtr&, const std::vector<VariablePtr>&, int);
   static void need_obs(const std::string& n, const VariablePtr& v, const char* what = "x") {
@@ -629,7 +635,11 @@ class BoundModel {
     events_ = to_event_table(ds);
     create(ds.observables(), ds.total_content(), backend);
   }
-  ~BoundModel() { pf_model_destroy(model_); }
+  ~BoundModel() {
+    for (const PdfNode* node : pre_)
+      if (node->owner_ == this) node->owner_ = nullptr;
+    pf_model_destroy(model_);
+  }
   BoundModel(const BoundModel&) = delete;
   BoundModel& operator=(const BoundModel&) = delete;
 
@@ -648,10 +658,16 @@ class BoundModel {
     pf_status st{};
     const int rc = pf_eval_metric(model_, params.data(), params.size(),
                                   metric == MetricKind::ChiSquared ? PF_CHISQ : PF_NLL, &out, nullptr, &st);
-    sync_norms();
+    evaluated();
     check(rc, st);
     return out;
   }
+
+  // the node norms of the last evaluation (pdf.hpp:88-92), fetched on demand
+  void refresh_norms() {
+    if (stale_) sync_norms();
+  }
+  void mark_evaluated() { evaluated(); }
 
   // K probes in one pass over the events (bitwise equal to K eval_metric calls)
   std::vector<double> eval_metric_batch(const std::vector<std::vector<double>>& ps, MetricKind metric) {
@@ -662,7 +678,7 @@ class BoundModel {
     pf_status st{};
     const int rc = pf_eval_metric_batch(model_, flat.data(), ps.size(), n,
                                         metric == MetricKind::ChiSquared ? PF_CHISQ : PF_NLL, out.data(), &st);
-    sync_norms();
+    evaluated();
     check(rc, st);
     return out;
   }
@@ -687,7 +703,13 @@ class BoundModel {
     for (std::size_t i = 0; i < pre_.size(); ++i)
       if (auto* poly = dynamic_cast<const PolynomialPdf*>(pre_[i])) poly->model_ = model_;
   }
+  void evaluated() {
+    stale_ = true;
+    if (!pre_.empty() && pre_[0]->owner_ != this)
+      for (const PdfNode* node : pre_) node->owner_ = this;
+  }
   void sync_norms() {
+    stale_ = false;
     const int n = static_cast<int>(pre_.size());
     std::vector<double> norms(n), errs(n);
     std::vector<int32_t> valid(n);
@@ -701,6 +723,7 @@ class BoundModel {
       }
   }
 
+  bool stale_ = false;
   PdfPtr pdf_;
   GridSpec grid_;
   bool binned_;
@@ -711,6 +734,10 @@ class BoundModel {
   std::vector<const PdfNode*> pre_;
   pf_model* model_ = nullptr;
 };
+
+inline void PdfNode::refresh() const {
+  if (owner_) owner_->refresh_norms();
+}
 
 // ---- fit.hpp ------------------------------------------------------------------
 enum class MinimizerKind { QuasiNewton, NelderMead };
@@ -774,9 +801,10 @@ inline FitResult fit(BoundModel& bm, MetricKind metric, const Backend& = Backend
   r.params = outp.data();
   r.uncertainties = outu.data();
   pf_status st{};
-  check(pf_fit(bm.handle(), metric == MetricKind::ChiSquared ? PF_CHISQ : PF_NLL, &c, start.data(),
-               fixed.data(), lo.data(), hi.data(), step.data(), &r, &st),
-        st);
+  const int rc = pf_fit(bm.handle(), metric == MetricKind::ChiSquared ? PF_CHISQ : PF_NLL, &c, start.data(),
+                        fixed.data(), lo.data(), hi.data(), step.data(), &r, &st);
+  bm.mark_evaluated();  // node norms: those of the fit's last evaluation
+  check(rc, st);
   FitResult out;
   out.status = static_cast<FitStatus>(r.status);
   for (const auto& p : reg.parameters()) out.names.push_back(p->name);

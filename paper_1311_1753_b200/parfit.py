@@ -962,7 +962,7 @@ def fit(bm: BoundModel, metric=MetricKind.NegLogLikelihood, backend=None,
     st = _abi.pf_status()
     rc = lib.pf_fit(bm._h, int(metric), C.byref(c), start, fixed, lower, upper, step, C.byref(res),
                     C.byref(st))
-    bm._sync_norms()
+    bm._evaluated()  # node norms: those of the fit's last evaluation (fetched on use)
     if rc:
         _raise(st)
     r = FitResult()
