@@ -44,11 +44,15 @@ def _worker(rank, world, port, n, out):
     acc = [0] * 6
     for v in terms:
         acc = [a + d for a, d in zip(acc, _digits_of(float(v)))]
-    t = torch.tensor(acc, dtype=torch.int64)
-    gathered = [torch.empty_like(t) for _ in range(world)]
-    dist.all_gather(gathered, t)
-    total = pf.combine_partials([g.tolist() for g in gathered])
-    reversed_total = pf.combine_partials([g.tolist() for g in gathered[::-1]])
+    # bench.py's exchange: 6 digits + penalty flag per rank, one flat gather
+    send = torch.empty(7, dtype=torch.int64)
+    send.numpy()[:] = acc + [0]
+    recv = torch.empty(7 * world, dtype=torch.int64)
+    dist.all_gather_into_tensor(recv, send)
+    rows = recv.view(world, 7).tolist()
+    assert not any(r[-1] for r in rows)
+    total = pf.combine_partials([r[:-1] for r in rows])
+    reversed_total = pf.combine_partials([r[:-1] for r in rows[::-1]])
     out[rank] = (total, reversed_total, int(count.value))
     dist.destroy_process_group()
 
