@@ -160,9 +160,9 @@ def cpu_side(W, pf, obs, pdf, cols, metric, fit=True, steps=3):
         sample = min(cols.shape[-1], 100_000)
         ds = W.data(pf, obs, sample)
     else:
-        sample = min(cols.shape[-1], 2_000_000)
+        sample = min(cols.shape[-1], 2_000_000 if W.name != "C5" else 200_000)
         ds = pf.UnbinnedDataSet.from_columns(obs, cols[..., :sample])
-    use_ref = oracle.Reference.available() and W.name != "C3"
+    use_ref = oracle.Reference.available() and W.has_reference
     if use_ref:
         kind, ev = "reference", oracle.Reference(pdf, ds, W.grid)
         call = lambda p: ev.eval(p, metric, threads)  # noqa: E731
@@ -203,7 +203,7 @@ def fit_leg(W, pf, obs, pdf, cols, device):
     r = pf.fit(bm, pf.MetricKind(W.metric))
     out = {"units": n, "gpu_wall_s": r.wall_time_s, "gpu_calls": r.n_metric_calls, "gpu_status": int(r.status),
            "params": dict(zip(r.names, r.params))}
-    if oracle.Reference.available() and W.name != "C3":
+    if oracle.Reference.available() and W.has_reference:
         for p in bm.registry().parameters():  # the fit wrote its result back: same start
             p.value = W.start[p.name]
         threads = os.cpu_count() or 1
@@ -224,18 +224,18 @@ def run_reference(args):
     import oracle
     from paper_1311_1753_b200 import parfit as pf
     W = WORKLOADS[args.config]
-    if not oracle.Reference.available() and W.name != "C3":
+    if not oracle.Reference.available() and W.has_reference:
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libparfit_ref.so not built"}))
         return
     obs, pdf = W.build(pf)
     n = args.events or W.default_n
     if W.unit == "bins":
         n = min(n, 100_000)  # one reference chi-squared call on 1e6 bins x Q=1024 takes ~7 s on 8 threads
-    elif W.name == "C3":
-        n = min(n, 2_000_000)
+    elif not W.has_reference:
+        n = min(n, 2_000_000 if W.name == "C3" else 200_000)
     ds = W.data(pf, obs, n)
     threads = os.cpu_count() or 1
-    if W.name == "C3":  # ArgusPdf: not in the reference; the C restatement stands in
+    if not W.has_reference:  # ArgusPdf / DalitzPlotPdf: the C restatement stands in
         kind, ev, threads = "port", oracle.Oracle(pdf, ds, W.grid), 1
         call = lambda p: ev.eval(p, W.metric)  # noqa: E731
     else:
@@ -434,7 +434,7 @@ def main():
             line["roofline"]["fp64_pipe_active_frac_ncu"] = fp64 / 100.0
         if issue is not None:
             line["roofline"]["issue_active_frac_ncu"] = issue / 100.0
-    if world == 1 and not args.no_fit and W.name != "C3":  # C3: no reference fit to compare with
+    if world == 1 and not args.no_fit and W.has_reference:  # otherwise no reference fit to compare with
         # full fit (fit.hpp:498-581) from the start point, GPU and reference
         # on the same bounded sample (at 1e7 events the reference's absolute
         # gradient tolerance is below the NLL's rounding noise and neither

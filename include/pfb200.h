@@ -36,8 +36,11 @@ extern "C" {
 #define PF_API
 #endif
 
-/* Node kinds: pdf.hpp:20-30 (Exponential..Convolution) plus ArgusPdf, which
- * the reference lacks (BASELINE config 3 needs it). */
+/* Node kinds: pdf.hpp:20-30 (Exponential..Convolution) plus ArgusPdf and
+ * DalitzPlotPdf, which the reference lacks (BASELINE configs 3 and 5; see
+ * DESIGN.md).  DalitzPlotPdf: obs = {m^2_12, m^2_13}; params = per resonance
+ * {mass, width, Re c, Im c}; reals = {M, m1, m2, m3, R, then per resonance
+ * channel (12, 13 or 23) and spin (0 or 1)}. */
 enum pf_kind {
   PF_EXPONENTIAL = 0,
   PF_GAUSSIAN = 1,
@@ -48,7 +51,8 @@ enum pf_kind {
   PF_COMPOSITE = 6,
   PF_MAPPED = 7,
   PF_CONVOLUTION = 8,
-  PF_ARGUS = 9
+  PF_ARGUS = 9,
+  PF_DALITZ = 10
 };
 
 /* MetricKind, engine.hpp:48 */

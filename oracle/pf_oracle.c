@@ -149,6 +149,83 @@ static void resolve_box(omodel* m, int id, int* colmap) { /* pdf.hpp:562-607 */
 
 /* ---- raw kernels (pdf.hpp:210-497) --------------------------------------- */
 static double raw(omodel* m, int id, double* evt, const double* p);
+/* DalitzPlotPdf (no reference kernel; parity unpinned): the GPU's
+ * pf_device.cuh pf_q2 / pf_dalitz_res / pf_dalitz_inside, same operation order
+ * (this file is compiled with -ffp-contract=off; the GPU uses explicitly
+ * rounded operations). */
+static double po_q2(double s, double ma, double mb) {
+  const double sp = ma + mb, sm = ma - mb;
+  const double v = ((s - sp * sp) * (s - sm * sm)) / (4.0 * s);
+  return v > 0.0 ? v : 0.0;
+}
+
+static void po_dalitz_res(double s, double Z, double m, double m2, double G, double q0, double br0, double mi,
+                          double mj, double R2, int spin, double* re, double* im) {
+  const double q2 = po_q2(s, mi, mj);
+  const double q = sqrt(q2);
+  const double x = q / q0;
+  double bf2 = 1.0, ratio = x;
+  if (spin == 1) {
+    bf2 = br0 / (1.0 + R2 * q2);
+    ratio = (x * x) * x;
+  }
+  const double gs = ((G * ratio) * (m / sqrt(s))) * bf2;
+  const double a = m2 - s, b = m * gs;
+  const double den = a * a + b * b;
+  const double f = (Z * sqrt(bf2)) / den;
+  *re = f * a;
+  *im = f * b;
+}
+
+static int po_dalitz_inside(double s12, double s13, double M, double m1, double m2, double m3) {
+  const double a12 = m1 + m2, b12 = M - m3;
+  if (!(s12 >= a12 * a12 && s12 <= b12 * b12)) return 0;
+  const double r12 = sqrt(s12);
+  const double e1 = ((s12 - m2 * m2) + m1 * m1) / (2.0 * r12);
+  const double e3 = ((M * M - s12) - m3 * m3) / (2.0 * r12);
+  const double t1 = e1 * e1 - m1 * m1, t3 = e3 * e3 - m3 * m3;
+  const double p1 = sqrt(t1 > 0.0 ? t1 : 0.0), p3 = sqrt(t3 > 0.0 ? t3 : 0.0);
+  const double e = e1 + e3, pp = p1 + p3, pm = p1 - p3;
+  const double lo = e * e - pp * pp, hi = e * e - pm * pm;
+  return s13 >= lo && s13 <= hi;
+}
+
+static double po_dalitz(const onode* o, const double* evt, const double* p) {
+  const double M = o->reals[0], m1 = o->reals[1], m2 = o->reals[2], m3 = o->reals[3], R = o->reals[4];
+  const double R2 = R * R;
+  const double ms[4] = {M, m1, m2, m3};
+  const double s12 = evt[o->ocol[0]], s13 = evt[o->ocol[1]];
+  if (!po_dalitz_inside(s12, s13, M, m1, m2, m3)) return 0.0;
+  double msum = M * M;
+  msum = msum + m1 * m1;
+  msum = msum + m2 * m2;
+  msum = msum + m3 * m3;
+  const double s23 = (msum - s12) - s13;
+  double are = 0.0, aim = 0.0;
+  const int nres = o->np / 4;
+  for (int r = 0; r < nres; ++r) {
+    const int ch = (int)o->reals[5 + 2 * r], spin = (int)o->reals[6 + 2 * r];
+    const int i = ch / 10, j = ch % 10, k = 6 - i - j;
+    const double sij = ch == 12 ? s12 : ch == 13 ? s13 : s23;
+    const double sik = ch == 12 ? s13 : s12;
+    const double sjk = ch == 12 ? s23 : ch == 13 ? s23 : s13;
+    double Z = 1.0;
+    if (spin == 1) {
+      const double a = M * M - ms[k] * ms[k];
+      const double b = ms[i] * ms[i] - ms[j] * ms[j];
+      Z = (sjk - sik) + (a * b) / sij;
+    }
+    const double m = p[o->p[4 * r]], mm2 = m * m, G = p[o->p[4 * r + 1]];
+    const double q20 = po_q2(mm2, ms[i], ms[j]);
+    double bre, bim;
+    po_dalitz_res(sij, Z, m, mm2, G, sqrt(q20), 1.0 + R2 * q20, ms[i], ms[j], R2, spin, &bre, &bim);
+    const double cre = p[o->p[4 * r + 2]], cim = p[o->p[4 * r + 3]];
+    are = are + (cre * bre - cim * bim);
+    aim = aim + (cre * bim + cim * bre);
+  }
+  return are * are + aim * aim;
+}
+
 
 static double density(omodel* m, int id, double* evt, const double* p) { /* pdf.hpp:83-91 */
   onode* o = &m->nodes[id];
@@ -189,6 +266,16 @@ static double raw(omodel* m, int id, double* evt, const double* p) {
         return 0.0;
       }
       return acc;
+    }
+    case PF_DALITZ: {
+      for (int r = 0; r < o->np / 4; ++r)
+        if (!(p[o->p[4 * r + 1]] > 0.0)) {
+          char buf[300];
+          snprintf(buf, sizeof buf, "%s: width must be > 0", o->name);
+          fail(m, "nonpositive-width", buf);
+          return 0.0;
+        }
+      return po_dalitz(o, evt, p);
     }
     case PF_ARGUS: { /* GooFit ArgusPdf, upper threshold; no reference kernel */
       double x = evt[o->ocol[0]];

@@ -552,6 +552,62 @@ __device__ __forceinline__ void pf_fac_accum(double& m, int& e, double v) {
 }
 
 // ----------------------------------------------------------------------------
+// DalitzPlotPdf pieces, every operation explicitly rounded (no contraction):
+// the C oracle (pf_oracle.c, -ffp-contract=off) evaluates the same sequence.
+struct pf_cplx {
+  double re, im;
+};
+
+// q^2 of a two-body split of invariant mass^2 s into masses ma, mb
+__device__ __forceinline__ double pf_q2(double s, double ma, double mb) {
+  const double sp = __dadd_rn(ma, mb), sm = __dsub_rn(ma, mb);
+  const double v = __ddiv_rn(__dmul_rn(__dsub_rn(s, __dmul_rn(sp, sp)), __dsub_rn(s, __dmul_rn(sm, sm))),
+                             __dmul_rn(4.0, s));
+  return v > 0.0 ? v : 0.0;
+}
+
+// one resonance: Z B(q)/B(q0) / (m^2 - s - i m Gamma(s)),
+// Gamma(s) = G (q/q0)^(2J+1) (m / sqrt s) (B(q)/B(q0))^2, B_1(q)^2 = 1/(1 + R^2 q^2).
+// m2, q0, br0 = 1 + R^2 q0^2 are per-call constants (pf_stage_pre).
+__device__ __forceinline__ pf_cplx pf_dalitz_res(double s, double Z, double m, double m2, double G,
+                                                 double q0, double br0, double mi, double mj, double R2,
+                                                 int spin) {
+  const double q2 = pf_q2(s, mi, mj);
+  const double q = __dsqrt_rn(q2);
+  const double x = __ddiv_rn(q, q0);
+  double bf2 = 1.0, ratio = x;  // (B(q)/B(q0))^2, (q/q0)^(2J+1)
+  if (spin == 1) {
+    bf2 = __ddiv_rn(br0, __dadd_rn(1.0, __dmul_rn(R2, q2)));
+    ratio = __dmul_rn(__dmul_rn(x, x), x);
+  }
+  const double gs = __dmul_rn(__dmul_rn(__dmul_rn(G, ratio), __ddiv_rn(m, __dsqrt_rn(s))), bf2);
+  const double a = __dsub_rn(m2, s), b = __dmul_rn(m, gs);
+  const double den = __dadd_rn(__dmul_rn(a, a), __dmul_rn(b, b));
+  const double f = __ddiv_rn(__dmul_rn(Z, __dsqrt_rn(bf2)), den);
+  pf_cplx r;
+  r.re = __dmul_rn(f, a);
+  r.im = __dmul_rn(f, b);
+  return r;
+}
+
+// inside the kinematic boundary of the (m12^2, m13^2) plane
+__device__ __forceinline__ bool pf_dalitz_inside(double s12, double s13, double M, double m1, double m2,
+                                                 double m3) {
+  const double a12 = __dadd_rn(m1, m2), b12 = __dsub_rn(M, m3);
+  if (!(s12 >= __dmul_rn(a12, a12) && s12 <= __dmul_rn(b12, b12))) return false;
+  const double r12 = __dsqrt_rn(s12);
+  const double e1 = __ddiv_rn(__dadd_rn(__dsub_rn(s12, __dmul_rn(m2, m2)), __dmul_rn(m1, m1)), __dmul_rn(2.0, r12));
+  const double e3 = __ddiv_rn(__dsub_rn(__dsub_rn(__dmul_rn(M, M), s12), __dmul_rn(m3, m3)), __dmul_rn(2.0, r12));
+  double t1 = __dsub_rn(__dmul_rn(e1, e1), __dmul_rn(m1, m1));
+  double t3 = __dsub_rn(__dmul_rn(e3, e3), __dmul_rn(m3, m3));
+  const double p1 = __dsqrt_rn(t1 > 0.0 ? t1 : 0.0), p3 = __dsqrt_rn(t3 > 0.0 ? t3 : 0.0);
+  const double e = __dadd_rn(e1, e3), pp = __dadd_rn(p1, p3), pm = __dsub_rn(p1, p3);
+  const double lo = __dsub_rn(__dmul_rn(e, e), __dmul_rn(pp, pp));
+  const double hi = __dsub_rn(__dmul_rn(e, e), __dmul_rn(pm, pm));
+  return s13 >= lo && s13 <= hi;
+}
+
+// ----------------------------------------------------------------------------
 // TMA bulk copies (cp.async.bulk, global -> shared) completed on mbarriers.
 __device__ __forceinline__ unsigned pf_smem_addr(const void* p) {
   return (unsigned)__cvta_generic_to_shared(p);

@@ -21,6 +21,7 @@ const char* kind_name(int kind) {
     case PF_MAPPED: return "MappedPdf";
     case PF_CONVOLUTION: return "ConvolutionPdf";
     case PF_ARGUS: return "ArgusPdf";
+    case PF_DALITZ: return "DalitzPlotPdf";
   }
   return "unknown";
 }
@@ -114,6 +115,27 @@ void validate_node(const pf_graph& g, int idx) {
       require(g.variables[n.params[0]].lower > 0, "nonpositive-endpoint",
               name + ": m0 limits must exclude 0");
       break;
+    case PF_DALITZ: {  // DalitzPlotPdf(m12^2, m13^2; resonances), new
+      require(n.n_obs == 2 && is_obs(n.obs[0]) && is_obs(n.obs[1]), "wrong-role",
+              name + ": m12^2 and m13^2 must be observables");
+      const int nres = n.n_params / 4;
+      require(nres >= 1 && n.n_params == 4 * nres, "bad-arity",
+              name + ": need (mass, width, Re c, Im c) per resonance");
+      require(n.n_reals == 5 + 2 * nres, "bad-arity", name + ": need M, m1, m2, m3, R and (channel, spin) per resonance");
+      for (int i = 0; i < n.n_params; ++i)
+        require(is_par(n.params[i]), "wrong-role", name + ": resonance constants must be parameters");
+      for (int r = 0; r < nres; ++r) {
+        const double ch = n.reals[5 + 2 * r], sp = n.reals[6 + 2 * r];
+        require(ch == 12 || ch == 13 || ch == 23, "bad-channel", name + ": channel must be 12, 13 or 23");
+        require(sp == 0 || sp == 1, "bad-spin", name + ": spin must be 0 or 1");
+        require(g.variables[n.params[4 * r + 1]].lower > 0, "nonpositive-width",
+                name + ": width limits must exclude 0");
+      }
+      require(n.reals[0] > n.reals[1] + n.reals[2] + n.reals[3] && n.reals[1] >= 0 && n.reals[2] >= 0 &&
+                  n.reals[3] >= 0 && n.reals[4] >= 0,
+              "bad-kinematics", name + ": need M > m1 + m2 + m3, masses and R >= 0");
+      break;
+    }
     case PF_PRODUCT:  // pdf.hpp:332-337
       require(n.n_children >= 2, "bad-arity", name + ": product needs >= 2 children");
       require(n.n_params == 0 && n.n_obs == 0, "bad-arity", name + ": product has no own variables");
@@ -367,6 +389,7 @@ Program finalize(const pf_graph& g, int n_data_obs, const int32_t* data_obs, int
 double subtree_cost(const Program& pg, int node) {
   const Node& n = pg.nodes[node];
   double c = 1.0;
+  if (n.kind == PF_DALITZ) return 8.0 * static_cast<double>(n.params.size() / 4);  // per resonance
   if (n.kind == PF_CONVOLUTION) {
     // model values are hoisted per call; the resolution runs Q times
     return 1.0 + static_cast<double>(n.q) * subtree_cost(pg, n.children[1]);

@@ -435,6 +435,44 @@ class ArgusPdf(PdfNode):
         self._params = [m0, c, p]
 
 
+class DalitzPlotPdf(PdfNode):
+    """Time-integrated isobar model over the Dalitz plot of M -> 1 2 3:
+    |sum_r c_r BW_r|^2 inside the kinematic boundary, 0 outside.
+    Observables m12^2, m13^2.  Each resonance is (mass, width, Re c, Im c)
+    parameters plus a channel (12, 13 or 23) and spin (0 or 1); BW_r is a
+    relativistic Breit-Wigner with mass-dependent width, Blatt-Weisskopf
+    barrier (radius R) and Zemach spin factor (pf_device.cuh / pf_oracle.c).
+    Not in the reference; BASELINE config 5's amplitude part."""
+
+    kind = _abi.PF_DALITZ
+
+    def __init__(self, name, m12sq, m13sq, resonances, masses, radius=1.5):
+        super().__init__(name)
+        _need_obs(name, m12sq, "m12sq")
+        _need_obs(name, m13sq, "m13sq")
+        M, m1, m2, m3 = (float(v) for v in masses)
+        if not (M > m1 + m2 + m3 and min(m1, m2, m3) >= 0 and radius >= 0):
+            raise Error("bad-kinematics", f"{name}: need M > m1 + m2 + m3, masses and R >= 0")
+        if not resonances:
+            raise Error("bad-arity", f"{name}: need >= 1 resonance")
+        params, reals = [], [M, m1, m2, m3, float(radius)]
+        for res in resonances:
+            mass, width, cre, cim, channel, spin = res
+            for v, w in ((mass, "mass"), (width, "width"), (cre, "Re c"), (cim, "Im c")):
+                _need_par(name, v, w)
+            if channel not in (12, 13, 23):
+                raise Error("bad-channel", f"{name}: channel must be 12, 13 or 23")
+            if spin not in (0, 1):
+                raise Error("bad-spin", f"{name}: spin must be 0 or 1")
+            if not (width.lower > 0):
+                raise Error("nonpositive-width", f"{name}: width limits must exclude 0")
+            params += [mass, width, cre, cim]
+            reals += [float(channel), float(spin)]
+        self._obs = [m12sq, m13sq]
+        self._params = params
+        self._reals = reals
+
+
 class ProdPdf(PdfNode):
     kind = _abi.PF_PRODUCT
 
@@ -524,6 +562,11 @@ def breit_wigner_pdf(name, x, mass, width):
 
 def polynomial_pdf(name, x, coeffs):
     return PolynomialPdf(name, x, coeffs)
+
+
+def dalitz_pdf(name, m12sq, m13sq, resonances, masses, radius=1.5):
+    """resonances: [(mass, width, Re c, Im c, channel, spin), ...]"""
+    return DalitzPlotPdf(name, m12sq, m13sq, resonances, masses, radius)
 
 
 def argus_pdf(name, x, m0, c, p):

@@ -24,6 +24,7 @@ class Workload:
     scaling = "weak"
     grid = 1024
     fit_n = 100_000       # events (bins) of the full-fit wall-time comparison
+    has_reference = True  # False: a PDF the reference lacks (CPU legs use the C restatement)
     start: dict = {}
     truth: dict = {}
 
@@ -128,6 +129,7 @@ class C3(Workload):
     description = "ProdPdf(GaussianPdf(x), ArgusPdf(y)), x in [0, 10], y in [5.20, 5.29]"
     default_n = 100_000_000
     scaling = "strong"
+    has_reference = False  # ArgusPdf
     start = dict(m=4.9, s=1.05, m0=5.29, c=-19.0, p=0.55)
     truth = dict(m=5.0, s=1.0, m0=5.29, c=-20.0, p=0.5)
     ylo, yhi = 5.20, 5.29
@@ -219,4 +221,130 @@ class C4(Workload):
         return 24.0  # EventTable row: bin centre, content, volume (dataset.hpp:161-182)
 
 
-WORKLOADS = {w.name: w for w in (C1(), C2(), C3(), C4())}
+def dalitz_amplitude2(s12, s13, M, ms, R, res):
+    """numpy |A|^2 of the isobar model (the generator's copy of the kernels in
+    pf_device.cuh / pf_oracle.c; used only to draw toy events)"""
+    m1, m2, m3 = ms
+    mm = {1: m1, 2: m2, 3: m3}
+    s12 = np.asarray(s12, dtype=np.float64)
+    s13 = np.asarray(s13, dtype=np.float64)
+    s23 = M * M + m1 * m1 + m2 * m2 + m3 * m3 - s12 - s13
+    # kinematic boundary (12 rest frame)
+    r12 = np.sqrt(np.clip(s12, 1e-300, None))
+    e1 = (s12 - m2 * m2 + m1 * m1) / (2 * r12)
+    e3 = (M * M - s12 - m3 * m3) / (2 * r12)
+    p1 = np.sqrt(np.clip(e1 * e1 - m1 * m1, 0, None))
+    p3 = np.sqrt(np.clip(e3 * e3 - m3 * m3, 0, None))
+    lo = (e1 + e3) ** 2 - (p1 + p3) ** 2
+    hi = (e1 + e3) ** 2 - (p1 - p3) ** 2
+    inside = (s12 >= (m1 + m2) ** 2) & (s12 <= (M - m3) ** 2) & (s13 >= lo) & (s13 <= hi)
+
+    def q2(s, a, b):
+        return np.clip((s - (a + b) ** 2) * (s - (a - b) ** 2) / (4 * s), 0, None)
+
+    A = np.zeros_like(s12, dtype=np.complex128)
+    for mass, width, cre, cim, ch, spin in res:
+        i, j = ch // 10, ch % 10
+        k = 6 - i - j
+        sv = {12: s12, 13: s13, 23: s23}
+        sij = sv[ch]
+        sik = sv[int(f"{min(i, k)}{max(i, k)}")]
+        sjk = sv[int(f"{min(j, k)}{max(j, k)}")]
+        qq = q2(sij, mm[i], mm[j])
+        q0 = q2(mass * mass, mm[i], mm[j])
+        x = np.sqrt(qq) / np.sqrt(q0)
+        if spin == 1:
+            bf2 = (1 + R * R * q0) / (1 + R * R * qq)
+            ratio = x ** 3
+            Z = sjk - sik + (M * M - mm[k] ** 2) * (mm[i] ** 2 - mm[j] ** 2) / sij
+        else:
+            bf2, ratio, Z = 1.0, x, 1.0
+        g = width * ratio * mass / np.sqrt(sij) * bf2
+        A += complex(cre, cim) * Z * np.sqrt(bf2) / (mass * mass - sij - 1j * mass * g)
+    return np.where(inside, np.abs(A) ** 2, 0.0)
+
+
+class C5(Workload):
+    name = "C5"
+    description = ("DalitzPlotPdf D0 -> pi+ pi- pi0 (rho+, rho-, rho0, f0(980) isobars), time-integrated, "
+                   "m12^2 x m13^2 grid 1024")
+    default_n = 10_000_000
+    fit_n = 20_000
+    has_reference = False  # DalitzPlotPdf
+    M, ms, R = 1.86484, (0.13957, 0.13957, 0.13498), 1.5
+    # (name, channel, spin, mass, width, Re c, Im c); rho+ is the reference amplitude
+    res = [("rhop", 13, 1, 0.7753, 0.1491, 1.0, 0.0),
+           ("rhom", 23, 1, 0.7753, 0.1491, 0.65, 0.05),
+           ("rho0", 12, 1, 0.7753, 0.1491, 0.53, 0.16),
+           ("f0", 12, 0, 0.980, 0.050, 0.08, 0.12)]
+    truth = {}
+    start = {}
+    for _n, _ch, _sp, _m, _w, _re, _im in res:
+        truth.update({f"{_n}_m": _m, f"{_n}_w": _w, f"{_n}_re": _re, f"{_n}_im": _im})
+        start.update({f"{_n}_m": _m, f"{_n}_w": _w * 1.02, f"{_n}_re": _re * 0.98 if _re != 1.0 else 1.0,
+                      f"{_n}_im": _im + 0.01 if _n != "rhop" else 0.0})
+
+    @classmethod
+    def box(cls):
+        M, (m1, m2, m3) = cls.M, cls.ms
+        return ((m1 + m2) ** 2, (M - m3) ** 2), ((m1 + m3) ** 2, (M - m2) ** 2)
+
+    def build(self, pf):
+        (a12, b12), (a13, b13) = self.box()
+        s12 = pf.new_observable("m12sq", a12, b12)
+        s13 = pf.new_observable("m13sq", a13, b13)
+        resonances = []
+        for nm, ch, sp, m, w, re, im in self.res:
+            mv = pf.new_parameter(f"{nm}_m", self.start[f"{nm}_m"], 0.001, m - 0.05, m + 0.05)
+            wv = pf.new_parameter(f"{nm}_w", self.start[f"{nm}_w"], 0.001, 0.01, 0.5)
+            cr = pf.new_parameter(f"{nm}_re", self.start[f"{nm}_re"], 0.01, -5.0, 5.0)
+            ci = pf.new_parameter(f"{nm}_im", self.start[f"{nm}_im"], 0.01, -5.0, 5.0)
+            mv.fixed = wv.fixed = True  # lineshapes fixed, couplings float
+            if nm == "rhop":
+                cr.fixed = ci.fixed = True  # the reference amplitude
+            resonances.append((mv, wv, cr, ci, ch, sp))
+        return [s12, s13], pf.dalitz_pdf("d0pipipi0", s12, s13, resonances, (self.M,) + self.ms, self.R)
+
+    @classmethod
+    def columns(cls, n, seed=11):
+        """accept-reject with the truth couplings under a piecewise-constant
+        envelope (64 x 64 cells, cell maxima from 16 x 16 sub-samples x 1.5)"""
+        rng = np.random.default_rng(seed)
+        (a12, b12), (a13, b13) = cls.box()
+        res = [(m, w, re, im, ch, sp) for _, ch, sp, m, w, re, im in cls.res]
+        nc, sub = 64, 16
+        h12, h13 = (b12 - a12) / nc, (b13 - a13) / nc
+        u = (np.arange(sub) + 0.5) / sub
+        f12 = (a12 + (np.arange(nc)[:, None] + u[None, :]) * h12).ravel()
+        f13 = (a13 + (np.arange(nc)[:, None] + u[None, :]) * h13).ravel()
+        g12, g13 = np.meshgrid(f12, f13, indexing="ij")
+        with np.errstate(all="ignore"):
+            v = dalitz_amplitude2(g12.ravel(), g13.ravel(), cls.M, cls.ms, cls.R, res)
+        env = 1.5 * v.reshape(nc, sub, nc, sub).max(axis=(1, 3)).ravel()
+        env[env <= 0] = 0.0
+        # cells touching the boundary: their sub-sample max may miss the plot
+        p = env / env.sum()
+        out = np.empty((2, n))
+        filled = 0
+        while filled < n:
+            k = min(2 * (n - filled) + 4096, 1 << 22)
+            cell = rng.choice(nc * nc, size=k, p=p)
+            c12 = a12 + (cell // nc + rng.random(k)) * h12
+            c13 = a13 + (cell % nc + rng.random(k)) * h13
+            with np.errstate(all="ignore"):
+                f = dalitz_amplitude2(c12, c13, cls.M, cls.ms, cls.R, res)
+            keep = rng.random(k) * env[cell] < f
+            take = min(int(keep.sum()), n - filled)
+            out[0, filled:filled + take] = c12[keep][:take]
+            out[1, filled:filled + take] = c13[keep][:take]
+            filled += take
+        return out
+
+    def data(self, pf, obs, n, seed=11):
+        return pf.UnbinnedDataSet.from_columns(obs, self.columns(n, seed))
+
+    def bytes_per_unit(self):
+        return 16.0
+
+
+WORKLOADS = {w.name: w for w in (C1(), C2(), C3(), C4(), C5())}

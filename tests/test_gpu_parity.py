@@ -227,3 +227,23 @@ def test_c4_binned_convolution_vs_reference():
         got = bm.eval_metric(p, pf.MetricKind.ChiSquared)
         want = ref.eval(p, 1)
         assert close(got, want), (pt, got, want)
+
+
+def test_c5_dalitz_vs_oracle():
+    """C5 shape: DalitzPlotPdf, 4 isobars, 2-D normalisation grid (128 here so
+    the oracle's walk stays short).  No reference code: parity against the C
+    restatement, itself checked against numpy in test_oracle.py."""
+    W = WORKLOADS["C5"]
+    obs, pdf = W.build(pf)
+    ds = pf.UnbinnedDataSet.from_columns(obs, W.columns(20_011, seed=4))
+    bm = pf.BoundModel(pdf, ds, pf.GridSpec(128))
+    o = oracle.Oracle(pdf, ds, 128)
+    names = [p.name for p in bm.registry().parameters()]
+    nodes = pf.GraphDesc(pdf, obs).preorder()
+    bumped = dict(W.truth, rhom_re=0.5, rho0_im=0.3, f0_re=0.2)
+    for pt in (W.start, W.truth, bumped):
+        p = [pt[n] for n in names]
+        got, want = bm.eval_metric(p), o.eval(p)
+        assert close(got, want), (got, want)
+        norms, _, valid = o.norms()
+        assert valid[0] and close(nodes[0].cached_norm(), norms[0])

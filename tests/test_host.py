@@ -189,6 +189,24 @@ def test_argus_evaluator_compiles():
     assert pf.lib.pf_graph_compile_check(C.byref(g.c_graph), C.byref(data), 1024, C.byref(n), C.byref(st)) == 0
 
 
+def test_dalitz_evaluator_compiles_and_validates():
+    from paper_1311_1753_b200.workloads import WORKLOADS
+    W = WORKLOADS["C5"]
+    obs, pdf = W.build(pf)
+    g = pf.GraphDesc(pdf, obs)
+    o = (C.c_int32 * 2)(g.var_index(obs[0]), g.var_index(obs[1]))
+    data = _abi.pf_data(0, 2, o, 0, None, 0.0)
+    st, n = _abi.pf_status(), C.c_size_t()
+    assert pf.lib.pf_graph_compile_check(C.byref(g.c_graph), C.byref(data), 1024, C.byref(n), C.byref(st)) == 0
+    m = pf.new_parameter("m", 0.77, 0.01, 0.5, 1.0)
+    w = pf.new_parameter("w", 0.15, 0.01, 0.01, 0.5)
+    c = pf.new_parameter("c", 1.0, 0.01, -5, 5)
+    with pytest.raises(pf.Error, match="bad-channel"):
+        pf.dalitz_pdf("d", obs[0], obs[1], [(m, w, c, c, 14, 1)], (1.86, 0.14, 0.14, 0.13))
+    with pytest.raises(pf.Error, match="bad-kinematics"):
+        pf.dalitz_pdf("d", obs[0], obs[1], [(m, w, c, c, 12, 1)], (0.3, 0.14, 0.14, 0.13))
+
+
 def _digits_of(x):
     """exact superaccumulator digits of a double (python restatement of
     pf_fxl_add: value = sum d_i 2^(32 i - 128), truncation below 2^-128)"""

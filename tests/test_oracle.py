@@ -113,3 +113,28 @@ def test_mt64_matches_std():
     """std::mt19937_64 default seed 5489: 10000th output is 9981545732273789042"""
     u = oracle.mt64_uniform(5489, 10000)
     assert int(u[-1] * 2 ** 53) == 9981545732273789042 >> 11
+
+
+def test_dalitz_restatement_vs_numpy():
+    """DalitzPlotPdf has no reference code (parity unpinned): the C oracle's
+    amplitude is checked against an independent numpy implementation of the
+    same formulas (workloads.dalitz_amplitude2): density / |A|^2 must be the
+    constant 1/norm at every point of the plot, and 0 outside."""
+    import numpy as np
+    from paper_1311_1753_b200.workloads import WORKLOADS, dalitz_amplitude2
+    W = WORKLOADS["C5"]
+    obs, pdf = W.build(pf)
+    pts = W.columns(2000, seed=3)
+    ds = pf.UnbinnedDataSet.from_columns(obs, pts)
+    o = oracle.Oracle(pdf, ds, 64)
+    names = o.param_names()
+    p = [W.truth[n] for n in names]
+    dens = o.density(p, pts)
+    res = [(m, w, re, im, ch, sp) for _, ch, sp, m, w, re, im in W.res]
+    ref = dalitz_amplitude2(pts[0], pts[1], W.M, W.ms, W.R, res)
+    ratio = dens / ref
+    assert np.all(ref > 0)
+    assert np.max(np.abs(ratio / ratio[0] - 1.0)) < 1e-12
+    (a12, b12), (a13, b13) = W.box()
+    corner = np.array([[b12 - 1e-6], [b13 - 1e-6]])  # far outside the plot
+    assert o.density(p, corner)[0] == 0.0
