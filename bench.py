@@ -278,6 +278,8 @@ def main():
     ap.add_argument("--events", type=int, default=0, help="events (bins) per GPU; 0: the config's size")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fit", action="store_true")
+    ap.add_argument("--force-exchange", action="store_true",
+                    help="run the multi-rank exchange path even with one rank (tests it on one GPU)")
     ap.add_argument("--diag-no-flush", action="store_true",
                     help="diagnostics only: keep L2 warm between steps (never a reported number)")
     args = ap.parse_args()
@@ -290,7 +292,8 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     dist = None
-    if world > 1:
+    multi = world > 1 or args.force_exchange
+    if multi:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local)
@@ -318,25 +321,33 @@ def main():
     import ctypes as C
     from paper_1311_1753_b200 import _abi
 
-    if world > 1:
-        # the exchange: every rank's 6 exact digits + penalty flag (56 bytes)
-        # all-gathered over NCCL; staging buffers allocated once
+    if multi:
+        # the exchange, stream-ordered on the model's own stream: the event
+        # pass writes its exact digits to a device record (aliased here as a
+        # torch tensor), NCCL all-gathers the 64-byte records, one D2H brings
+        # them to the host, where every rank combines them identically
         import torch
-        send_h = torch.empty(7, dtype=torch.int64, pin_memory=True)
-        send_d = torch.empty(7, dtype=torch.int64, device=f"cuda:{local}")
-        recv_d = torch.empty(7 * world, dtype=torch.int64, device=f"cuda:{local}")
+
+        class _DeviceRecord:
+            def __init__(self, ptr, n):
+                self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<i8", "data": (ptr, False),
+                                                 "version": 3}
+
+        part_d = torch.as_tensor(_DeviceRecord(bm.partial_device(), 8), device=f"cuda:{local}")
+        model_stream = torch.cuda.ExternalStream(bm.stream(), device=f"cuda:{local}")
+        recv_d = torch.empty(8 * world, dtype=torch.int64, device=f"cuda:{local}")
 
     def step_value(p):
-        if world == 1:
+        if not multi:
             return bm.eval_metric(p, metric)
-        fx, pen = bm.eval_partial(p, metric)
-        send_h.numpy()[:] = fx + [1 if pen else 0]
-        send_d.copy_(send_h, non_blocking=True)
-        dist.all_gather_into_tensor(recv_d, send_d)
-        rows = recv_d.cpu().view(world, 7).tolist()  # one D2H: the value goes back to the host
-        if any(r[-1] for r in rows):
+        if bm.eval_launch(p, metric):  # invalid parameters: the same on every rank
             return pf.kPenaltyValue
-        return pf.combine_partials([r[:-1] for r in rows])
+        with torch.cuda.stream(model_stream):
+            dist.all_gather_into_tensor(recv_d, part_d)
+            rows = recv_d.cpu().view(world, 8).tolist()
+        if any(r[6] != 0xFFFFFFFF or r[7] for r in rows):  # zero integral or a non-finite term
+            return pf.kPenaltyValue
+        return pf.combine_partials([r[:6] for r in rows])
 
     for _ in range(args.warmup):
         step_value(params)
@@ -344,7 +355,7 @@ def main():
 
     sampler = ClockSampler(local) if rank == 0 else None
     launches0 = pf.kernel_launches()
-    if world == 1:
+    if not multi:
         res = _abi.pf_bench_result()
         st = _abi.pf_status()
         with sampler:
@@ -372,7 +383,7 @@ def main():
         ms_step = dt.item() / args.steps * 1e3
         ev_ms = None
         launches = pf.kernel_launches() - launches0
-        h2d, d2h = 8 * params.size, 88
+        h2d, d2h = 8 * params.size, 64 * world
 
     # e2e: the public API call (pf_eval_metric via BoundModel.eval_metric) with
     # host parameters in and the host scalar out, host wall clock, L2 flushed
@@ -387,7 +398,7 @@ def main():
         step_value(params)
         e2e_times.append(time.perf_counter() - t)
     e2e_s = statistics.mean(e2e_times)
-    if world > 1:
+    if multi:
         v = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{local}")
         dist.all_reduce(v, op=dist.ReduceOp.MAX)
         e2e_s = v.item()

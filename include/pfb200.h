@@ -212,6 +212,19 @@ PF_API int pf_eval_metric_batch(pf_model* model, const double* params, size_t k,
 PF_API int pf_eval_partial(pf_model* model, const double* params, size_t n_params, int32_t metric,
                            int64_t* partial_fx, int32_t* penalty, pf_status* status);
 
+/* Multi-process exchange without a host round trip (single-device models):
+ * pf_eval_launch enqueues one evaluation on the model's stream and returns
+ * at once (*penalty set, nothing enqueued, when the parameters are invalid).
+ * The event pass also writes a device record of 8 int64 at
+ * pf_model_partial_device(): the PF_FX_DIGITS exact digits, the norm error
+ * word (~0u when none) and a nonzero flag on a non-finite term or event error.
+ * A collective enqueued on pf_model_stream() (cudaStream_t as an integer)
+ * after the launch sees the record. */
+PF_API int pf_eval_launch(pf_model* model, const double* params, size_t n_params, int32_t metric,
+                          int32_t* penalty, pf_status* status);
+PF_API uint64_t pf_model_stream(const pf_model* model);
+PF_API uint64_t pf_model_partial_device(const pf_model* model);
+
 /* Exact combine of shard_count accumulators (shard_count x PF_FX_DIGITS) and
  * the correctly rounded metric: bitwise the single-device value. */
 PF_API double pf_combine_partials(const int64_t* partials_fx, int32_t shard_count);

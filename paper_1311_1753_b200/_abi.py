@@ -120,6 +120,10 @@ _SIGNATURES = {
     "pf_abi_version": (C.c_int32, []),
     "pf_kernel_launches": (C.c_uint64, []),
     "pf_debug_trace": (C.c_int64, [C.c_void_p, C.POINTER(C.c_uint64), C.c_int64]),
+    "pf_eval_launch": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int32, C.POINTER(C.c_int32),
+                                 C.POINTER(pf_status)]),
+    "pf_model_stream": (C.c_uint64, [C.c_void_p]),
+    "pf_model_partial_device": (C.c_uint64, [C.c_void_p]),
 }
 
 

@@ -169,6 +169,24 @@ int pf_eval_partial(pf_model* model, const double* params, size_t n_params, int3
   });
 }
 
+int pf_eval_launch(pf_model* model, const double* params, size_t n_params, int32_t metric, int32_t* penalty,
+                   pf_status* status) {
+  return guarded(status, [&] {
+    if (!model || !penalty) throw pfb::Error("bad-model", "null argument");
+    int pen = 0;
+    model->impl->eval_launch(params, n_params, metric, &pen);
+    *penalty = pen;
+  });
+}
+
+uint64_t pf_model_stream(const pf_model* model) {
+  return model ? reinterpret_cast<uint64_t>(model->impl->stream()) : 0;
+}
+
+uint64_t pf_model_partial_device(const pf_model* model) {
+  return model ? reinterpret_cast<uint64_t>(model->impl->partial_device()) : 0;
+}
+
 double pf_combine_partials(const int64_t* partials_fx, int32_t shard_count) {
   int64_t fx[PF_FX_DIGITS] = {0, 0, 0, 0, 0, 0};
   for (int32_t s = 0; s < shard_count; ++s)

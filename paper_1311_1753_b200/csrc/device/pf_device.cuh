@@ -89,6 +89,7 @@ struct pf_args {
   double total_content; // binned: N_tot (engine.hpp:153)
   pf_u32* done;         // [finished-block counter (self-resetting), per-k completion sequence]
   long long* fxbins;    // K x PF_FX_BINS x 16: binned block digits (self-resetting)
+  long long* dpart;     // K x 8 (device): exact digits, norm error, event-error flag of this call
   int npin;             // K = 1: parameters passed inline (pin[0..npin))
   int pad1;
   double pin[PF_MAX_INLINE];

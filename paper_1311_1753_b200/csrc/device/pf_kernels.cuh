@@ -61,6 +61,10 @@ __device__ void pf_publish(const pf_args& a, int k, int tid, int nt) {
   if (tid == 0) {
     long long fx[PF_FX_DIGITS];
     for (int i = 0; i < PF_FX_DIGITS; ++i) fx[i] = (long long)__ldcg((const unsigned long long*)(r->fx + i));
+    long long* dp = a.dpart + (pf_u64)k * 8;
+    for (int i = 0; i < PF_FX_DIGITS; ++i) dp[i] = fx[i];
+    dp[6] = (long long)__ldcg(&r->norm_error);
+    dp[7] = (__ldcg(&r->first_nonfinite) != ~0ull || __ldcg(&r->first_event_error) != ~0ull) ? 1 : 0;
     o->result = pf_fx_round(fx);
     for (int i = 0; i < PF_FX_DIGITS; ++i) o->fx[i] = fx[i];
     o->floor_count = __ldcg(&r->floor_count);
@@ -896,6 +900,11 @@ extern "C" __global__ void __launch_bounds__(PF_EV_THREADS, PF_EVENT_MIN_BLOCKS)
       }
       pf_out* o = a.hout + k;
       if (lane == 0) {
+        long long* dp = a.dpart + (pf_u64)k * 8;  // the device copy, for a stream-ordered collective
+#pragma unroll
+        for (int i = 0; i < PF_FX_DIGITS; ++i) dp[i] = d[i];
+        dp[6] = (long long)normerr;
+        dp[7] = (nonfinite != ~0ull || evterr != ~0ull) ? 1 : 0;
         o->result = pf_fx_round(d);
 #pragma unroll
         for (int i = 0; i < PF_FX_DIGITS; ++i) o->fx[i] = d[i];

@@ -277,6 +277,8 @@ Model::Model(const pf_graph& g, const pf_data& d, uint32_t grid_points, const pf
     ck(cudaMalloc(&sh.d_partials, 16 * part_elems), "cudaMalloc partials");
     ck(cudaMalloc(&sh.d_done, sizeof(uint32_t) * (1 + kMaxBatch)), "cudaMalloc done");
     ck(cudaMemset(sh.d_done, 0, sizeof(uint32_t) * (1 + kMaxBatch)), "memset done");
+    ck(cudaMalloc(&sh.d_part, sizeof(int64_t) * 8 * kMaxBatch), "cudaMalloc partial");
+    ck(cudaMemset(sh.d_part, 0, sizeof(int64_t) * 8 * kMaxBatch), "memset partial");
     const size_t bins = sizeof(int64_t) * kMaxBatch * kFxBins * 16;
     ck(cudaMalloc(&sh.d_fxbins, bins), "cudaMalloc fxbins");
     ck(cudaMemset(sh.d_fxbins, 0, bins), "memset fxbins");
@@ -332,6 +334,7 @@ Model::~Model() {
     cudaFree(sh.d_partials);
     cudaFree(sh.d_done);
     cudaFree(sh.d_fxbins);
+    cudaFree(sh.d_part);
     cudaFree(sh.d_rec);
     cudaFree(sh.d_clamp);
     cudaFreeHost(sh.h_out);
@@ -430,6 +433,7 @@ Args Model::base_args(Shard& sh, int K) {
   a.partials = sh.d_partials;
   a.done = sh.d_done;
   a.fxbins = sh.d_fxbins;
+  a.dpart = sh.d_part;
   a.rec = sh.d_rec;
   a.total_content = total_content_;
   // norm-stage clamps are counted once (shard 0); the others discard them
@@ -552,7 +556,11 @@ std::string Model::error_message(uint32_t code_node) const {
 }
 
 void Model::run(const double* params, int K, std::vector<Raw>& out, bool partial_only) {
-  const size_t np = std::max(L_.np, 1);
+  launch_graphs(params, K);
+  wait_results(K, out, partial_only);
+}
+
+void Model::launch_graphs(const double* params, int K) {
   if (L_.np > 0) std::memcpy(h_params_, params, sizeof(double) * K * L_.np);
   for (Shard& sh : shards_) {
     cudaGraphExec_t g = graph_for(sh, K);
@@ -576,6 +584,10 @@ void Model::run(const double* params, int K, std::vector<Raw>& out, bool partial
     g_launches += sh.kernels_per_graph;
     for (int k = 0; k < K; ++k) ++sh.seq[k];
   }
+}
+
+void Model::wait_results(int K, std::vector<Raw>& out, bool partial_only) {
+  const size_t np = std::max(L_.np, 1);
   // the result is in mapped memory as soon as the publishing block has
   // written its completion word: spin on it (a stream synchronisation costs
   // a wake-up); the stream is queried now and then so errors still surface
@@ -704,6 +716,21 @@ void Model::eval_partial(const double* params, size_t n, int metric, int64_t* fx
     return;
   }
   for (int i = 0; i < 6; ++i) fx[i] = out[0].fx[i];
+}
+
+// Enqueue one evaluation without waiting (multi-process exchange): the event
+// pass also writes its exact digits to the device partial buffer, so a
+// collective can follow on the same stream.  The host records the call as
+// published; mapped results stay valid once the stream has drained.
+void Model::eval_launch(const double* params, size_t n, int metric, int* penalty) {
+  check_call(n, metric);
+  if (shards_.size() != 1) throw Error("bad-backend", "eval_launch needs a single-device model");
+  *penalty = 0;
+  if (!params_valid(params)) {
+    *penalty = 1;
+    return;
+  }
+  launch_graphs(params, 1);
 }
 
 uint64_t Model::clamp_count(int node) const {

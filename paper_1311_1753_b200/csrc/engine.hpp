@@ -82,6 +82,7 @@ struct Args {
   double total_content;
   uint32_t* done;
   int64_t* fxbins;
+  int64_t* dpart;
   int npin;
   int pad1;
   double pin[64];
@@ -112,6 +113,7 @@ struct Shard {
   uint32_t* d_done = nullptr;   // [finished-block counter, kMaxBatch completion sequences]
   uint32_t seq[kMaxBatch] = {};  // completion sequence the host expects next, per k
   int64_t* d_fxbins = nullptr;  // kMaxBatch x kFxBins x 16 binned digits of the event pass
+  int64_t* d_part = nullptr;    // kMaxBatch x 8: exact digits + error words of the last call (device)
   KRec* d_rec = nullptr;
   uint64_t* d_clamp = nullptr;  // [n_poly counted | n_poly discarded]
   Out* h_out = nullptr;         // mapped, kMaxBatch
@@ -149,6 +151,9 @@ class Model {
   void eval_batch(const double* params, size_t K, size_t n, int metric, double* out);
   // this process's shard partial (shard_count > 1)
   void eval_partial(const double* params, size_t n, int metric, int64_t* fx, int* penalty);
+  void eval_launch(const double* params, size_t n, int metric, int* penalty);
+  cudaStream_t stream() const { return shards_[0].stream; }
+  int64_t* partial_device() const { return shards_[0].d_part; }
   int64_t debug_trace(uint64_t* out, int64_t n);
   BenchResult bench(const double* params, size_t n, int metric, int steps, bool flush);
 
@@ -170,6 +175,8 @@ class Model {
   void check_call(size_t n, int metric) const;
   bool params_valid(const double* p) const;
   void run(const double* params, int K, std::vector<Raw>& out, bool partial_only);
+  void launch_graphs(const double* params, int K);
+  void wait_results(int K, std::vector<Raw>& out, bool partial_only);
   cudaGraphExec_t graph_for(Shard& s, int K);
   Args base_args(Shard& s, int K);
   void build_tasks(uint32_t grid_points);

@@ -899,6 +899,27 @@ class BoundModel:
             _raise(st)
         return out
 
+    def eval_launch(self, params, metric=MetricKind.NegLogLikelihood) -> bool:
+        """enqueue one evaluation on the model's stream, do not wait; True when
+        the parameters are invalid (penalty, nothing enqueued).  The exact
+        digits land in partial_device() for a stream-ordered collective."""
+        p = np.ascontiguousarray(params, dtype=np.float64).ravel()
+        pen = C.c_int32()
+        st = _abi.pf_status()
+        if lib.pf_eval_launch(self._h, p.ctypes.data, p.size, int(metric), C.byref(pen), C.byref(st)):
+            _raise(st)
+        self._evaluated()
+        return bool(pen.value)
+
+    def stream(self) -> int:
+        """the model's cudaStream_t (integer), e.g. for torch.cuda.ExternalStream"""
+        return int(lib.pf_model_stream(self._h))
+
+    def partial_device(self) -> int:
+        """device address of the K x 8 int64 record (6 exact digits, norm error
+        word, event-error flag) the last evaluation wrote"""
+        return int(lib.pf_model_partial_device(self._h))
+
     def eval_partial(self, params, metric=MetricKind.NegLogLikelihood):
         """(exact accumulator digits, penalty) of this process's shard"""
         p = np.ascontiguousarray(np.asarray(params, dtype=np.float64).ravel())

@@ -247,3 +247,30 @@ def test_c5_dalitz_vs_oracle():
         assert close(got, want), (got, want)
         norms, _, valid = o.norms()
         assert valid[0] and close(nodes[0].cached_norm(), norms[0])
+
+
+def test_device_partial_record_matches_host_partial():
+    """pf_eval_launch + the device record (what bench.py all-gathers over NCCL
+    on the model's stream) carry the same exact digits as pf_eval_partial"""
+    import torch
+    x, pdf = mixture()
+    ds = pf.UnbinnedDataSet.from_columns([x], 10.0 * oracle.mt64_uniform(21, 300_007))
+    bm = pf.BoundModel(pdf, ds)
+    p = [0.3, -0.8, 4.6, 1.3]
+    fx, pen = bm.eval_partial(p)
+    assert not pen
+
+    class _Rec:
+        def __init__(self, ptr):
+            self.__cuda_array_interface__ = {"shape": (8,), "typestr": "<i8", "data": (ptr, False), "version": 3}
+
+    rec = torch.as_tensor(_Rec(bm.partial_device()), device="cuda:0")
+    stream = torch.cuda.ExternalStream(bm.stream(), device="cuda:0")
+    p2 = [0.35, -0.7, 4.9, 1.1]
+    want, _ = bm.eval_partial(p2)
+    assert not bm.eval_launch(p)  # enqueued, not waited for
+    with torch.cuda.stream(stream):
+        got = rec.cpu().tolist()
+    assert got[:6] == fx and got[6] == 0xFFFFFFFF and got[7] == 0
+    assert bm.eval_launch([1.5, -0.7, 4.9, 1.1])  # invalid fraction: penalty, nothing enqueued
+    assert bm.eval_partial(p2)[0] == want  # the host path stays in step after launches
