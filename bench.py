@@ -278,6 +278,9 @@ def main():
     ap.add_argument("--events", type=int, default=0, help="events (bins) per GPU; 0: the config's size")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fit", action="store_true")
+    ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
+                    help="N > 1: p2p = exact records stored into every rank's buffer by the event pass "
+                         "over NVLink (CUDA IPC); nccl = device records all-gathered by NCCL on the model stream")
     ap.add_argument("--force-exchange", action="store_true",
                     help="run the multi-rank exchange path even with one rank (tests it on one GPU)")
     ap.add_argument("--diag-no-flush", action="store_true",
@@ -336,9 +339,16 @@ def main():
         part_d = torch.as_tensor(_DeviceRecord(bm.partial_device(), 8), device=f"cuda:{local}")
         model_stream = torch.cuda.ExternalStream(bm.stream(), device=f"cuda:{local}")
         recv_d = torch.empty(8 * world, dtype=torch.int64, device=f"cuda:{local}")
+        if args.exchange == "p2p":
+            # the peer-memory group: handles exchanged once, then every
+            # evaluation combines on the device and returns the global value
+            handles = [None] * world
+            dist.all_gather_object(handles, bm.group_handle())
+            bm.group_join(world, rank, handles)
+            dist.barrier()
 
     def step_value(p):
-        if not multi:
+        if not multi or args.exchange == "p2p":
             return bm.eval_metric(p, metric)
         if bm.eval_launch(p, metric):  # invalid parameters: the same on every rank
             return pf.kPenaltyValue
@@ -383,7 +393,7 @@ def main():
         ms_step = dt.item() / args.steps * 1e3
         ev_ms = None
         launches = pf.kernel_launches() - launches0
-        h2d, d2h = 8 * params.size, 64 * world
+        h2d, d2h = 8 * params.size, (88 if args.exchange == "p2p" else 64 * world)
 
     # e2e: the public API call (pf_eval_metric via BoundModel.eval_metric) with
     # host parameters in and the host scalar out, host wall clock, L2 flushed
@@ -418,7 +428,10 @@ def main():
                                f"params at the fit start",
                    f"{W.unit}_per_gpu": n_local, f"global_{W.unit}": n_total,
                    "l2": "flushed (256 MiB device write) before every timed step",
-                   "parallelism": f"dp{world}"},
+                   "parallelism": f"dp{world}",
+                   "exchange": (("p2p: exact digit records stored over NVLink into every rank's buffer by "
+                                 "the event pass (CUDA IPC), summed on device") if args.exchange == "p2p" else
+                                "nccl: device records all-gathered on the model stream") if multi else None},
         "evals_per_s": 1e3 / ms_step,
         "metric_value": value,
         "gpu_launches": int(launches),

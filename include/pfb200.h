@@ -225,6 +225,18 @@ PF_API int pf_eval_launch(pf_model* model, const double* params, size_t n_params
 PF_API uint64_t pf_model_stream(const pf_model* model);
 PF_API uint64_t pf_model_partial_device(const pf_model* model);
 
+/* Exchange group over peer memory (one process per GPU on one NVLink node):
+ * every rank exports its model's receive buffer (pf_group_handle: a 64-byte
+ * CUDA IPC handle), the handles are all-gathered by the caller (any
+ * transport), and every rank calls pf_group_join with all of them, then
+ * barriers.  From then on each evaluation's event pass stores its exact
+ * record into every rank's buffer over NVLink and sums the group's digits on
+ * the device: pf_eval_metric returns the GLOBAL metric on every rank, bitwise
+ * the single-device value, with no host collective.  All ranks must issue the
+ * same sequence of evaluations (as a fit does). */
+PF_API int pf_group_handle(pf_model* model, void* handle64, pf_status* status);
+PF_API int pf_group_join(pf_model* model, int32_t world, int32_t rank, const void* handles, pf_status* status);
+
 /* Exact combine of shard_count accumulators (shard_count x PF_FX_DIGITS) and
  * the correctly rounded metric: bitwise the single-device value. */
 PF_API double pf_combine_partials(const int64_t* partials_fx, int32_t shard_count);

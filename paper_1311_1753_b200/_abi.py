@@ -124,6 +124,8 @@ _SIGNATURES = {
                                  C.POINTER(pf_status)]),
     "pf_model_stream": (C.c_uint64, [C.c_void_p]),
     "pf_model_partial_device": (C.c_uint64, [C.c_void_p]),
+    "pf_group_handle": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(pf_status)]),
+    "pf_group_join": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.POINTER(pf_status)]),
 }
 
 

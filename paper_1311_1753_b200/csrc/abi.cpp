@@ -276,3 +276,17 @@ extern "C" PF_API int64_t pf_debug_trace(pf_model* model, uint64_t* out, int64_t
     return 0;
   }
 }
+
+int pf_group_handle(pf_model* model, void* handle64, pf_status* status) {
+  return guarded(status, [&] {
+    if (!model || !handle64) throw pfb::Error("bad-model", "null argument");
+    model->impl->group_handle(handle64);
+  });
+}
+
+int pf_group_join(pf_model* model, int32_t world, int32_t rank, const void* handles, pf_status* status) {
+  return guarded(status, [&] {
+    if (!model || !handles) throw pfb::Error("bad-model", "null argument");
+    model->impl->group_join(world, rank, handles);
+  });
+}

@@ -28,6 +28,8 @@ typedef unsigned int pf_u32;
 #define PF_E_OUT_OF_DOMAIN 3  // pdf.hpp:443-444
 #define PF_E_ZERO_INTEGRAL 4  // pdf.hpp:186-187
 #define PF_E_NONPOS_ENDPOINT 5 // ArgusPdf m0 <= 0
+#define PF_E_GROUP_TIMEOUT 6   // a peer's record never arrived (exchange group)
+#define PF_GROUP_MAX 16        // ranks of a peer-memory exchange group (engine.hpp kMaxGroup)
 
 struct pf_dd {
   double hi, lo;
@@ -90,6 +92,9 @@ struct pf_args {
   pf_u32* done;         // [finished-block counter (self-resetting), per-k completion sequence]
   long long* fxbins;    // K x PF_FX_BINS x 16: binned block digits (self-resetting)
   long long* dpart;     // K x 8 (device): exact digits, norm error, event-error flag of this call
+  long long** peers;    // peer-memory exchange group: every rank's receive buffer (null: none)
+  int gworld;           // ranks in the group
+  int grank;            // this rank
   int npin;             // K = 1: parameters passed inline (pin[0..npin))
   int pad1;
   double pin[PF_MAX_INLINE];

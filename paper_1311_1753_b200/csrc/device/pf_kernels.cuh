@@ -729,6 +729,74 @@ __device__ __forceinline__ pf_lacc pf_stage_terms(const pf_args& a, int k, pf_u6
 #endif
 }
 
+// Peer-memory exchange group (one process per GPU, NVLink): the finalizing
+// warp sends this rank's exact record (6 digits, norm error, error flag) into
+// slot [k][rank] of every rank's receive buffer (IPC-mapped, P2P stores,
+// system-scope release of a per-call sequence word), waits with acquire loads
+// until every rank's record for this call is in its own buffer, and replaces
+// the local digits by the sum over ranks: every rank then rounds and publishes
+// the same global metric.  Integer digits make the sum order-free, so the
+// value is bitwise the single-device one.  A peer missing for 5 s reports
+// PF_E_GROUP_TIMEOUT instead of hanging.
+__device__ __noinline__ void pf_group_exchange(const pf_args& a, int k, int lane, long long* d, pf_u32& normerr,
+                                                pf_u64& nonfinite, pf_u64& evterr) {
+  long long g[PF_FX_DIGITS];
+#pragma unroll
+  for (int i = 0; i < PF_FX_DIGITS; ++i) g[i] = __shfl_sync(0xffffffffu, d[i], 0);
+  const pf_u32 nerr = __shfl_sync(0xffffffffu, normerr, 0);
+  const int flag = __shfl_sync(0xffffffffu, (int)(nonfinite != ~0ull || evterr != ~0ull), 0);
+  const unsigned long long seq = (unsigned long long)(a.done[1 + k] + 1u);
+  if (lane < a.gworld) {  // send: lane q writes this rank's record into rank q's buffer
+    long long* dst = a.peers[lane] + ((pf_u64)k * PF_GROUP_MAX + a.grank) * 16;
+#pragma unroll
+    for (int i = 0; i < PF_FX_DIGITS; ++i) dst[i] = g[i];
+    dst[6] = (long long)nerr;
+    dst[7] = flag;
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(dst + 8), "l"(seq) : "memory");
+  }
+  long long h[PF_FX_DIGITS];
+#pragma unroll
+  for (int i = 0; i < PF_FX_DIGITS; ++i) h[i] = 0;
+  pf_u32 qerr = ~0u;
+  int qflag = 0, timeout = 0;
+  if (lane < a.gworld) {  // receive: lane q waits for rank q's record
+    const long long* src = a.peers[a.grank] + ((pf_u64)k * PF_GROUP_MAX + lane) * 16;
+    unsigned long long t0, t, got;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(got) : "l"(src + 8) : "memory");
+      if (got == seq) break;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > 5000000000ull) {
+        timeout = 1;
+        break;
+      }
+    }
+    if (!timeout) {
+#pragma unroll
+      for (int i = 0; i < PF_FX_DIGITS; ++i) h[i] = (long long)__ldcv((const unsigned long long*)(src + i));
+      qerr = (pf_u32)__ldcv((const unsigned long long*)(src + 6));
+      qflag = (int)__ldcv((const unsigned long long*)(src + 7));
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < PF_FX_DIGITS; ++i) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) h[i] += __shfl_down_sync(0xffffffffu, h[i], off);
+    d[i] = h[i];  // the group total (valid in lane 0)
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    qerr = min(qerr, __shfl_down_sync(0xffffffffu, qerr, off));
+    qflag |= __shfl_down_sync(0xffffffffu, qflag, off);
+    timeout |= __shfl_down_sync(0xffffffffu, timeout, off);
+  }
+  if (lane == 0) {
+    normerr = timeout ? ((0xffffffu << 8) | PF_E_GROUP_TIMEOUT) : min(normerr, qerr);
+    if (qflag && nonfinite == ~0ull && evterr == ~0ull) nonfinite = 0;  // a peer's term was non-finite
+  }
+}
+
 #ifndef PF_EVENT_MIN_BLOCKS
 #define PF_EVENT_MIN_BLOCKS 8
 #endif
@@ -898,6 +966,7 @@ extern "C" __global__ void __launch_bounds__(PF_EV_THREADS, PF_EVENT_MIN_BLOCKS)
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) d[i] += __shfl_down_sync(0xffffffffu, d[i], off);
       }
+      if (a.peers) pf_group_exchange(a, k, lane, d, normerr, nonfinite, evterr);
       pf_out* o = a.hout + k;
       if (lane == 0) {
         long long* dp = a.dpart + (pf_u64)k * 8;  // the device copy, for a stream-ordered collective

@@ -277,6 +277,8 @@ Model::Model(const pf_graph& g, const pf_data& d, uint32_t grid_points, const pf
     ck(cudaMalloc(&sh.d_partials, 16 * part_elems), "cudaMalloc partials");
     ck(cudaMalloc(&sh.d_done, sizeof(uint32_t) * (1 + kMaxBatch)), "cudaMalloc done");
     ck(cudaMemset(sh.d_done, 0, sizeof(uint32_t) * (1 + kMaxBatch)), "memset done");
+    ck(cudaMalloc(&sh.d_recv, sizeof(int64_t) * 16 * kMaxGroup * kMaxBatch), "cudaMalloc group receive");
+    ck(cudaMemset(sh.d_recv, 0, sizeof(int64_t) * 16 * kMaxGroup * kMaxBatch), "memset group receive");
     ck(cudaMalloc(&sh.d_part, sizeof(int64_t) * 8 * kMaxBatch), "cudaMalloc partial");
     ck(cudaMemset(sh.d_part, 0, sizeof(int64_t) * 8 * kMaxBatch), "memset partial");
     const size_t bins = sizeof(int64_t) * kMaxBatch * kFxBins * 16;
@@ -335,6 +337,9 @@ Model::~Model() {
     cudaFree(sh.d_done);
     cudaFree(sh.d_fxbins);
     cudaFree(sh.d_part);
+    for (void* p : sh.ipc_mapped) cudaIpcCloseMemHandle(p);
+    cudaFree(sh.d_peers);
+    cudaFree(sh.d_recv);
     cudaFree(sh.d_rec);
     cudaFree(sh.d_clamp);
     cudaFreeHost(sh.h_out);
@@ -434,6 +439,9 @@ Args Model::base_args(Shard& sh, int K) {
   a.done = sh.d_done;
   a.fxbins = sh.d_fxbins;
   a.dpart = sh.d_part;
+  a.peers = sh.d_peers;
+  a.gworld = group_world_;
+  a.grank = group_rank_;
   a.rec = sh.d_rec;
   a.total_content = total_content_;
   // norm-stage clamps are counted once (shard 0); the others discard them
@@ -618,6 +626,8 @@ void Model::wait_results(int K, std::vector<Raw>& out, bool partial_only) {
       ev_err = std::min(ev_err, sh.h_out[k].first_event_error);
       nonfinite = std::min(nonfinite, sh.h_out[k].first_nonfinite);
     }
+    if (norm_err != ~0u && (norm_err & 0xff) == 6)
+      throw Error("group-timeout", "a rank of the exchange group did not deliver its record within 5 s");
     if (norm_err != ~0u) {  // refresh_normalizations threw (engine.hpp:174-178)
       out[k].penalty = true;
       continue;
@@ -731,6 +741,60 @@ void Model::eval_launch(const double* params, size_t n, int metric, int* penalty
     return;
   }
   launch_graphs(params, 1);
+}
+
+// Peer-memory exchange group (pf_group_handle / pf_group_join): the
+// receive buffer of this model is exported as a CUDA IPC handle; joining maps
+// every other rank's buffer into this process, so the event pass of every
+// rank can store its exact record into all of them (pf_group_exchange).
+void Model::group_handle(void* out) const {
+  if (shards_.size() != 1) throw Error("bad-backend", "exchange groups need single-device models");
+  const Shard& sh = shards_[0];
+  ck(cudaSetDevice(sh.device), "cudaSetDevice");
+  cudaIpcMemHandle_t h;
+  ck(cudaIpcGetMemHandle(&h, sh.d_recv), "cudaIpcGetMemHandle");
+  std::memcpy(out, &h, sizeof h);
+}
+
+void Model::group_join(int world, int rank, const void* handles) {
+  if (shards_.size() != 1) throw Error("bad-backend", "exchange groups need single-device models");
+  if (world < 1 || world > kMaxGroup || rank < 0 || rank >= world)
+    throw Error("bad-backend", "exchange group: rank/world out of range");
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  Shard& sh = shards_[0];
+  ck(cudaSetDevice(sh.device), "cudaSetDevice");
+  ck(cudaStreamSynchronize(sh.stream), "cudaStreamSynchronize");
+  for (void* p : sh.ipc_mapped) cudaIpcCloseMemHandle(p);
+  sh.ipc_mapped.clear();
+  std::vector<int64_t*> ptrs(world);
+  for (int q = 0; q < world; ++q) {
+    if (q == rank) {
+      ptrs[q] = sh.d_recv;
+      continue;
+    }
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, static_cast<const char*>(handles) + 64 * q, 64);
+    void* p = nullptr;
+    ck(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+    sh.ipc_mapped.push_back(p);
+    ptrs[q] = static_cast<int64_t*>(p);
+  }
+  if (!sh.d_peers) ck(cudaMalloc(&sh.d_peers, sizeof(int64_t*) * kMaxGroup), "cudaMalloc peers");
+  ck(cudaMemcpy(sh.d_peers, ptrs.data(), sizeof(int64_t*) * world, cudaMemcpyHostToDevice), "peers H2D");
+  // every rank restarts its per-call sequence at 0 (callers barrier after
+  // joining, before the first evaluation)
+  ck(cudaMemset(sh.d_recv, 0, sizeof(int64_t) * 16 * kMaxGroup * kMaxBatch), "memset group receive");
+  ck(cudaMemset(sh.d_done, 0, sizeof(uint32_t) * (1 + kMaxBatch)), "memset done");
+  for (int k = 0; k < kMaxBatch; ++k) sh.seq[k] = 0;
+  std::memset(sh.h_out, 0, sizeof(Out) * kMaxBatch);
+  group_world_ = world;
+  group_rank_ = rank;
+  // the captured graphs carry the old arguments: rebuild on next use
+  for (auto& kv : sh.graphs) cudaGraphExecDestroy(kv.second);
+  sh.graphs.clear();
+  if (sh.graph1) cudaGraphDestroy(sh.graph1);
+  sh.graph1 = nullptr;
+  ck(cudaDeviceSynchronize(), "group join");
 }
 
 uint64_t Model::clamp_count(int node) const {

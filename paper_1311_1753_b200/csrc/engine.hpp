@@ -19,6 +19,7 @@ constexpr double kPenaltyValue = 1e300;  // engine.hpp:52
 constexpr int kMaxBatch = 16;            // parameter sets per launch
 constexpr int kEventWarps = 2;           // warps per event-pass block (PF_EV_WARPS)
 constexpr int kEventBlocksPerSM = 8;     // resident event blocks per SM (PF_EVENT_MIN_BLOCKS)
+constexpr int kMaxGroup = 16;              // PF_GROUP_MAX: ranks of a peer-memory exchange group
 constexpr int kFxBins = 32;               // PF_FX_BINS (x 16 int64 per bin)
 constexpr double kSmallNormWork = 65536; // raw evaluations: single-CTA setup path
 
@@ -83,6 +84,9 @@ struct Args {
   uint32_t* done;
   int64_t* fxbins;
   int64_t* dpart;
+  int64_t** peers;  // group exchange: every rank's receive buffer (null: no group)
+  int gworld;
+  int grank;
   int npin;
   int pad1;
   double pin[64];
@@ -114,6 +118,9 @@ struct Shard {
   uint32_t seq[kMaxBatch] = {};  // completion sequence the host expects next, per k
   int64_t* d_fxbins = nullptr;  // kMaxBatch x kFxBins x 16 binned digits of the event pass
   int64_t* d_part = nullptr;    // kMaxBatch x 8: exact digits + error words of the last call (device)
+  int64_t* d_recv = nullptr;    // group exchange: kMaxBatch x kMaxGroup x 16 receive slots
+  int64_t** d_peers = nullptr;  // group exchange: device array of every rank's d_recv (IPC-mapped)
+  std::vector<void*> ipc_mapped;
   KRec* d_rec = nullptr;
   uint64_t* d_clamp = nullptr;  // [n_poly counted | n_poly discarded]
   Out* h_out = nullptr;         // mapped, kMaxBatch
@@ -152,6 +159,8 @@ class Model {
   // this process's shard partial (shard_count > 1)
   void eval_partial(const double* params, size_t n, int metric, int64_t* fx, int* penalty);
   void eval_launch(const double* params, size_t n, int metric, int* penalty);
+  void group_handle(void* out) const;
+  void group_join(int world, int rank, const void* handles);
   cudaStream_t stream() const { return shards_[0].stream; }
   int64_t* partial_device() const { return shards_[0].d_part; }
   int64_t debug_trace(uint64_t* out, int64_t n);
@@ -193,6 +202,7 @@ class Model {
   uint64_t chunk_ = 0, n_chunks_total_ = 0;
   int shard_count_ = 1, shard_index_ = 0;
   bool small_norms_ = true;
+  int group_world_ = 1, group_rank_ = 0;  // peer-memory exchange group (group_join)
   std::vector<Shard> shards_;
   std::vector<Task> tasks_;  // host copy, all levels
   std::vector<int> level_first_task_, level_n_tasks_, level_blocks_;

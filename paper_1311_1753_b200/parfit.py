@@ -920,6 +920,24 @@ class BoundModel:
         word, event-error flag) the last evaluation wrote"""
         return int(lib.pf_model_partial_device(self._h))
 
+    def group_handle(self) -> bytes:
+        """64-byte CUDA IPC handle of this model's exchange receive buffer"""
+        buf = C.create_string_buffer(64)
+        st = _abi.pf_status()
+        if lib.pf_group_handle(self._h, buf, C.byref(st)):
+            _raise(st)
+        return buf.raw
+
+    def group_join(self, world: int, rank: int, handles) -> None:
+        """join a peer-memory exchange group (collective: every rank, then a
+        barrier); afterwards eval_metric returns the global metric on every rank"""
+        blob = b"".join(bytes(h) for h in handles)
+        if len(blob) != 64 * world:
+            raise Error("bad-backend", "group_join: need one 64-byte handle per rank")
+        st = _abi.pf_status()
+        if lib.pf_group_join(self._h, int(world), int(rank), blob, C.byref(st)):
+            _raise(st)
+
     def eval_partial(self, params, metric=MetricKind.NegLogLikelihood):
         """(exact accumulator digits, penalty) of this process's shard"""
         p = np.ascontiguousarray(np.asarray(params, dtype=np.float64).ravel())

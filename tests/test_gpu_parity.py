@@ -274,3 +274,20 @@ def test_device_partial_record_matches_host_partial():
     assert got[:6] == fx and got[6] == 0xFFFFFFFF and got[7] == 0
     assert bm.eval_launch([1.5, -0.7, 4.9, 1.1])  # invalid fraction: penalty, nothing enqueued
     assert bm.eval_partial(p2)[0] == want  # the host path stays in step after launches
+
+
+def test_exchange_group_of_one_is_bitwise_the_plain_value():
+    """the peer-memory exchange group (pf_group_join) with a single rank: the
+    event pass stores its record into its own buffer, waits for it and sums
+    the group's digits; the value must equal the ungrouped evaluation bit
+    for bit, and keep doing so over repeated and batched calls"""
+    x, pdf = mixture()
+    ds = pf.UnbinnedDataSet.from_columns([x], 10.0 * oracle.mt64_uniform(23, 200_003))
+    plain = pf.BoundModel(pdf, ds)
+    grouped = pf.BoundModel(pdf, ds)
+    grouped.group_join(1, 0, [grouped.group_handle()])
+    rng = np.random.default_rng(8)
+    P = [[rng.uniform(0, 1), rng.uniform(-2, 0), rng.uniform(3, 7), rng.uniform(0.5, 2)] for _ in range(6)]
+    for p in P:
+        assert grouped.eval_metric(p) == plain.eval_metric(p)
+    assert np.array_equal(grouped.eval_metric_batch(np.array(P)), plain.eval_metric_batch(np.array(P)))
