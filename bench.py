@@ -365,10 +365,16 @@ def main():
 
     sampler = ClockSampler(local) if rank == 0 else None
     launches0 = pf.kernel_launches()
-    if not multi:
+    if not multi or args.exchange == "p2p":
+        # device timing inside the library (CUDA events around each graph
+        # launch on the model stream, L2 flushed before each, outside the
+        # window); in an exchange group every rank runs it in lockstep, each
+        # launch including the peer-memory exchange, and the MAX is taken
         res = _abi.pf_bench_result()
         st = _abi.pf_status()
-        with sampler:
+        if multi:
+            dist.barrier()
+        with (sampler if sampler else _Null()):
             rc = pf.lib.pf_bench(bm._h, params.ctypes.data_as(C.POINTER(C.c_double)), params.size, W.metric,
                                  args.steps, 0 if args.diag_no_flush else 1, C.byref(res), C.byref(st))
         if rc:
@@ -378,22 +384,35 @@ def main():
         ev_ms = res.event_kernel_ms_mean
         value = res.metric
         h2d, d2h = res.h2d_bytes_per_step, res.d2h_bytes_per_step
+        if multi:
+            import torch
+            t = torch.tensor([ms_step, ev_ms], dtype=torch.float64, device=f"cuda:{local}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms_step, ev_ms = t.tolist()
     else:
+        # NCCL exchange: CUDA events on the model stream around every step
+        # (evaluation + collective + D2H), L2 flushed before each, MAX over ranks
         import torch
+        flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
+        total_ms = 0.0
         with (sampler if sampler else _Null()):
             dist.barrier()
-            torch.cuda.synchronize()
-            t = time.perf_counter()
-            for _ in range(args.steps):
+            for k in range(args.steps):
+                with torch.cuda.stream(model_stream):
+                    flush_buf.fill_(k & 0xff)
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(model_stream)
                 value = step_value(params)
-            torch.cuda.synchronize()
-            dist.barrier()
-            dt = torch.tensor([time.perf_counter() - t], dtype=torch.float64, device=f"cuda:{local}")
+                with torch.cuda.stream(model_stream):
+                    e1.record(model_stream)
+                e1.synchronize()
+                total_ms += e0.elapsed_time(e1)
+            dt = torch.tensor([total_ms / args.steps], dtype=torch.float64, device=f"cuda:{local}")
             dist.all_reduce(dt, op=dist.ReduceOp.MAX)
-        ms_step = dt.item() / args.steps * 1e3
+        ms_step = dt.item()
         ev_ms = None
         launches = pf.kernel_launches() - launches0
-        h2d, d2h = 8 * params.size, (88 if args.exchange == "p2p" else 64 * world)
+        h2d, d2h = 8 * params.size, 64 * world
 
     # e2e: the public API call (pf_eval_metric via BoundModel.eval_metric) with
     # host parameters in and the host scalar out, host wall clock, L2 flushed
