@@ -53,42 +53,6 @@ __device__ __forceinline__ void pf_finish_norm(double* S, pf_krec* r, int node, 
     atomicMin(&r->norm_error, ((pf_u32)node << 8) | PF_E_ZERO_INTEGRAL);
 }
 
-// Results of parameter set k into mapped host memory (one thread writes the
-// record; the calling threads copy the norms).
-__device__ void pf_publish(const pf_args& a, int k, int tid, int nt) {
-  const pf_krec* r = a.rec + k;
-  pf_out* o = a.hout + k;
-  if (tid == 0) {
-    long long fx[PF_FX_DIGITS];
-    for (int i = 0; i < PF_FX_DIGITS; ++i) fx[i] = (long long)__ldcg((const unsigned long long*)(r->fx + i));
-    long long* dp = a.dpart + (pf_u64)k * 8;
-    for (int i = 0; i < PF_FX_DIGITS; ++i) dp[i] = fx[i];
-    dp[6] = (long long)__ldcg(&r->norm_error);
-    dp[7] = (__ldcg(&r->first_nonfinite) != ~0ull || __ldcg(&r->first_event_error) != ~0ull) ? 1 : 0;
-    o->result = pf_fx_round(fx);
-    for (int i = 0; i < PF_FX_DIGITS; ++i) o->fx[i] = fx[i];
-    o->floor_count = __ldcg(&r->floor_count);
-    o->first_nonfinite = __ldcg(&r->first_nonfinite);
-    o->first_event_error = __ldcg(&r->first_event_error);
-    o->norm_error = __ldcg(&r->norm_error);
-  }
-  const double* S = a.S + (pf_u64)k * PF_SS;
-  for (int i = tid; i < 3 * a.n_nodes; i += nt) a.hnorms[(pf_u64)k * 3 * a.n_nodes + i] = S[i];
-#if PF_NPOLY > 0
-  if (k == a.K - 1)
-    for (int i = tid; i < PF_NPOLY; i += nt) a.hclamp[i] = __ldcg(a.clamp + i);
-#endif
-  // completion word: the host spins on it instead of synchronising the
-  // stream (every field above is visible to the host first)
-  __syncthreads();
-  if (tid == 0) {
-    const pf_u32 seq = a.done[1 + k] + 1u;
-    a.done[1 + k] = seq;
-    __threadfence_system();
-    *(volatile pf_u32*)&o->pad = seq;
-  }
-}
-
 // ---------------------------------------------------------------------------
 #define PF_SETUP_THREADS 512  // 128 registers: the level's 8 reductions interleave unspilled
 #ifndef PF_SETUP_CLUSTER
@@ -797,6 +761,79 @@ __device__ __noinline__ void pf_group_exchange(const pf_args& a, int k, int lane
   }
 }
 
+// Warp 0 finishes every parameter set of the call: lane b reads digit bin b
+// (one round trip, 32 bins), integer shuffles add the digits (and, in an
+// exchange group, pf_group_exchange sums the ranks), lane 0 rounds and writes
+// the record straight into mapped host memory; one system fence, then the
+// completion words.  Used by the event pass's last block and by the publish
+// kernel of a shard without events (whose bins are zero).
+__device__ void pf_finalize_warp0(const pf_args& a, int lane) {
+  static_assert(PF_FX_BINS == 32, "one bin per lane of warp 0");
+  {
+    for (int k = 0; k < a.K; ++k) {
+      const pf_krec* r = a.rec + k;
+      long long* bin = a.fxbins + ((pf_u64)k * PF_FX_BINS + lane) * PF_FX_BIN_STRIDE;
+      long long d[PF_FX_DIGITS];
+#pragma unroll
+      for (int i = 0; i < PF_FX_DIGITS; ++i) d[i] = (long long)__ldcg((const unsigned long long*)(bin + i));
+      pf_u64 floors = 0, nonfinite = 0, evterr = 0;
+      pf_u32 normerr = 0;
+      if (lane == 0) {
+        floors = __ldcg(&r->floor_count);
+        nonfinite = __ldcg(&r->first_nonfinite);
+        evterr = __ldcg(&r->first_event_error);
+        normerr = __ldcg(&r->norm_error);
+      }
+#pragma unroll
+      for (int i = 0; i < PF_FX_DIGITS; ++i) bin[i] = 0ll;  // self-resetting
+#pragma unroll
+      for (int i = 0; i < PF_FX_DIGITS; ++i) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) d[i] += __shfl_down_sync(0xffffffffu, d[i], off);
+      }
+      if (a.peers) pf_group_exchange(a, k, lane, d, normerr, nonfinite, evterr);
+      pf_out* o = a.hout + k;
+      if (lane == 0) {
+        long long* dp = a.dpart + (pf_u64)k * 8;  // the device copy, for a stream-ordered collective
+#pragma unroll
+        for (int i = 0; i < PF_FX_DIGITS; ++i) dp[i] = d[i];
+        dp[6] = (long long)normerr;
+        dp[7] = (nonfinite != ~0ull || evterr != ~0ull) ? 1 : 0;
+        o->result = pf_fx_round(d);
+#pragma unroll
+        for (int i = 0; i < PF_FX_DIGITS; ++i) o->fx[i] = d[i];
+        o->floor_count = floors;
+        o->first_nonfinite = nonfinite;
+        o->first_event_error = evterr;
+        o->norm_error = normerr;
+      }
+      const double* S = a.S + (pf_u64)k * PF_SS;
+      for (int i = lane; i < 3 * a.n_nodes; i += 32) a.hnorms[(pf_u64)k * 3 * a.n_nodes + i] = S[i];
+#if PF_NPOLY > 0
+      if (k == a.K - 1)
+        for (int i = lane; i < PF_NPOLY; i += 32) a.hclamp[i] = __ldcg(a.clamp + i);
+#endif
+    }
+    __syncwarp();
+    if (lane == 0) {
+#ifdef PF_PUBLISH_FENCE
+      __threadfence_system();  // every field above reaches the host first
+#endif
+      for (int k = 0; k < a.K; ++k) {
+        const pf_u32 seq = a.done[1 + k] + 1u;
+        a.done[1 + k] = seq;
+#ifdef PF_PUBLISH_FENCE
+        *(volatile pf_u32*)&a.hout[k].pad = seq;
+#else
+        // system-scope release: every field above (this warp's writes, made
+        // visible to lane 0 by the __syncwarp) reaches the host first
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(&a.hout[k].pad), "r"(seq) : "memory");
+#endif
+      }
+    }
+  }
+}
+
 #ifndef PF_EVENT_MIN_BLOCKS
 #define PF_EVENT_MIN_BLOCKS 8
 #endif
@@ -939,74 +976,7 @@ extern "C" __global__ void __launch_bounds__(PF_EV_THREADS, PF_EVENT_MIN_BLOCKS)
 #endif
   __threadfence();
   if (threadIdx.x == 0) *a.done = 0u;  // self-resetting (bench relaunches)
-  // warp 0 finishes every parameter set: lane b reads bin b (one round trip,
-  // 32 bins), integer shuffles add the digits, lane 0 rounds and writes the
-  // record straight into mapped host memory; one system fence, then the
-  // completion words
-  static_assert(PF_FX_BINS == 32, "one bin per lane of warp 0");
-  if (warp == 0) {
-    for (int k = 0; k < a.K; ++k) {
-      const pf_krec* r = a.rec + k;
-      long long* bin = a.fxbins + ((pf_u64)k * PF_FX_BINS + lane) * PF_FX_BIN_STRIDE;
-      long long d[PF_FX_DIGITS];
-#pragma unroll
-      for (int i = 0; i < PF_FX_DIGITS; ++i) d[i] = (long long)__ldcg((const unsigned long long*)(bin + i));
-      pf_u64 floors = 0, nonfinite = 0, evterr = 0;
-      pf_u32 normerr = 0;
-      if (lane == 0) {
-        floors = __ldcg(&r->floor_count);
-        nonfinite = __ldcg(&r->first_nonfinite);
-        evterr = __ldcg(&r->first_event_error);
-        normerr = __ldcg(&r->norm_error);
-      }
-#pragma unroll
-      for (int i = 0; i < PF_FX_DIGITS; ++i) bin[i] = 0ll;  // self-resetting
-#pragma unroll
-      for (int i = 0; i < PF_FX_DIGITS; ++i) {
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) d[i] += __shfl_down_sync(0xffffffffu, d[i], off);
-      }
-      if (a.peers) pf_group_exchange(a, k, lane, d, normerr, nonfinite, evterr);
-      pf_out* o = a.hout + k;
-      if (lane == 0) {
-        long long* dp = a.dpart + (pf_u64)k * 8;  // the device copy, for a stream-ordered collective
-#pragma unroll
-        for (int i = 0; i < PF_FX_DIGITS; ++i) dp[i] = d[i];
-        dp[6] = (long long)normerr;
-        dp[7] = (nonfinite != ~0ull || evterr != ~0ull) ? 1 : 0;
-        o->result = pf_fx_round(d);
-#pragma unroll
-        for (int i = 0; i < PF_FX_DIGITS; ++i) o->fx[i] = d[i];
-        o->floor_count = floors;
-        o->first_nonfinite = nonfinite;
-        o->first_event_error = evterr;
-        o->norm_error = normerr;
-      }
-      const double* S = a.S + (pf_u64)k * PF_SS;
-      for (int i = lane; i < 3 * a.n_nodes; i += 32) a.hnorms[(pf_u64)k * 3 * a.n_nodes + i] = S[i];
-#if PF_NPOLY > 0
-      if (k == a.K - 1)
-        for (int i = lane; i < PF_NPOLY; i += 32) a.hclamp[i] = __ldcg(a.clamp + i);
-#endif
-    }
-    __syncwarp();
-    if (lane == 0) {
-#ifdef PF_PUBLISH_FENCE
-      __threadfence_system();  // every field above reaches the host first
-#endif
-      for (int k = 0; k < a.K; ++k) {
-        const pf_u32 seq = a.done[1 + k] + 1u;
-        a.done[1 + k] = seq;
-#ifdef PF_PUBLISH_FENCE
-        *(volatile pf_u32*)&a.hout[k].pad = seq;
-#else
-        // system-scope release: every field above (this warp's writes, made
-        // visible to lane 0 by the __syncwarp) reaches the host first
-        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(&a.hout[k].pad), "r"(seq) : "memory");
-#endif
-      }
-    }
-  }
+  if (warp == 0) pf_finalize_warp0(a, lane);
 #ifdef PF_EVENT_TRACE
   if (threadIdx.x == 0) pf_trace_buf[4094 * 6 + 2] = pf_gtime();
 #endif
@@ -1016,5 +986,5 @@ extern "C" __global__ void __launch_bounds__(PF_EV_THREADS, PF_EVENT_MIN_BLOCKS)
 // publish only (a shard without events: the metric is 0)
 extern "C" __global__ void __launch_bounds__(PF_THREADS) pf_publish_kernel(const __grid_constant__ pf_args a) {
   pf_pdl_wait();
-  pf_publish(a, blockIdx.x, threadIdx.x, blockDim.x);
+  if (threadIdx.x < 32) pf_finalize_warp0(a, (int)threadIdx.x);
 }

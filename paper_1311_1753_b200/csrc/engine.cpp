@@ -504,7 +504,7 @@ cudaGraphExec_t Model::graph_for(Shard& sh, int K) {
       sh.event_grid = grid;
     }
   } else {
-    launch(sh.mod->publish, dim3(K), dim3(256), 0, sh.stream, e);
+    launch(sh.mod->publish, dim3(1), dim3(256), 0, sh.stream, e);
     ++kernels;
   }
   ck(cudaStreamEndCapture(sh.stream, &graph), "end capture");

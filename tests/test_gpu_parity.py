@@ -291,3 +291,14 @@ def test_exchange_group_of_one_is_bitwise_the_plain_value():
     for p in P:
         assert grouped.eval_metric(p) == plain.eval_metric(p)
     assert np.array_equal(grouped.eval_metric_batch(np.array(P)), plain.eval_metric_batch(np.array(P)))
+
+
+def test_exchange_group_with_an_empty_shard():
+    """a rank without events publishes through the publish kernel, which must
+    take part in the exchange too (here: a group of one, empty data)"""
+    x, pdf = mixture()
+    ds = pf.UnbinnedDataSet.from_columns([x], np.zeros(0))
+    bm = pf.BoundModel(pdf, ds)
+    bm.group_join(1, 0, [bm.group_handle()])
+    assert bm.eval_metric([0.4, -0.6, 5.0, 1.0]) == 0.0
+    assert bm.eval_metric([0.3, -0.5, 5.1, 1.1]) == 0.0
