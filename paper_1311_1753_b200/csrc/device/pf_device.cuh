@@ -272,11 +272,6 @@ struct pf_fxl {
   long long d[PF_FX_DIGITS];
 };
 
-__device__ __forceinline__ void pf_fxl_init(pf_fxl& A) {
-#pragma unroll
-  for (int i = 0; i < PF_FX_DIGITS; ++i) A.d[i] = 0;
-}
-
 __device__ __forceinline__ void pf_fxl_add(pf_fxl& A, double x) {
   const pf_u64 bits = (pf_u64)__double_as_longlong(x);
   const int be = (int)((bits >> 52) & 0x7ff);
@@ -366,101 +361,15 @@ __device__ __forceinline__ double pf_fx_round(const long long* acc) {
 }
 
 // ----------------------------------------------------------------------------
-// Reference reduction shape over chunk partials (engine.hpp:63-68): a
-// recursive pairwise tree that splits [lo, hi) at lo + (hi - lo) / 2.  An
-// empty range is 0 and x + 0 == x exactly, so padding the top of the tree
-// with empty subtrees leaves every value unchanged.
-//
-// Stack-free sequential evaluation: the tree over [lo, hi) is embedded in the
-// complete binary tree of depth s = ceil(log2 m); virtual leaf p (descend s
-// levels by the bits of p) is an element or empty, and a binary-counter merge
-// over the 2^s virtual leaves forms every node as left + right.
-__device__ pf_dd pf_pairwise_seq(const pf_dd* v, pf_u64 lo, pf_u64 hi) {
-  const pf_u64 m = hi > lo ? hi - lo : 0;
-  if (m == 0) return pf_dd_zero();
-  if (m == 1) return v[lo];
-  const int s = 64 - __clzll(m - 1);
-  pf_dd stk[40];
-  int top = 0;
-  for (pf_u64 p = 0; p < (1ull << s); ++p) {
-    pf_u64 a = lo, b = hi;
-    for (int lev = 0; lev < s; ++lev) {
-      const pf_u64 mid = a + (b - a) / 2;
-      if ((p >> (s - 1 - lev)) & 1)
-        a = mid;
-      else
-        b = mid;
-    }
-    pf_dd x = (b - a == 1) ? v[a] : pf_dd_zero();
-    for (pf_u64 q = p; q & 1; q >>= 1) x = pf_dd_add(stk[--top], x);
-    stk[top++] = x;
-  }
-  return stk[0];
-}
-
-// The same tree evaluated by one warp: lane l owns the subtree at depth 5
-// selected by the bits of l; sibling lanes combine as (2i, 2i+1) pairs.
-// All 32 lanes must call; the result is valid in lane 0.
-__device__ pf_dd pf_pairwise_warp(const pf_dd* v, pf_u64 n) {
-  const int lane = threadIdx.x & 31;
-  pf_u64 a = 0, b = n;
-  for (int lev = 0; lev < 5; ++lev) {
-    const pf_u64 mid = a + (b - a) / 2;
-    if ((lane >> (4 - lev)) & 1)
-      a = mid;
-    else
-      b = mid;
-  }
-  pf_dd x = pf_pairwise_seq(v, a, b);
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const pf_dd o = pf_shfl_down_dd(x, d);
-    if ((lane & (2 * d - 1)) == 0) x = pf_dd_add(x, o);
-  }
-  return x;
-}
-
-// Block-parallel evaluation of the same tree with nthreads = 2^d threads:
-// thread t owns the subtree at depth d selected by the bits of t (MSB
-// first); the top d levels are a complete binary tree combined in shared
-// memory.  Every node is still left + right of the reference's split, so the
-// value does not depend on d.
-__device__ pf_dd pf_pairwise_block(const pf_dd* v, pf_u64 n, pf_dd* sm, int nthreads) {
-  const int t = threadIdx.x;
-  int depth = 0;
-  while ((1 << depth) < nthreads) ++depth;
-  pf_u64 lo = 0, hi = n;
-#pragma unroll 1
-  for (int level = 0; level < depth; ++level) {
-    pf_u64 mid = lo + (hi - lo) / 2;
-    if ((t >> (depth - 1 - level)) & 1)
-      lo = mid;
-    else
-      hi = mid;
-  }
-  pf_dd own = pf_pairwise_seq(v, lo, hi);
-  __syncthreads();  // sm may alias data the block read before
-  sm[t] = own;
-  __syncthreads();
-  for (int width = nthreads >> 1; width >= 1; width >>= 1) {
-    pf_dd x;
-    if (t < width) x = pf_dd_add(sm[2 * t], sm[2 * t + 1]);
-    __syncthreads();
-    if (t < width) sm[t] = x;
-    __syncthreads();
-  }
-  return sm[0];
-}
-
-// ----------------------------------------------------------------------------
 // scalar math used by the node kernels
 //
 // pf_exp: table-driven exp.  x = (128 e + j) ln2/128 + r, |r| <= ln2/256;
 // exp(x) = 2^e * 2^(j/128) * (1 + expm1(r)) with 2^(j/128) = hi + lo from a
 // 128-entry shared-memory table and expm1(r) a degree-5 Taylor polynomial
 // (truncation r^6/720 < 6e-19).  One rounding dominates: error ~0.51 ulp,
-// 12 FP64 instructions instead of libdevice's ~17.  |x| >= 708, inf and NaN
-// take libdevice's exp.
+// 12 FP64 instructions instead of libdevice's ~17.  Branch-free range
+// handling: x is clamped to +-1100 (NaN kept) and 2^e applied in two exact
+// steps, so underflow to 0 and overflow to inf come out of the last multiply.
 #include "pf_exp_table.cuh"
 
 __shared__ double2 pf_exp_tab[128];

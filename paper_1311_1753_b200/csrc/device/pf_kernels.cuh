@@ -78,14 +78,6 @@ __device__ __forceinline__ double pf_dsmem_load(const double* p, unsigned rank) 
   asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(ra) : "memory");
   return v;
 }
-__device__ __forceinline__ pf_dd pf_dsmem_load_dd(const pf_dd* p, unsigned rank) {
-  unsigned ra;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(pf_smem_addr(p)), "r"(rank));
-  double hi, lo;
-  asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];" : "=d"(hi), "=d"(lo) : "r"(ra) : "memory");
-  return pf_dd{hi, lo};
-}
-
 // ---------------------------------------------------------------------------
 // setup: call records, pre stage and EVERY normalisation level for one
 // parameter set in one thread-block cluster of PF_SETUP_CLUSTER CTAs (small
