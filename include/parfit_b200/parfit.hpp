@@ -236,7 +236,7 @@ inline EventTable to_event_table(const BinnedDataSet& ds) {
 
 // ---- pdf.hpp ----------------------------------------------------------------
 enum class PdfKind { Exponential, Gaussian, BreitWigner, Polynomial, Product, Sum, Composite, Mapped,
-                     Convolution, Argus };
+                     Convolution, Argus, Dalitz };
 
 struct GridSpec {
   std::size_t points = 1024;
@@ -367,6 +367,44 @@ class ArgusPdf final : public PdfNode {
   }
 };
 
+// Time-integrated isobar model over the Dalitz plot of M -> 1 2 3 (not in the
+// reference; BASELINE config 5): |sum_r c_r BW_r|^2 inside the kinematic
+// boundary.  Observables m12^2, m13^2; per resonance (mass, width, Re c, Im c)
+// parameters, channel 12 / 13 / 23 and spin 0 / 1 (pfb200.h PF_DALITZ).
+struct DalitzResonance {
+  VariablePtr mass, width, re, im;
+  int channel = 12;
+  int spin = 1;
+};
+
+class DalitzPlotPdf final : public PdfNode {
+ public:
+  DalitzPlotPdf(std::string name, VariablePtr m12sq, VariablePtr m13sq, const std::vector<DalitzResonance>& res,
+                double M, double m1, double m2, double m3, double radius = 1.5)
+      : PdfNode(std::move(name), PdfKind::Dalitz) {
+    need_obs(name_, m12sq, "m12sq");
+    need_obs(name_, m13sq, "m13sq");
+    if (!(M > m1 + m2 + m3 && m1 >= 0 && m2 >= 0 && m3 >= 0 && radius >= 0))
+      throw Error("bad-kinematics", name_ + ": need M > m1 + m2 + m3, masses and R >= 0");
+    if (res.empty()) throw Error("bad-arity", name_ + ": need >= 1 resonance");
+    reals_ = {M, m1, m2, m3, radius};
+    for (const auto& r : res) {
+      need_par(name_, r.mass, "mass");
+      need_par(name_, r.width, "width");
+      need_par(name_, r.re, "Re c");
+      need_par(name_, r.im, "Im c");
+      if (r.channel != 12 && r.channel != 13 && r.channel != 23)
+        throw Error("bad-channel", name_ + ": channel must be 12, 13 or 23");
+      if (r.spin != 0 && r.spin != 1) throw Error("bad-spin", name_ + ": spin must be 0 or 1");
+      if (!(r.width->lower > 0)) throw Error("nonpositive-width", name_ + ": width limits must exclude 0");
+      params_.insert(params_.end(), {r.mass, r.width, r.re, r.im});
+      reals_.push_back(r.channel);
+      reals_.push_back(r.spin);
+    }
+    obs_ = {std::move(m12sq), std::move(m13sq)};
+  }
+};
+
 class ProdPdf final : public PdfNode {
  public:
   ProdPdf(std::string name, std::vector<PdfPtr> children) : PdfNode(std::move(name), PdfKind::Product) {
@@ -440,6 +478,11 @@ inline PdfPtr polynomial_pdf(std::string n, VariablePtr x, std::vector<VariableP
 }
 inline PdfPtr argus_pdf(std::string n, VariablePtr x, VariablePtr m0, VariablePtr c, VariablePtr p) {
   return std::make_shared<ArgusPdf>(std::move(n), std::move(x), std::move(m0), std::move(c), std::move(p));
+}
+inline PdfPtr dalitz_pdf(std::string n, VariablePtr m12sq, VariablePtr m13sq, const std::vector<DalitzResonance>& res,
+                         double M, double m1, double m2, double m3, double radius = 1.5) {
+  return std::make_shared<DalitzPlotPdf>(std::move(n), std::move(m12sq), std::move(m13sq), res, M, m1, m2, m3,
+                                         radius);
 }
 inline PdfPtr prod_pdf(std::string n, std::vector<PdfPtr> ch) {
   return std::make_shared<ProdPdf>(std::move(n), std::move(ch));

@@ -104,6 +104,39 @@ int main() {
     const double analytic = (std::exp(-2.4 * 5) - 1) / -2.4 * ((std::exp(-1.1 * 5) - 1) / -1.1);
     CHECK(std::abs(pdf->cached_norm() - analytic) / analytic <= 1e-6);
   }
+  {  // DalitzPlotPdf (BASELINE config 5; no reference counterpart): the C++
+     // front-end builds, binds and evaluates it; repeated calls agree bitwise
+    const double M = 1.86484, m1 = 0.13957, m2 = 0.13957, m3 = 0.13498;
+    auto s12 = new_observable("m12sq", (m1 + m2) * (m1 + m2), (M - m3) * (M - m3));
+    auto s13 = new_observable("m13sq", (m1 + m3) * (m1 + m3), (M - m2) * (M - m2));
+    auto res = [](const char* n, int ch, int spin, double m, double w, double re, double im) {
+      DalitzResonance r;
+      r.mass = new_parameter(std::string(n) + "_m", m, 0.001, m - 0.05, m + 0.05);
+      r.width = new_parameter(std::string(n) + "_w", w, 0.001, 0.01, 0.5);
+      r.re = new_parameter(std::string(n) + "_re", re, 0.01, -5, 5);
+      r.im = new_parameter(std::string(n) + "_im", im, 0.01, -5, 5);
+      r.channel = ch;
+      r.spin = spin;
+      return r;
+    };
+    auto pdf = dalitz_pdf("d0", s12, s13,
+                          {res("rhop", 13, 1, 0.7753, 0.1491, 1.0, 0.0), res("rhom", 23, 1, 0.7753, 0.1491, 0.65, 0.05),
+                           res("rho0", 12, 1, 0.7753, 0.1491, 0.53, 0.16)},
+                          M, m1, m2, m3);
+    UnbinnedDataSet ds({s12, s13});
+    std::mt19937_64 gen(5);
+    for (int i = 0; i < 4000; ++i) {  // points inside the plot near its centre
+      s12->value = 1.0 + 0.5 * uniform01(gen);
+      s13->value = 1.0 + 0.5 * uniform01(gen);
+      ds.add_event();
+    }
+    BoundModel bm(pdf, ds, GridSpec{256});
+    const auto p = bm.registry().export_values();
+    const double a = bm.eval_metric(p, MetricKind::NegLogLikelihood);
+    const double b = bm.eval_metric(p, MetricKind::NegLogLikelihood);
+    CHECK(std::isfinite(a) && a == b);
+    CHECK(pdf->cached_norm() > 0);
+  }
   std::printf("%s (%d failures)\n", failures ? "FAILED" : "PASSED", failures);
   return failures ? 1 : 0;
 }
