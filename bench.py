@@ -341,10 +341,23 @@ def main():
         recv_d = torch.empty(8 * world, dtype=torch.int64, device=f"cuda:{local}")
         if args.exchange == "p2p":
             # the peer-memory group: handles exchanged once, then every
-            # evaluation combines on the device and returns the global value
-            handles = [None] * world
-            dist.all_gather_object(handles, bm.group_handle())
-            bm.group_join(world, rank, handles)
+            # evaluation combines on the device and returns the global value.
+            # Where CUDA IPC / peer access is unavailable, every rank falls
+            # back to the NCCL record exchange together.
+            ok = torch.ones(1, dtype=torch.int32, device=f"cuda:{local}")
+            try:
+                handles = [None] * world
+                dist.all_gather_object(handles, bm.group_handle())
+                bm.group_join(world, rank, handles)
+            except Exception as e:  # noqa: BLE001 - reported, then the fallback
+                print(f"rank {rank}: peer-memory group unavailable ({e}); using NCCL", file=sys.stderr)
+                ok.zero_()
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            if ok.item() == 0:
+                args.exchange = "nccl"
+                bm = pf.BoundModel(pdf, ds, pf.GridSpec(W.grid), pf.Backend.gpus(1, local))  # ungrouped
+                part_d = torch.as_tensor(_DeviceRecord(bm.partial_device(), 8), device=f"cuda:{local}")
+                model_stream = torch.cuda.ExternalStream(bm.stream(), device=f"cuda:{local}")
             dist.barrier()
 
     def step_value(p):
