@@ -153,26 +153,26 @@ static double raw(omodel* m, int id, double* evt, const double* p);
  * pf_device.cuh pf_q2 / pf_dalitz_res / pf_dalitz_inside, same operation order
  * (this file is compiled with -ffp-contract=off; the GPU uses explicitly
  * rounded operations). */
-static double po_q2(double s, double ma, double mb) {
+static double po_q2(double s, double quarter, double ma, double mb) {
   const double sp = ma + mb, sm = ma - mb;
-  const double v = ((s - sp * sp) * (s - sm * sm)) / (4.0 * s);
+  const double v = ((s - sp * sp) * (s - sm * sm)) * quarter;
   return v > 0.0 ? v : 0.0;
 }
 
-static void po_dalitz_res(double s, double Z, double m, double m2, double G, double q0, double br0, double mi,
-                          double mj, double R2, int spin, double* re, double* im) {
-  const double q2 = po_q2(s, mi, mj);
-  const double q = sqrt(q2);
-  const double x = q / q0;
-  double bf2 = 1.0, ratio = x;
+static void po_dalitz_res(double s, double quarter, double rs, double Z, double m, double m2, double G, double iq0,
+                          double br0, double mi, double mj, double R2, int spin, double* re, double* im) {
+  const double q2 = po_q2(s, quarter, mi, mj);
+  const double x = sqrt(q2) * iq0;
+  double bf2 = 1.0, ratio = x, sbf = 1.0;
   if (spin == 1) {
     bf2 = br0 / (1.0 + R2 * q2);
     ratio = (x * x) * x;
+    sbf = sqrt(bf2);
   }
-  const double gs = ((G * ratio) * (m / sqrt(s))) * bf2;
+  const double gs = ((G * ratio) * (m * rs)) * bf2;
   const double a = m2 - s, b = m * gs;
   const double den = a * a + b * b;
-  const double f = (Z * sqrt(bf2)) / den;
+  const double f = (Z * sbf) / den;
   *re = f * a;
   *im = f * b;
 }
@@ -209,16 +209,17 @@ static double po_dalitz(const onode* o, const double* evt, const double* p) {
     const double sij = ch == 12 ? s12 : ch == 13 ? s13 : s23;
     const double sik = ch == 12 ? s13 : s12;
     const double sjk = ch == 12 ? s23 : ch == 13 ? s23 : s13;
+    const double qt = 0.25 / sij, rs = sqrt(4.0 * qt);  /* 1/(4 s), 1/sqrt(s) */
     double Z = 1.0;
     if (spin == 1) {
       const double a = M * M - ms[k] * ms[k];
       const double b = ms[i] * ms[i] - ms[j] * ms[j];
-      Z = (sjk - sik) + (a * b) / sij;
+      Z = (sjk - sik) + (4.0 * (a * b)) * qt;
     }
     const double m = p[o->p[4 * r]], mm2 = m * m, G = p[o->p[4 * r + 1]];
-    const double q20 = po_q2(mm2, ms[i], ms[j]);
+    const double q20 = po_q2(mm2, 0.25 / mm2, ms[i], ms[j]);
     double bre, bim;
-    po_dalitz_res(sij, Z, m, mm2, G, sqrt(q20), 1.0 + R2 * q20, ms[i], ms[j], R2, spin, &bre, &bim);
+    po_dalitz_res(sij, qt, rs, Z, m, mm2, G, 1.0 / sqrt(q20), 1.0 + R2 * q20, ms[i], ms[j], R2, spin, &bre, &bim);
     const double cre = p[o->p[4 * r + 2]], cim = p[o->p[4 * r + 3]];
     are = are + (cre * bre - cim * bim);
     aim = aim + (cre * bim + cim * bre);

@@ -473,32 +473,34 @@ struct pf_cplx {
   double re, im;
 };
 
-// q^2 of a two-body split of invariant mass^2 s into masses ma, mb
-__device__ __forceinline__ double pf_q2(double s, double ma, double mb) {
+// q^2 of a two-body split of invariant mass^2 s into masses ma, mb, given
+// quarter = 1 / (4 s) (shared by every resonance of the channel)
+__device__ __forceinline__ double pf_q2(double s, double quarter, double ma, double mb) {
   const double sp = __dadd_rn(ma, mb), sm = __dsub_rn(ma, mb);
-  const double v = __ddiv_rn(__dmul_rn(__dsub_rn(s, __dmul_rn(sp, sp)), __dsub_rn(s, __dmul_rn(sm, sm))),
-                             __dmul_rn(4.0, s));
+  const double v = __dmul_rn(__dmul_rn(__dsub_rn(s, __dmul_rn(sp, sp)), __dsub_rn(s, __dmul_rn(sm, sm))), quarter);
   return v > 0.0 ? v : 0.0;
 }
 
 // one resonance: Z B(q)/B(q0) / (m^2 - s - i m Gamma(s)),
 // Gamma(s) = G (q/q0)^(2J+1) (m / sqrt s) (B(q)/B(q0))^2, B_1(q)^2 = 1/(1 + R^2 q^2).
-// m2, q0, br0 = 1 + R^2 q0^2 are per-call constants (pf_stage_pre).
-__device__ __forceinline__ pf_cplx pf_dalitz_res(double s, double Z, double m, double m2, double G,
-                                                 double q0, double br0, double mi, double mj, double R2,
-                                                 int spin) {
-  const double q2 = pf_q2(s, mi, mj);
-  const double q = __dsqrt_rn(q2);
-  const double x = __ddiv_rn(q, q0);
-  double bf2 = 1.0, ratio = x;  // (B(q)/B(q0))^2, (q/q0)^(2J+1)
+// Channel terms: quarter = 1/(4 s), rs = 1/sqrt(s) = sqrt(4 quarter)/2 (one
+// division and one root per channel).  Per call (pf_stage_pre): m2 = m^2,
+// iq0 = 1/q0, br0 = 1 + R^2 q0^2.
+__device__ __forceinline__ pf_cplx pf_dalitz_res(double s, double quarter, double rs, double Z, double m,
+                                                 double m2, double G, double iq0, double br0, double mi,
+                                                 double mj, double R2, int spin) {
+  const double q2 = pf_q2(s, quarter, mi, mj);
+  const double x = __dmul_rn(__dsqrt_rn(q2), iq0);
+  double bf2 = 1.0, ratio = x, sbf = 1.0;  // (B(q)/B(q0))^2, (q/q0)^(2J+1), B(q)/B(q0)
   if (spin == 1) {
     bf2 = __ddiv_rn(br0, __dadd_rn(1.0, __dmul_rn(R2, q2)));
     ratio = __dmul_rn(__dmul_rn(x, x), x);
+    sbf = __dsqrt_rn(bf2);
   }
-  const double gs = __dmul_rn(__dmul_rn(__dmul_rn(G, ratio), __ddiv_rn(m, __dsqrt_rn(s))), bf2);
+  const double gs = __dmul_rn(__dmul_rn(__dmul_rn(G, ratio), __dmul_rn(m, rs)), bf2);
   const double a = __dsub_rn(m2, s), b = __dmul_rn(m, gs);
   const double den = __dadd_rn(__dmul_rn(a, a), __dmul_rn(b, b));
-  const double f = __ddiv_rn(__dmul_rn(Z, __dsqrt_rn(bf2)), den);
+  const double f = __ddiv_rn(__dmul_rn(Z, sbf), den);
   pf_cplx r;
   r.re = __dmul_rn(f, a);
   r.im = __dmul_rn(f, b);
