@@ -15,7 +15,12 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
+#include <fstream>
+#include <istream>
 #include <memory>
+#include <ostream>
+#include <sstream>
 #include <numeric>
 #include <span>
 #include <stdexcept>
@@ -141,6 +146,64 @@ class UnbinnedDataSet {
   std::vector<VariablePtr> obs_;
   std::vector<std::vector<double>> cols_;
 };
+
+// Text event store (dataset.hpp:184-245): '#' header naming the observables,
+// one event per line, %.17g.  Same header checks and error codes.
+inline void write_text(const UnbinnedDataSet& ds, std::ostream& out) {
+  out << '#';
+  for (const auto& o : ds.observables()) out << ' ' << o->name;
+  out << '\n';
+  char buf[40];
+  const auto& cols = ds.columns();
+  for (std::size_t e = 0; e < ds.n_events(); ++e) {
+    for (std::size_t c = 0; c < cols.size(); ++c) {
+      std::snprintf(buf, sizeof buf, "%.17g", cols[c][e]);
+      if (c) out << ' ';
+      out << buf;
+    }
+    out << '\n';
+  }
+}
+
+inline void write_text_file(const UnbinnedDataSet& ds, const std::string& path) {
+  std::ofstream f(path);
+  if (!f) throw Error("io-error", "cannot open '" + path + "' for writing");
+  write_text(ds, f);
+}
+
+inline UnbinnedDataSet read_text(std::istream& in, const std::vector<VariablePtr>& observables) {
+  std::string line;
+  if (!std::getline(in, line) || line.empty() || line[0] != '#') throw Error("bad-format", "missing '#' header line");
+  {
+    std::istringstream hs(line.substr(1));
+    std::string name;
+    std::size_t i = 0;
+    while (hs >> name) {
+      if (i >= observables.size() || observables[i]->name != name)
+        throw Error("bad-format", "header observable '" + name + "' does not match expected order");
+      ++i;
+    }
+    if (i != observables.size()) throw Error("bad-format", "header names fewer observables than expected");
+  }
+  UnbinnedDataSet ds(observables);
+  while (std::getline(in, line)) {
+    if (line.empty()) continue;
+    std::istringstream ls(line);
+    for (const auto& o : observables) {
+      double v;
+      if (!(ls >> v)) throw Error("bad-format", "short row in data file");
+      o->value = v;
+    }
+    ds.add_event();
+  }
+  return ds;
+}
+
+inline UnbinnedDataSet read_text_file(const std::string& path, const std::vector<VariablePtr>& observables) {
+  std::ifstream f(path);
+  if (!f) throw Error("io-error", "cannot open '" + path + "'");
+  return read_text(f, observables);
+}
 
 class BinnedDataSet {
  public:

@@ -189,6 +189,96 @@ class UnbinnedDataSet:
         return len(self._obs)
 
 
+# ---- event-store I/O --------------------------------------------------------
+def write_text(ds: UnbinnedDataSet, out) -> None:
+    """dataset.hpp:187-200: '#' header naming the observables, then one event
+    per line, columns in observable order, %.17g (round-trip precision)"""
+    cols = ds.columns()
+    out.write("#" + "".join(" " + o.name for o in ds.observables()) + "\n")
+    if cols.shape[1]:
+        np.savetxt(out, cols.T, fmt="%.17g", delimiter=" ")
+
+
+def write_text_file(ds: UnbinnedDataSet, path: str) -> None:
+    try:
+        fh = open(path, "w")
+    except OSError:
+        raise Error("io-error", f"cannot open '{path}' for writing") from None
+    with fh:
+        write_text(ds, fh)
+
+
+def read_text(inp, observables) -> UnbinnedDataSet:
+    """dataset.hpp:208-238 (same header check and error codes)"""
+    observables = list(observables)
+    header = inp.readline()
+    if not header or not header.startswith("#"):
+        raise Error("bad-format", "missing '#' header line")
+    names = header[1:].split()
+    for i, name in enumerate(names):
+        if i >= len(observables) or observables[i].name != name:
+            raise Error("bad-format", f"header observable '{name}' does not match expected order")
+    if len(names) != len(observables):
+        raise Error("bad-format", "header names fewer observables than expected")
+    rows = []
+    for line in inp:
+        parts = line.split()
+        if not parts:
+            continue
+        if len(parts) < len(observables):
+            raise Error("bad-format", "short row in data file")
+        try:
+            rows.append([float(v) for v in parts[:len(observables)]])
+        except ValueError:
+            raise Error("bad-format", "short row in data file") from None
+    cols = np.asarray(rows, dtype=np.float64).reshape(-1, len(observables)).T
+    return UnbinnedDataSet.from_columns(observables, cols)
+
+
+def read_text_file(path: str, observables) -> UnbinnedDataSet:
+    try:
+        fh = open(path)
+    except OSError:
+        raise Error("io-error", f"cannot open '{path}'") from None
+    with fh:
+        return read_text(fh, observables)
+
+
+_BIN_MAGIC = b"PFB200EV"
+
+
+def write_binary_file(ds: UnbinnedDataSet, path: str) -> None:
+    """binary event store for large fixtures: magic, n_obs, n_events (uint64),
+    the observable names (NUL-separated), then the column-major float64
+    EventTable as it lies in HBM"""
+    cols = np.ascontiguousarray(ds.columns(), dtype="<f8")
+    names = b"\0".join(o.name.encode() for o in ds.observables())
+    with open(path, "wb") as fh:
+        fh.write(_BIN_MAGIC)
+        fh.write(np.array([cols.shape[0], cols.shape[1], len(names)], dtype="<u8").tobytes())
+        fh.write(names)
+        fh.write(cols.tobytes())
+
+
+def read_binary_file(path: str, observables) -> UnbinnedDataSet:
+    observables = list(observables)
+    try:
+        fh = open(path, "rb")
+    except OSError:
+        raise Error("io-error", f"cannot open '{path}'") from None
+    with fh:
+        if fh.read(8) != _BIN_MAGIC:
+            raise Error("bad-format", "not a pfb200 binary event store")
+        n_obs, n_ev, nlen = (int(v) for v in np.frombuffer(fh.read(24), dtype="<u8"))
+        names = fh.read(nlen).split(b"\0") if nlen else []
+        if [n.decode() for n in names] != [o.name for o in observables] or n_obs != len(observables):
+            raise Error("bad-format", "observables do not match the file's")
+        cols = np.frombuffer(fh.read(8 * n_obs * n_ev), dtype="<f8")
+        if cols.size != n_obs * n_ev:
+            raise Error("bad-format", "truncated event store")
+    return UnbinnedDataSet.from_columns(observables, cols.reshape(n_obs, n_ev))
+
+
 class BinnedDataSet:
     """dataset.hpp:55-129: uniform bins, last upper edge inclusive."""
 

@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstdio>
 #include <random>
+#include <sstream>
 #include <vector>
 
 #include "parfit_b200/parfit.hpp"
@@ -136,6 +137,18 @@ int main() {
     const double b = bm.eval_metric(p, MetricKind::NegLogLikelihood);
     CHECK(std::isfinite(a) && a == b);
     CHECK(pdf->cached_norm() > 0);
+  }
+  {  // text event store round trip (dataset.hpp:184-245)
+    auto x = new_observable("x", 0, 10);
+    UnbinnedDataSet ds(x);
+    for (double v : {0.1, 1.0 / 3.0, 5e-324, 9.999999999999998}) {
+      x->value = v;
+      ds.add_event();
+    }
+    std::stringstream ss;
+    write_text(ds, ss);
+    const auto back = read_text(ss, {x});
+    CHECK(back.n_events() == 4 && back.columns()[0] == ds.columns()[0]);
   }
   std::printf("%s (%d failures)\n", failures ? "FAILED" : "PASSED", failures);
   return failures ? 1 : 0;

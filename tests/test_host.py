@@ -264,3 +264,58 @@ def test_markstein_division_is_correctly_rounded():
     assert f(2_000_000, 1, 5.20, 5.29, 5.28, 5.30) == 0       # the C3 range
     assert f(2_000_000, 2, 1e-3, 1e3, 1e-3, 1e3) == 0         # wide operands
     assert f(1_000_000, 3, 0.5, 2.0, 1.0 - 1e-15, 1.0 + 1e-15) == 0  # near-1 divisors
+
+
+def test_event_store_text_and_binary(tmp_path):
+    """dataset.hpp:184-245 text format (same header checks and error codes) and
+    the binary SoA store; both round-trip the event table bit for bit"""
+    x = pf.new_observable("x", 0, 10)
+    y = pf.new_observable("y", -1, 1)
+    rng = np.random.default_rng(4)
+    cols = np.stack([10 * rng.random(1000), rng.uniform(-1, 1, 1000)])
+    cols[0, :3] = [0.1, 1.0 / 3.0, 5e-324]
+    ds = pf.UnbinnedDataSet.from_columns([x, y], cols)
+    pf.write_text_file(ds, str(tmp_path / "ev.txt"))
+    back = pf.read_text_file(str(tmp_path / "ev.txt"), [x, y])
+    assert np.array_equal(back.columns(), cols)
+    pf.write_binary_file(ds, str(tmp_path / "ev.bin"))
+    assert np.array_equal(pf.read_binary_file(str(tmp_path / "ev.bin"), [x, y]).columns(), cols)
+    with pytest.raises(pf.Error, match="bad-format"):
+        pf.read_text_file(str(tmp_path / "ev.txt"), [y, x])  # header order
+    (tmp_path / "short.txt").write_text("# x y\n1 2\n3\n")
+    with pytest.raises(pf.Error, match="bad-format: short row"):
+        pf.read_text_file(str(tmp_path / "short.txt"), [x, y])
+    with pytest.raises(pf.Error, match="io-error"):
+        pf.read_text_file(str(tmp_path / "missing.txt"), [x, y])
+
+
+def test_event_store_text_matches_reference_writer(tmp_path):
+    """our writer's bytes equal the reference's write_text (dataset.hpp:187-200),
+    compiled from the reference headers (skipped where they are absent)"""
+    import shutil
+    import subprocess
+    inc = "/root/reference/proj/include"
+    if not os.path.isdir(inc) or not shutil.which("g++"):
+        pytest.skip("reference headers not present")
+    src = tmp_path / "w.cpp"
+    src.write_text(
+        '#include <iostream>\n#include "parfit/dataset.hpp"\n#include "parfit/variable.hpp"\n'
+        "using namespace parfit;\nint main() {\n"
+        '  auto x = new_observable("x", 0, 10); auto y = new_observable("y", -1, 1);\n'
+        "  UnbinnedDataSet ds({x, y});\n"
+        "  double vals[4][2] = {{0.1, -0.5}, {1.0 / 3.0, 0.25}, {5e-324, 1e300}, {9.999999999999998, -1}};\n"
+        "  for (auto& v : vals) { x->value = v[0]; y->value = v[1]; ds.add_event(); }\n"
+        "  write_text(ds, std::cout);\n}\n")
+    exe = tmp_path / "w"
+    r = subprocess.run(["g++", "-std=gnu++20", "-I", inc, str(src), "-o", str(exe)], capture_output=True, text=True)
+    if r.returncode:
+        pytest.skip("reference headers do not build here: " + r.stderr[:200])
+    ref = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout
+    x = pf.new_observable("x", 0, 10)
+    y = pf.new_observable("y", -1, 1)
+    ds = pf.UnbinnedDataSet.from_columns([x, y], np.array([[0.1, 1.0 / 3.0, 5e-324, 9.999999999999998],
+                                                         [-0.5, 0.25, 1e300, -1.0]]))
+    import io
+    buf = io.StringIO()
+    pf.write_text(ds, buf)
+    assert buf.getvalue() == ref
