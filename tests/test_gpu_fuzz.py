@@ -1,6 +1,6 @@
-"""Randomised parity: seeded random PDF trees over every node kind (Exp,
-Gauss, Breit-Wigner, Polynomial, Argus, AddPdf, ProdPdf, Composite, Mapped,
-Convolution) on one or two observables, evaluated through the C ABI and by
+"""Randomised parity: seeded random PDF trees (Exp, Gauss, Breit-Wigner,
+Polynomial, Argus, AddPdf, ProdPdf, Mapped, Convolution; Composite and
+Dalitz are covered by the golden and C5 tests) on one or two observables, evaluated through the C ABI and by
 the C oracle at several parameter points.  Exercises the code generator's
 combinations that the golden cases do not: folded AddPdf / ProdPdf norms
 at several levels, both log-domain forms and their fast paths, mixtures of
