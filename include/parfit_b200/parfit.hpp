@@ -7,9 +7,10 @@
 // and linking libpfb200.so.  Every metric evaluation runs on the GPU through
 // the C ABI (pfb200.h); this header only describes graphs and data sets.
 //
-// Not part of the drop-in (host-side utilities off the hot path, SURVEY §2
-// "OUT OF SCOPE"): PdfNode::raw/density for plotting, generate_events, the
-// JSON config front-end and the CLI.
+// generate_events runs on the GPU too (pf_generate_events; same ToyRng stream,
+// so a seed gives the reference's sample).  Not part of the drop-in (host-side
+// utilities off the hot path, SURVEY §2 "OUT OF SCOPE"): PdfNode::raw/density
+// for plotting, the JSON config front-end and the CLI.
 #ifndef PARFIT_B200_PARFIT_HPP
 #define PARFIT_B200_PARFIT_HPP
 
@@ -20,6 +21,7 @@
 #include <istream>
 #include <memory>
 #include <ostream>
+#include <random>
 #include <sstream>
 #include <numeric>
 #include <span>
@@ -143,6 +145,7 @@ class UnbinnedDataSet {
   const std::vector<std::vector<double>>& columns() const { return cols_; }
 
  private:
+  friend class detail_generate;
   std::vector<VariablePtr> obs_;
   std::vector<std::vector<double>> cols_;
 };
@@ -840,6 +843,52 @@ class BoundModel {
   std::vector<const PdfNode*> pre_;
   pf_model* model_ = nullptr;
 };
+
+// ---- generate.hpp --------------------------------------------------------
+// ToyRng (generate.hpp:19-27): the fixed uniform bit recipe
+// (mt19937_64() >> 11) * 2^-53, host side.
+class ToyRng {
+ public:
+  explicit ToyRng(std::uint64_t seed) : engine_(seed) {}
+  double uniform() { return 0x1.0p-53 * static_cast<double>(engine_() >> 11); }
+  double uniform(double lo, double hi) { return lo + (hi - lo) * uniform(); }
+
+ private:
+  std::mt19937_64 engine_;
+};
+
+class detail_generate {
+ public:
+  static void fill(UnbinnedDataSet& ds, const std::vector<double>& cols, std::size_t n) {
+    for (std::size_t c = 0; c < ds.obs_.size(); ++c)
+      ds.cols_[c].assign(cols.begin() + static_cast<std::ptrdiff_t>(c * n),
+                         cols.begin() + static_cast<std::ptrdiff_t>((c + 1) * n));
+  }
+};
+
+// generate_events (generate.hpp:33-86), accept-reject on the GPU with the
+// reference's envelope and ToyRng stream: the same seed gives the same
+// sample; box observables are left at the last accepted event.
+inline UnbinnedDataSet generate_events(const PdfPtr& pdf, const std::vector<VariablePtr>& observables,
+                                       std::size_t n_events, std::uint64_t seed, GridSpec grid = GridSpec{}) {
+  if (n_events < 1) throw Error("bad-arity", "generate_events: n_events >= 1");
+  UnbinnedDataSet ds(observables);
+  detail::GraphDesc g;
+  g.build(pdf, observables);
+  std::vector<int32_t> oi(observables.size());
+  for (std::size_t i = 0; i < observables.size(); ++i) oi[i] = g.vidx.at(observables[i].get());
+  std::vector<double> cols(observables.size() * n_events), last(observables.size());
+  pf_options opt{};
+  opt.n_devices = 1;
+  opt.shard_count = 1;
+  pf_status st{};
+  check(pf_generate_events(&g.graph, oi.data(), static_cast<int32_t>(oi.size()), n_events, seed,
+                           static_cast<uint32_t>(grid.points), &opt, cols.data(), last.data(), nullptr, &st),
+        st);
+  detail_generate::fill(ds, cols, n_events);
+  for (std::size_t i = 0; i < observables.size(); ++i) observables[i]->value = last[i];
+  return ds;
+}
 
 inline void PdfNode::refresh() const {
   if (owner_) owner_->refresh_norms();

@@ -316,6 +316,23 @@ PF_API int pf_fit(pf_model* model, int32_t metric, const pf_fit_config* config, 
            const int32_t* fixed, const double* lower, const double* upper, const double* step,
            pf_fit_result* result, pf_status* status);
 
+/* ---- event-store: toy generation ----------------------------------------- */
+
+/* generate_events(pdf, observables, n_events, seed, GridSpec) —
+ * generate.hpp:33-86 (ToyRng, :19-27).  The graph's parameters take their
+ * current values (pf_variable.value).  obs: the data set's observables
+ * (variable indices, column order).  out: column-major n_obs x n_events.
+ * last (optional, n_obs): the observables' values afterwards — the last
+ * accepted event for the PDF's box observables, their current value
+ * otherwise (the reference sets Variable::value per accepted event, :79).
+ * Runs on options->device (null: device 0).  gen_ms (optional): device time
+ * of the generation.  Errors: bad-arity (n_events < 1), the norm and raw
+ * errors of the PDF, envelope-failure (generate.hpp:65-76). */
+PF_API int pf_generate_events(const pf_graph* graph, const int32_t* obs, int32_t n_obs,
+                              uint64_t n_events, uint64_t seed, uint32_t grid_points,
+                              const pf_options* options, double* out, double* last, double* gen_ms,
+                              pf_status* status);
+
 /* Diagnostics: copies up to n of the model's %globaltimer stamps (built with
  * PFB200_DEFINES=PF_EVENT_TRACE; per event block: entry, prologue, PDL wait,
  * main loop, done, published; block 4095: setup entry/exit) into out.

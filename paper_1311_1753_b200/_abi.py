@@ -120,6 +120,9 @@ _SIGNATURES = {
     "pf_abi_version": (C.c_int32, []),
     "pf_kernel_launches": (C.c_uint64, []),
     "pf_debug_trace": (C.c_int64, [C.c_void_p, C.POINTER(C.c_uint64), C.c_int64]),
+    "pf_generate_events": (C.c_int, [C.POINTER(pf_graph), C.POINTER(C.c_int32), C.c_int32, C.c_uint64,
+                                     C.c_uint64, C.c_uint32, C.POINTER(pf_options), C.POINTER(C.c_double),
+                                     C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(pf_status)]),
     "pf_eval_launch": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int32, C.POINTER(C.c_int32),
                                  C.POINTER(pf_status)]),
     "pf_model_stream": (C.c_uint64, [C.c_void_p]),

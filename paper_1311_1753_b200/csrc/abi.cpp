@@ -5,6 +5,7 @@
 #include <cstring>
 #include <memory>
 #include <new>
+#include <vector>
 
 #include "codegen.hpp"
 #include "engine.hpp"
@@ -129,6 +130,50 @@ int pf_model_create(const pf_graph* graph, const pf_data* data, uint32_t grid_po
 }
 
 void pf_model_destroy(pf_model* model) { delete model; }
+
+int pf_generate_events(const pf_graph* graph, const int32_t* obs, int32_t n_obs, uint64_t n_events,
+                       uint64_t seed, uint32_t grid_points, const pf_options* options, double* out,
+                       double* last, double* gen_ms, pf_status* status) {
+  return guarded(status, [&] {
+    if (n_events < 1) throw pfb::Error("bad-arity", "generate_events: n_events >= 1");  // generate.hpp:37
+    if (!graph || !out || (n_obs > 0 && !obs)) throw pfb::Error("bad-graph", "null argument");
+    if (n_obs < 1) throw pfb::Error("empty-observables", "UnbinnedDataSet needs >= 1 observable");
+    pf_options opt;
+    std::memset(&opt, 0, sizeof opt);
+    if (options) opt.device = options->device;
+    opt.n_devices = 1;
+    opt.shard_count = 1;
+    // the evaluator is bound to one placeholder event at the observables'
+    // lower edges; generation uses its parameters, norms and constants
+    std::vector<double> row(n_obs);
+    for (int32_t c = 0; c < n_obs; ++c) {
+      if (obs[c] < 0 || obs[c] >= graph->n_variables) throw pfb::Error("bad-graph", "observable index");
+      row[c] = graph->variables[obs[c]].lower;
+    }
+    pf_data d;
+    std::memset(&d, 0, sizeof d);
+    d.n_obs = n_obs;
+    d.obs = obs;
+    d.n_events = 1;
+    d.values = row.data();
+    pfb::Model m(*graph, d, grid_points, opt, /*generator=*/true);
+    const auto& box = m.program().nodes[0].box;
+    std::vector<double> cols(box.size() * n_events);
+    m.generate(n_events, seed, grid_points, cols.data(), gen_ms);
+    for (int32_t c = 0; c < n_obs; ++c) {
+      int dim = -1;
+      for (size_t b = 0; b < box.size(); ++b)
+        if (box[b].var == obs[c]) dim = static_cast<int>(b);
+      double* dst = out + static_cast<size_t>(c) * n_events;
+      if (dim >= 0) {
+        std::memcpy(dst, cols.data() + static_cast<size_t>(dim) * n_events, sizeof(double) * n_events);
+      } else {
+        std::fill(dst, dst + n_events, graph->variables[obs[c]].value);
+      }
+      if (last) last[c] = dst[n_events - 1];
+    }
+  });
+}
 
 uint64_t pf_model_n_events(const pf_model* m) { return m ? m->impl->n_events() : 0; }
 int32_t pf_model_n_params(const pf_model* m) {

@@ -53,5 +53,6 @@ const char* device_header_source();
 const char* kernels_header_source();
 const char* counters_header_source();
 const char* exp_table_header_source();
+const char* generate_header_source();
 
 }  // namespace pfb

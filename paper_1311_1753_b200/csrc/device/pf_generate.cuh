@@ -1,0 +1,258 @@
+// pf_generate.cuh — toy generation on the GPU: generate_events
+// (generate.hpp:33-86) with the reference's ToyRng bit recipe.
+//
+// Included after pf_kernels.cuh when the module is built for a generator
+// (PF_GEN).  The reference draws candidates one at a time from ONE
+// std::mt19937_64 stream: per candidate, one uniform per box dimension (box
+// order) and one for the accept test.  Here:
+//   pf_gen_max_kernel      the envelope scan: max of raw/norm over the
+//                          midpoint grid (generate.hpp:47-63), order-free
+//   pf_mt_kernel           the mt19937_64 stream, one CTA: each 312-word
+//                          twist is two dependency-free halves of 156 words
+//                          (x[k+312] = x[k+156] ^ twist(x[k], x[k+1])), so a
+//                          round is two barriers over double-buffered state
+//   pf_gen_eval_kernel     every candidate of a batch in parallel: density,
+//                          accept flag, first envelope failure / raw error
+//   pf_gen_scan_kernel     exclusive scan of the per-block accept counts
+//   pf_gen_scatter_kernel  accepted candidates, in stream order, into the
+//                          SoA output columns (stops at the n-th acceptance)
+// Candidate arithmetic is the reference's, rounded explicitly (no FMA
+// contraction): x = lo + (hi - lo) * u and accept iff u * envelope < density.
+#pragma once
+
+#define PF_GEN_THREADS 256
+#define PF_GEN_PER_THREAD 8
+#define PF_GEN_SEGMENT (PF_GEN_THREADS * PF_GEN_PER_THREAD)  // candidates per block
+#define PF_MT_N 312
+#define PF_MT_M 156
+
+struct pf_gen_args {
+  const double* P;
+  const double* S;
+  const double* C;
+  int dims;             // root box dimensions
+  int pad0;
+  int cols[8];          // event column per box dimension (box order)
+  double lo[8];         // observable lower bound
+  double span[8];       // upper - lower (candidates)
+  double h[8];          // grid spacing (envelope scan)
+  pf_u64 points;        // grid points per dimension
+  pf_u64 total;         // grid points
+  double envelope;
+  const double* u;      // batch uniforms: (dims + 1) per candidate
+  pf_u64 n_cand;        // candidates in the batch
+  unsigned char* flags; // per candidate: 1 accepted
+  pf_u32* block_count;  // accepted per block
+  pf_u32* block_base;   // exclusive scan of block_count
+  pf_u64* rec;          // [0] max density bits, [1] first error key, [2] first failure,
+                        // [3] candidate of the last needed acceptance, [4] accepted in batch
+  double* fail_density; // density of a failing candidate (sparse)
+  double* out;          // SoA: dims columns, stride out_stride
+  pf_u64 out_stride;
+  pf_u64 out_base;      // events already generated
+  pf_u64 remaining;     // events still needed
+  pf_u64* mt;           // 312-word generator state
+  pf_u64 rounds;        // twists this launch
+};
+
+__device__ __forceinline__ double pf_gen_density(const pf_gen_args& g, double* ev, pf_ctx& cx) {
+  pf_cnt cnt;  // scratch: generation does not count clamps
+  pf_cnt_init(cnt);
+  return pf_eval_event(ev, g.P, g.S, g.C, cx, cnt);
+}
+
+// generate.hpp:47-63: max over the midpoint grid of raw / norm (last
+// dimension fastest; the max is order-free so any traversal gives the same).
+extern "C" __global__ void __launch_bounds__(PF_GEN_THREADS) pf_gen_max_kernel(const __grid_constant__ pf_gen_args g) {
+  pf_math_init();  // the exp table in shared memory
+  double best = 0.0;
+  pf_u64 err_key = ~0ull;
+  for (pf_u64 flat = (pf_u64)blockIdx.x * blockDim.x + threadIdx.x; flat < g.total;
+       flat += (pf_u64)gridDim.x * blockDim.x) {
+    double ev[PF_NCOLS];
+#pragma unroll
+    for (int q = 0; q < PF_NCOLS; ++q) ev[q] = 0.0;
+    pf_u64 rem = flat;
+    for (int d = g.dims - 1; d >= 0; --d) {
+      const pf_u64 k = rem % g.points;
+      rem /= g.points;
+      ev[g.cols[d]] = __dadd_rn(g.lo[d], __dmul_rn((double)k + 0.5, g.h[d]));
+    }
+    pf_ctx cx;
+    cx.err = 0;
+    const double v = pf_gen_density(g, ev, cx);
+    if (cx.err) {
+      const pf_u64 key = (flat << 24) | cx.err;
+      err_key = key < err_key ? key : err_key;
+    } else if (v > best) {
+      best = v;  // NaN never compares greater (generate.hpp:61)
+    }
+  }
+  pf_u64 bits = (pf_u64)__double_as_longlong(best);  // non-negative: integer order = value order
+  for (int o = 16; o > 0; o >>= 1) {
+    const pf_u64 ob = __shfl_xor_sync(0xffffffffu, bits, o);
+    const pf_u64 oe = __shfl_xor_sync(0xffffffffu, err_key, o);
+    bits = ob > bits ? ob : bits;
+    err_key = oe < err_key ? oe : err_key;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (bits) atomicMax(&g.rec[0], bits);
+    if (err_key != ~0ull) atomicMin(&g.rec[1], err_key);
+  }
+}
+
+__device__ __forceinline__ pf_u64 pf_mt_twist(pf_u64 a, pf_u64 b, pf_u64 c) {
+  const pf_u64 y = (a & 0xFFFFFFFF80000000ull) | (b & 0x7FFFFFFFull);
+  return c ^ (y >> 1) ^ ((y & 1ull) ? 0xB5026F5AA96619E9ull : 0ull);
+}
+
+__device__ __forceinline__ double pf_mt_uniform(pf_u64 y) {
+  y ^= (y >> 29) & 0x5555555555555555ull;
+  y ^= (y << 17) & 0x71D67FFFEDA60000ull;
+  y ^= (y << 37) & 0xFFF7EEE000000000ull;
+  y ^= y >> 43;
+  return (double)(y >> 11) * 0x1.0p-53;  // ToyRng::uniform (generate.hpp:22)
+}
+
+// `rounds` twists of the stream; the uniforms of round r go to u[312 r ..].
+extern "C" __global__ void __launch_bounds__(320) pf_mt_kernel(const __grid_constant__ pf_gen_args g) {
+  __shared__ pf_u64 buf[2][PF_MT_N];
+  const int t = threadIdx.x;
+  for (int i = t; i < PF_MT_N; i += blockDim.x) buf[0][i] = g.mt[i];
+  __syncthreads();
+  int cur = 0;
+  double* out = const_cast<double*>(g.u);
+  for (pf_u64 r = 0; r < g.rounds; ++r) {
+    const pf_u64* A = buf[cur];
+    pf_u64* B = buf[cur ^ 1];
+    if (t < PF_MT_M) B[t] = pf_mt_twist(A[t], A[t + 1], A[t + PF_MT_M]);
+    __syncthreads();
+    if (t < PF_MT_M) {
+      const int i = t + PF_MT_M;
+      B[i] = pf_mt_twist(A[i], i + 1 < PF_MT_N ? A[i + 1] : B[0], B[i - PF_MT_M]);
+    }
+    __syncthreads();
+    if (t < PF_MT_N) out[r * PF_MT_N + t] = pf_mt_uniform(B[t]);
+    cur ^= 1;
+  }
+  for (int i = t; i < PF_MT_N; i += blockDim.x) g.mt[i] = buf[cur][i];
+}
+
+// Candidate c of the batch: box coordinates from its first `dims` uniforms
+// (generate.hpp:70-71), then its density and accept test (:72-78).
+__device__ __forceinline__ void pf_gen_candidate(const pf_gen_args& g, pf_u64 c, double* ev) {
+#pragma unroll
+  for (int q = 0; q < PF_NCOLS; ++q) ev[q] = 0.0;
+  const double* uc = g.u + c * (pf_u64)(g.dims + 1);
+  for (int d = 0; d < g.dims; ++d) ev[g.cols[d]] = __dadd_rn(g.lo[d], __dmul_rn(g.span[d], uc[d]));
+}
+
+__device__ __forceinline__ pf_u32 pf_gen_block_sum(pf_u32 v, pf_u32* sh) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  pf_u32 s = 0;
+  for (int w = 0; w < PF_GEN_THREADS / 32; ++w) s += sh[w];
+  return s;
+}
+
+extern "C" __global__ void __launch_bounds__(PF_GEN_THREADS) pf_gen_eval_kernel(const __grid_constant__ pf_gen_args g) {
+  __shared__ pf_u32 sh[PF_GEN_THREADS / 32];
+  pf_math_init();  // the exp table in shared memory
+  const pf_u64 base = (pf_u64)blockIdx.x * PF_GEN_SEGMENT;
+  pf_u32 accepted = 0;
+  pf_u64 err_key = ~0ull, fail = ~0ull;
+  for (int j = 0; j < PF_GEN_PER_THREAD; ++j) {
+    const pf_u64 c = base + (pf_u64)j * PF_GEN_THREADS + threadIdx.x;
+    if (c >= g.n_cand) break;
+    double ev[PF_NCOLS];
+    pf_gen_candidate(g, c, ev);
+    pf_ctx cx;
+    cx.err = 0;
+    const double density = pf_gen_density(g, ev, cx);
+    const double ua = g.u[c * (pf_u64)(g.dims + 1) + g.dims];
+    unsigned char f = 0;
+    if (cx.err) {
+      const pf_u64 key = (c << 24) | cx.err;
+      err_key = key < err_key ? key : err_key;
+    } else if (density > g.envelope) {
+      g.fail_density[c] = density;
+      fail = c < fail ? c : fail;
+    } else if (__dmul_rn(ua, g.envelope) < density) {
+      f = 1;
+      ++accepted;
+    }
+    g.flags[c] = f;
+  }
+  if (err_key != ~0ull) atomicMin(&g.rec[1], err_key);
+  if (fail != ~0ull) atomicMin(&g.rec[2], fail);
+  const pf_u32 s = pf_gen_block_sum(accepted, sh);
+  if (threadIdx.x == 0) g.block_count[blockIdx.x] = s;
+}
+
+// one block: exclusive scan of the per-block counts, batch total into rec[4]
+extern "C" __global__ void __launch_bounds__(1024) pf_gen_scan_kernel(const __grid_constant__ pf_gen_args g) {
+  __shared__ pf_u64 warp_tot[32];
+  __shared__ pf_u64 carry;
+  const int n = (int)((g.n_cand + PF_GEN_SEGMENT - 1) / PF_GEN_SEGMENT);
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  if (t == 0) carry = 0;
+  __syncthreads();
+  for (int b0 = 0; b0 < n; b0 += 1024) {
+    const int b = b0 + t;
+    const pf_u64 v = b < n ? g.block_count[b] : 0u;
+    pf_u64 x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const pf_u64 y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[w] = x;
+    __syncthreads();
+    if (w == 0) {
+      pf_u64 s = warp_tot[lane];
+      for (int o = 1; o < 32; o <<= 1) {
+        const pf_u64 y = __shfl_up_sync(0xffffffffu, s, o);
+        if (lane >= o) s += y;
+      }
+      warp_tot[lane] = s;  // inclusive over warps
+    }
+    __syncthreads();
+    const pf_u64 excl = carry + (w ? warp_tot[w - 1] : 0ull) + x - v;
+    if (b < n) g.block_base[b] = (pf_u32)excl;
+    __syncthreads();
+    if (t == 0) carry += warp_tot[31];
+    __syncthreads();
+  }
+  if (t == 0) g.rec[4] = carry;
+}
+
+// accepted candidates in stream order -> out[col][out_base + rank], rank <
+// remaining; the candidate holding rank remaining - 1 is recorded (rec[3])
+extern "C" __global__ void __launch_bounds__(PF_GEN_THREADS) pf_gen_scatter_kernel(const __grid_constant__ pf_gen_args g) {
+  __shared__ pf_u32 wsum[PF_GEN_THREADS / 32];
+  const pf_u64 base = (pf_u64)blockIdx.x * PF_GEN_SEGMENT;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  pf_u64 rank0 = g.block_base[blockIdx.x];
+  if (rank0 >= g.remaining) return;
+  for (int j = 0; j < PF_GEN_PER_THREAD; ++j) {
+    const pf_u64 c = base + (pf_u64)j * PF_GEN_THREADS + threadIdx.x;
+    const bool acc = c < g.n_cand && g.flags[c];
+    const pf_u32 m = __ballot_sync(0xffffffffu, acc);
+    if (lane == 0) wsum[w] = __popc(m);
+    __syncthreads();
+    pf_u32 before = 0, all = 0;
+    for (int q = 0; q < PF_GEN_THREADS / 32; ++q) {
+      before += q < w ? wsum[q] : 0u;
+      all += wsum[q];
+    }
+    const pf_u64 rank = rank0 + before + __popc(m & ((1u << lane) - 1u));
+    if (acc && rank < g.remaining) {
+      const double* uc = g.u + c * (pf_u64)(g.dims + 1);
+      for (int d = 0; d < g.dims; ++d)
+        g.out[(pf_u64)d * g.out_stride + g.out_base + rank] = __dadd_rn(g.lo[d], __dmul_rn(g.span[d], uc[d]));
+      if (rank == g.remaining - 1) g.rec[3] = c;
+    }
+    rank0 += all;
+    __syncthreads();
+  }
+}

@@ -83,6 +83,13 @@ const Module* load_module(const Layout& L, int device) {
   ck(cudaLibraryGetKernel(&m->pre, m->lib, "pf_pre_kernel"), "get pf_pre_kernel");
   ck(cudaLibraryGetKernel(&m->norm, m->lib, "pf_norm_kernel"), "get pf_norm_kernel");
   ck(cudaLibraryGetKernel(&m->event, m->lib, "pf_event_kernel"), "get pf_event_kernel");
+  if (L.source.rfind("#define PF_GEN 1\n", 0) == 0) {
+    ck(cudaLibraryGetKernel(&m->gen_max, m->lib, "pf_gen_max_kernel"), "get pf_gen_max_kernel");
+    ck(cudaLibraryGetKernel(&m->gen_mt, m->lib, "pf_mt_kernel"), "get pf_mt_kernel");
+    ck(cudaLibraryGetKernel(&m->gen_eval, m->lib, "pf_gen_eval_kernel"), "get pf_gen_eval_kernel");
+    ck(cudaLibraryGetKernel(&m->gen_scan, m->lib, "pf_gen_scan_kernel"), "get pf_gen_scan_kernel");
+    ck(cudaLibraryGetKernel(&m->gen_scatter, m->lib, "pf_gen_scatter_kernel"), "get pf_gen_scatter_kernel");
+  }
   ck(cudaKernelSetAttributeForDevice(m->event, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(event_smem(L, kMaxBatch)), device),
      "event kernel smem attribute");
@@ -148,9 +155,10 @@ int sm_count(int device) {
 std::vector<char> compile_cubin(const Layout& L, std::string* log) {
   nvrtcProgram prog;
   const char* headers[] = {device_header_source(), kernels_header_source(), counters_header_source(),
-                           exp_table_header_source()};
-  const char* names[] = {"pf_device.cuh", "pf_kernels.cuh", "pf_counters.cuh", "pf_exp_table.cuh"};
-  ckr(nvrtcCreateProgram(&prog, L.source.c_str(), "pf_model.cu", 4, headers, names),
+                           exp_table_header_source(), generate_header_source()};
+  const char* names[] = {"pf_device.cuh", "pf_kernels.cuh", "pf_counters.cuh", "pf_exp_table.cuh",
+                         "pf_generate.cuh"};
+  ckr(nvrtcCreateProgram(&prog, L.source.c_str(), "pf_model.cu", 5, headers, names),
       "nvrtcCreateProgram");
   const char* opts[] = {"--gpu-architecture=sm_100a", "-lineinfo", "--std=c++17",
                         "--device-as-default-execution-space"};
@@ -174,14 +182,19 @@ std::vector<char> compile_cubin(const Layout& L, std::string* log) {
 
 // ---------------------------------------------------------------------------
 
-Model::Model(const pf_graph& g, const pf_data& d, uint32_t grid_points, const pf_options& opt) {
+Model::Model(const pf_graph& g, const pf_data& d, uint32_t grid_points, const pf_options& opt,
+             bool generator) {
   if (grid_points < 2) throw Error("bad-grid", "GridSpec needs >= 2 points");  // pdf.hpp:35-37
   if (!d.obs && d.n_obs > 0) throw Error("bad-data", "null observable list");
   binned_ = d.binned != 0;
   n_events_ = d.n_events;
   total_content_ = d.total_content;
   pg_ = finalize(g, d.n_obs, d.obs, binned_ ? 2 : 0);
-  L_ = generate(pg_, binned_);
+  L_ = pfb::generate(pg_, binned_);
+  if (generator) {
+    L_.source = "#define PF_GEN 1\n" + L_.source;
+    L_.structure_key = L_.source;
+  }
   if (binned_) L_.constants[L_.nc_total_slot] = total_content_;
   if (L_.data_range_base >= 0) {
     // (min, max) of every data column over ALL events, for the per-call
@@ -561,6 +574,12 @@ std::string Model::error_message(uint32_t code_node) const {
     case 5: return "nonpositive-endpoint: " + name;
   }
   return "device-error: code " + std::to_string(code);
+}
+
+void Model::throw_device_error(uint32_t code_node) const {
+  const std::string m = error_message(code_node);
+  const size_t colon = m.find(": ");
+  throw Error(m.substr(0, colon), colon == std::string::npos ? "" : m.substr(colon + 2));
 }
 
 void Model::run(const double* params, int K, std::vector<Raw>& out, bool partial_only) {

@@ -96,6 +96,9 @@ struct Module {
   cudaLibrary_t lib = nullptr;
   cudaKernel_t setup = nullptr, pre = nullptr, norm = nullptr, event = nullptr, final = nullptr,
                publish = nullptr;
+  // generator modules only (PF_GEN, pf_generate.cuh)
+  cudaKernel_t gen_max = nullptr, gen_mt = nullptr, gen_eval = nullptr, gen_scan = nullptr,
+               gen_scatter = nullptr;
 };
 
 // NVRTC compile of (library headers + generated source) for sm_100a.
@@ -147,7 +150,9 @@ int sm_count(int device);
 
 class Model {
  public:
-  Model(const pf_graph& g, const pf_data& d, uint32_t grid_points, const pf_options& opt);
+  // generator: also compile the toy-generation kernels (pf_generate.cuh)
+  Model(const pf_graph& g, const pf_data& d, uint32_t grid_points, const pf_options& opt,
+        bool generator = false);
   ~Model();
   Model(const Model&) = delete;
   Model& operator=(const Model&) = delete;
@@ -165,6 +170,9 @@ class Model {
   int64_t* partial_device() const { return shards_[0].d_part; }
   int64_t debug_trace(uint64_t* out, int64_t n);
   BenchResult bench(const double* params, size_t n, int metric, int steps, bool flush);
+  // generate_events (generate.hpp:33-86) at the parameters' current values:
+  // n events into out, column-major in root-box order (generate.cpp)
+  void generate(uint64_t n, uint64_t seed, uint32_t grid_points, double* out, double* gen_ms);
 
   const Program& program() const { return pg_; }
   const Layout& layout() const { return L_; }
@@ -190,6 +198,7 @@ class Model {
   Args base_args(Shard& s, int K);
   void build_tasks(uint32_t grid_points);
   std::string error_message(uint32_t code_node) const;
+  [[noreturn]] void throw_device_error(uint32_t code_node) const;
   size_t setup_smem_bytes() const {
     return sizeof(double) * (std::max(L_.np, 1) + std::max(L_.ss, 1));
   }

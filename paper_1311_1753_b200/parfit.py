@@ -279,6 +279,72 @@ def read_binary_file(path: str, observables) -> UnbinnedDataSet:
     return UnbinnedDataSet.from_columns(observables, cols.reshape(n_obs, n_ev))
 
 
+# ---- toy generation (generate.hpp) -------------------------------------------
+class ToyRng:
+    """generate.hpp:19-27: uniforms (mt19937_64() >> 11) * 2^-53 from a fixed
+    bit recipe, so identical seeds give identical samples everywhere.  Host
+    side (a plain mt19937_64); generate_events draws the same stream on the
+    GPU."""
+
+    _N, _M = 312, 156
+
+    def __init__(self, seed: int):
+        m = [0] * self._N
+        m[0] = seed & 0xFFFFFFFFFFFFFFFF
+        for i in range(1, self._N):
+            m[i] = (6364136223846793005 * (m[i - 1] ^ (m[i - 1] >> 62)) + i) & 0xFFFFFFFFFFFFFFFF
+        self._mt, self._i = m, self._N
+
+    def _twist(self):
+        m, N, M = self._mt, self._N, self._M
+        for i in range(N):
+            y = (m[i] & 0xFFFFFFFF80000000) | (m[(i + 1) % N] & 0x7FFFFFFF)
+            m[i] = m[(i + M) % N] ^ (y >> 1) ^ (0xB5026F5AA96619E9 if y & 1 else 0)
+        self._i = 0
+
+    def next_u64(self) -> int:
+        if self._i >= self._N:
+            self._twist()
+        y = self._mt[self._i]
+        self._i += 1
+        y ^= (y >> 29) & 0x5555555555555555
+        y ^= (y << 17) & 0x71D67FFFEDA60000
+        y ^= (y << 37) & 0xFFF7EEE000000000
+        y ^= y >> 43
+        return y & 0xFFFFFFFFFFFFFFFF
+
+    def uniform(self, lo: Optional[float] = None, hi: Optional[float] = None) -> float:
+        u = float(self.next_u64() >> 11) * 2.0 ** -53
+        return u if lo is None else lo + (hi - lo) * u
+
+
+def generate_events(pdf: "PdfNode", observables, n_events: int, seed: int,
+                    grid: Optional["GridSpec"] = None, device: int = 0) -> UnbinnedDataSet:
+    """generate_events (generate.hpp:33-86) on the GPU: the reference's
+    envelope, ToyRng stream and accept-reject order, so a seed gives the
+    reference's sample.  Sets each box observable's value to the last
+    accepted event, as the reference does."""
+    grid = grid or GridSpec()
+    observables = list(observables)
+    g = GraphDesc(pdf, observables)
+    idx = (C.c_int32 * max(len(observables), 1))(*[g.var_index(o) for o in observables])
+    n = int(n_events)
+    out = np.empty((len(observables), max(n, 1)))
+    last = (C.c_double * max(len(observables), 1))()
+    ms = C.c_double()
+    opt = _abi.pf_options(device, 1, 0, 1, 0)
+    st = _abi.pf_status()
+    if lib.pf_generate_events(C.byref(g.c_graph), idx, len(observables), max(n, 0), seed & 0xFFFFFFFFFFFFFFFF,
+                              grid.points, C.byref(opt), out.ctypes.data_as(C.POINTER(C.c_double)), last,
+                              C.byref(ms), C.byref(st)):
+        _raise(st)
+    for i, o in enumerate(observables):
+        o.value = last[i]
+    ds = UnbinnedDataSet.from_columns(observables, out)
+    ds.generation_ms = ms.value
+    return ds
+
+
 class BinnedDataSet:
     """dataset.hpp:55-129: uniform bins, last upper edge inclusive."""
 

@@ -150,6 +150,26 @@ int main() {
     const auto back = read_text(ss, {x});
     CHECK(back.n_events() == 4 && back.columns()[0] == ds.columns()[0]);
   }
+  {  // toy generation on the GPU, closed with a fit (test_generate.cpp:128-139)
+    auto x = new_observable("x", 0, 10);
+    auto a = new_parameter("a", -0.7, 0.2, -5, -0.05);
+    auto ds = generate_events(exp_pdf("gen", x, a), {x}, 20000, 314);
+    CHECK(ds.n_events() == 20000 && x->value == ds.columns()[0].back());
+    auto again = generate_events(exp_pdf("gen", x, a), {x}, 20000, 314);
+    CHECK(again.columns()[0] == ds.columns()[0]);
+    ToyRng rng(7);
+    bool in_unit = true;
+    for (int i = 0; i < 1000; ++i) {
+      const double u = rng.uniform();
+      in_unit = in_unit && u >= 0.0 && u < 1.0;
+    }
+    CHECK(in_unit);
+    auto afit = new_parameter("a", -0.3, 0.2, -5, -0.05);
+    BoundModel bm(exp_pdf("fit", x, afit), ds);
+    FitResult res = fit(bm, MetricKind::NegLogLikelihood, Backend::serial());
+    CHECK(res.converged() && std::abs(res.params[0] + 0.7) < 5 * res.uncertainties[0]);
+    std::printf("generated closure a = %.6f\n", res.params[0]);
+  }
   std::printf("%s (%d failures)\n", failures ? "FAILED" : "PASSED", failures);
   return failures ? 1 : 0;
 }

@@ -319,3 +319,21 @@ def test_event_store_text_matches_reference_writer(tmp_path):
     buf = io.StringIO()
     pf.write_text(ds, buf)
     assert buf.getvalue() == ref
+
+
+def test_toy_rng_is_the_reference_stream():
+    """ToyRng (generate.hpp:19-27) == the oracle's mt19937_64 recipe"""
+    import oracle
+    r = pf.ToyRng(7)
+    got = np.array([r.uniform() for _ in range(2000)])
+    assert np.array_equal(got, oracle.mt64_uniform(7, 2000))
+    r = pf.ToyRng(7)
+    assert all(-3.0 <= r.uniform(-3, 5) < 5.0 for _ in range(500))
+
+
+def test_generate_events_rejects_empty_request_without_a_gpu():
+    """test_generate.cpp:141-146: checked before any device work"""
+    x = pf.new_observable("x", 0, 10)
+    pdf = pf.exp_pdf("e", x, pf.new_parameter("a", -0.5, 0.1, -5, 5))
+    with pytest.raises(pf.Error, match="bad-arity: generate_events: n_events"):
+        pf.generate_events(pdf, [x], 0, 1)

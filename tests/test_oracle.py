@@ -138,3 +138,19 @@ def test_dalitz_restatement_vs_numpy():
     (a12, b12), (a13, b13) = W.box()
     corner = np.array([[b12 - 1e-6], [b13 - 1e-6]])  # far outside the plot
     assert o.density(p, corner)[0] == 0.0
+
+
+def test_generate_restatement_matches_reference_samples():
+    """the test-side restatement of generate_events (ToyRng stream + the C
+    oracle's densities, tests/golden/gen_cases.py) reproduces the reference's
+    samples bit for bit (tests/golden/generate.json, made by oracle/_ref)"""
+    import hashlib
+    import json
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden"))
+    from gen_cases import CASES, restated_generate
+    golden = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "generate.json")))
+    for name in ("exp_seed42", "uniform", "gauss", "bw", "mixture", "composite_mapped", "criterion2"):
+        pdf, obs, n, seed, grid = CASES[name](pf)
+        cols = restated_generate(pf, pdf, obs, n, seed, grid)
+        assert hashlib.sha256(np.ascontiguousarray(cols).tobytes()).hexdigest() == golden[name]["sha256"], name
