@@ -9,8 +9,9 @@
 //                          midpoint grid (generate.hpp:47-63), order-free
 //   pf_mt_kernel           the mt19937_64 stream, one CTA: each 312-word
 //                          twist is two dependency-free halves of 156 words
-//                          (x[k+312] = x[k+156] ^ twist(x[k], x[k+1])), so a
-//                          round is two barriers over double-buffered state
+//                          (x[k+312] = x[k+156] ^ twist(x[k], x[k+1])), two
+//                          barriers per twist; it overlaps the previous
+//                          batch's evaluation (second stream)
 //   pf_gen_eval_kernel     every candidate of a batch in parallel: density,
 //                          accept flag, first envelope failure / raw error
 //   pf_gen_scan_kernel     exclusive scan of the per-block accept counts
@@ -39,7 +40,7 @@ struct pf_gen_args {
   pf_u64 points;        // grid points per dimension
   pf_u64 total;         // grid points
   double envelope;
-  const double* u;      // batch uniforms: (dims + 1) per candidate
+  const double* u;      // batch stream words (raw mt19937_64 state words, as bits): dims + 1 per candidate
   pf_u64 n_cand;        // candidates in the batch
   unsigned char* flags; // per candidate: 1 accepted
   pf_u32* block_count;  // accepted per block
@@ -106,36 +107,62 @@ __device__ __forceinline__ pf_u64 pf_mt_twist(pf_u64 a, pf_u64 b, pf_u64 c) {
   return c ^ (y >> 1) ^ ((y & 1ull) ? 0xB5026F5AA96619E9ull : 0ull);
 }
 
+// tempering + ToyRng::uniform (generate.hpp:22), applied by the consumers
 __device__ __forceinline__ double pf_mt_uniform(pf_u64 y) {
   y ^= (y >> 29) & 0x5555555555555555ull;
   y ^= (y << 17) & 0x71D67FFFEDA60000ull;
   y ^= (y << 37) & 0xFFF7EEE000000000ull;
   y ^= y >> 43;
-  return (double)(y >> 11) * 0x1.0p-53;  // ToyRng::uniform (generate.hpp:22)
+  return (double)(y >> 11) * 0x1.0p-53;
 }
 
-// `rounds` twists of the stream; the uniforms of round r go to u[312 r ..].
-extern "C" __global__ void __launch_bounds__(320) pf_mt_kernel(const __grid_constant__ pf_gen_args g) {
-  __shared__ pf_u64 buf[2][PF_MT_N];
+// `rounds` twists of the stream; the raw (untempered) words of round r go to
+// u[312 r ..].  Thread t < 156 owns the state pair (x[t], x[t + 156]):
+//   x'[t]       = x[t + 156] ^ twist(x[t], x[t + 1])
+//   x'[t + 156] = x'[t] ^ twist(x[t + 156], x[t + 157])   (x[312] = x'[0])
+// so a round needs only the successor's old pair, exchanged through
+// double-buffered shared memory: two barriers per 312 words.  (A one-barrier
+// variant, where thread 155 recomputes x'[156] itself, and a one-warp
+// shuffle variant both measured slower: the twist's 64-bit integer chain,
+// not the barrier, sets the round time.)
+extern "C" __global__ void __launch_bounds__(160) pf_mt_kernel(const __grid_constant__ pf_gen_args g) {
+  __shared__ pf_u64 sa[2][PF_MT_M + 1], sb[2][PF_MT_M + 1];
   const int t = threadIdx.x;
-  for (int i = t; i < PF_MT_N; i += blockDim.x) buf[0][i] = g.mt[i];
+  const bool own = t < PF_MT_M;
+  pf_u64 a = own ? g.mt[t] : 0ull, b = own ? g.mt[t + PF_MT_M] : 0ull;
+  if (own) {
+    sa[0][t] = a;
+    sb[0][t] = b;
+  }
+  if (t == 0) sa[0][PF_MT_M] = b;  // x[156] is thread 0's second word
   __syncthreads();
+  pf_u64* out = (pf_u64*)g.u;
   int cur = 0;
-  double* out = const_cast<double*>(g.u);
   for (pf_u64 r = 0; r < g.rounds; ++r) {
-    const pf_u64* A = buf[cur];
-    pf_u64* B = buf[cur ^ 1];
-    if (t < PF_MT_M) B[t] = pf_mt_twist(A[t], A[t + 1], A[t + PF_MT_M]);
-    __syncthreads();
-    if (t < PF_MT_M) {
-      const int i = t + PF_MT_M;
-      B[i] = pf_mt_twist(A[i], i + 1 < PF_MT_N ? A[i + 1] : B[0], B[i - PF_MT_M]);
+    pf_u64* o = out + r * PF_MT_N;
+    pf_u64 n1 = 0ull;
+    if (own) {
+      n1 = pf_mt_twist(a, sa[cur][t + 1], b);
+      sa[cur ^ 1][t] = n1;
+      o[t] = n1;
     }
     __syncthreads();
-    if (t < PF_MT_N) out[r * PF_MT_N + t] = pf_mt_uniform(B[t]);
+    if (own) {
+      const pf_u64 bn = t + 1 < PF_MT_M ? sb[cur][t + 1] : sa[cur ^ 1][0];
+      const pf_u64 n2 = pf_mt_twist(b, bn, n1);
+      sb[cur ^ 1][t] = n2;
+      if (t == 0) sa[cur ^ 1][PF_MT_M] = n2;
+      o[t + PF_MT_M] = n2;
+      a = n1;
+      b = n2;
+    }
     cur ^= 1;
+    __syncthreads();
   }
-  for (int i = t; i < PF_MT_N; i += blockDim.x) g.mt[i] = buf[cur][i];
+  if (own) {
+    g.mt[t] = a;
+    g.mt[t + PF_MT_M] = b;
+  }
 }
 
 // Candidate c of the batch: box coordinates from its first `dims` uniforms
@@ -143,8 +170,9 @@ extern "C" __global__ void __launch_bounds__(320) pf_mt_kernel(const __grid_cons
 __device__ __forceinline__ void pf_gen_candidate(const pf_gen_args& g, pf_u64 c, double* ev) {
 #pragma unroll
   for (int q = 0; q < PF_NCOLS; ++q) ev[q] = 0.0;
-  const double* uc = g.u + c * (pf_u64)(g.dims + 1);
-  for (int d = 0; d < g.dims; ++d) ev[g.cols[d]] = __dadd_rn(g.lo[d], __dmul_rn(g.span[d], uc[d]));
+  const pf_u64* uc = (const pf_u64*)g.u + c * (pf_u64)(g.dims + 1);
+  for (int d = 0; d < g.dims; ++d)
+    ev[g.cols[d]] = __dadd_rn(g.lo[d], __dmul_rn(g.span[d], pf_mt_uniform(uc[d])));
 }
 
 __device__ __forceinline__ pf_u32 pf_gen_block_sum(pf_u32 v, pf_u32* sh) {
@@ -170,7 +198,7 @@ extern "C" __global__ void __launch_bounds__(PF_GEN_THREADS) pf_gen_eval_kernel(
     pf_ctx cx;
     cx.err = 0;
     const double density = pf_gen_density(g, ev, cx);
-    const double ua = g.u[c * (pf_u64)(g.dims + 1) + g.dims];
+    const double ua = pf_mt_uniform(((const pf_u64*)g.u)[c * (pf_u64)(g.dims + 1) + g.dims]);
     unsigned char f = 0;
     if (cx.err) {
       const pf_u64 key = (c << 24) | cx.err;
@@ -247,9 +275,10 @@ extern "C" __global__ void __launch_bounds__(PF_GEN_THREADS) pf_gen_scatter_kern
     }
     const pf_u64 rank = rank0 + before + __popc(m & ((1u << lane) - 1u));
     if (acc && rank < g.remaining) {
-      const double* uc = g.u + c * (pf_u64)(g.dims + 1);
+      const pf_u64* uc = (const pf_u64*)g.u + c * (pf_u64)(g.dims + 1);
       for (int d = 0; d < g.dims; ++d)
-        g.out[(pf_u64)d * g.out_stride + g.out_base + rank] = __dadd_rn(g.lo[d], __dmul_rn(g.span[d], uc[d]));
+        g.out[(pf_u64)d * g.out_stride + g.out_base + rank] =
+            __dadd_rn(g.lo[d], __dmul_rn(g.span[d], pf_mt_uniform(uc[d])));
       if (rank == g.remaining - 1) g.rec[3] = c;
     }
     rank0 += all;

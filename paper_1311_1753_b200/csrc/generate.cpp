@@ -16,6 +16,7 @@
 // probability ~1e-16 per candidate (tests/test_gpu_generate.py checks whole
 // samples against the reference).
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -85,6 +86,30 @@ struct Events {
   ~Events() {
     cudaEventDestroy(a);
     cudaEventDestroy(b);
+  }
+};
+
+// the generator's second stream: the mt19937_64 draw of the next batch
+struct Side {
+  cudaStream_t s = nullptr;
+  cudaEvent_t ready = nullptr, drawn[2] = {nullptr, nullptr}, used[2] = {nullptr, nullptr};
+  explicit Side(int device) {
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+    ck(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming), "event");
+    for (int i = 0; i < 2; ++i) {
+      ck(cudaEventCreateWithFlags(&drawn[i], cudaEventDisableTiming), "event");
+      ck(cudaEventCreateWithFlags(&used[i], cudaEventDisableTiming), "event");
+    }
+  }
+  ~Side() {  // a draw past the last batch may still be running
+    cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+    cudaEventDestroy(ready);
+    for (int i = 0; i < 2; ++i) {
+      cudaEventDestroy(drawn[i]);
+      cudaEventDestroy(used[i]);
+    }
   }
 };
 
@@ -162,10 +187,13 @@ void Model::generate(uint64_t n, uint64_t seed, uint32_t grid_points, double* ou
   const uint64_t per_twist = kMtN / std::gcd(kMtN, w);  // candidates per whole number of twists
   const uint64_t unit = std::lcm(kSegment, per_twist);
   const uint64_t full = unit * std::max<uint64_t>(1, (1ull << 22) / unit);
-  const uint64_t first = std::min(full, (std::max<uint64_t>(4 * n, 1) + unit - 1) / unit * unit);
+  auto round_up = [&](double c) {
+    const double u = std::ceil(std::max(c, 1.0) / static_cast<double>(unit));
+    return std::min(full, unit * static_cast<uint64_t>(std::min(u, 1e12)));
+  };
 
-  DevBuf b_u, b_flags, b_cnt, b_base, b_fail, b_out, b_mt;
-  g.u = b_u.alloc<double>(sizeof(double) * full * w);
+  DevBuf b_u[2], b_flags, b_cnt, b_base, b_fail, b_out, b_mt;
+  double* u[2] = {b_u[0].alloc<double>(sizeof(double) * full * w), b_u[1].alloc<double>(sizeof(double) * full * w)};
   g.flags = b_flags.alloc<unsigned char>(full);
   g.block_count = b_cnt.alloc<uint32_t>(sizeof(uint32_t) * (full / kSegment));
   g.block_base = b_base.alloc<uint32_t>(sizeof(uint32_t) * (full / kSegment));
@@ -177,23 +205,49 @@ void Model::generate(uint64_t n, uint64_t seed, uint32_t grid_points, double* ou
   mt_seed(seed, mt.data());
   ck(cudaMemcpyAsync(g.mt, mt.data(), sizeof(uint64_t) * kMtN, cudaMemcpyHostToDevice, s), "mt seed");
 
-  uint64_t done = 0;
-  bool first_batch = true;
-  while (done < n) {
-    const uint64_t B = first_batch ? first : full;
-    first_batch = false;
+  // the stream of batch b + 1 is drawn (second stream, one SM) while batch b
+  // is evaluated; batch sizes follow the measured acceptance so the stream
+  // drawn past the last needed candidate stays small
+  Side side(sh.device);
+  uint64_t size[2] = {round_up(4.0 * static_cast<double>(n)), 0};
+  ck(cudaEventRecord(side.ready, s), "event record");  // the seeded state
+  ck(cudaStreamWaitEvent(side.s, side.ready, 0), "stream wait");
+  auto draw = [&](int slot, uint64_t B) {
+    GenArgs m = g;
+    m.u = u[slot];
+    m.rounds = B * w / kMtN;
+    size[slot] = B;
+    launch_gen(sh.mod->gen_mt, 1, 160, side.s, m);
+    ck(cudaEventRecord(side.drawn[slot], side.s), "event record");
+  };
+  draw(0, size[0]);
+  uint64_t done = 0, cand_total = 0, acc_total = 0;
+  for (int b = 0;; ++b) {
+    const int slot = b & 1;
+    const uint64_t B = size[slot];
+    g.u = u[slot];
     g.n_cand = B;
-    g.rounds = B * w / kMtN;
     g.out_base = done;
     g.remaining = n - done;
     uint64_t r[8] = {0, ~0ull, ~0ull, ~0ull, 0, 0, 0, 0};
     ck(cudaMemcpyAsync(g.rec, r, sizeof r, cudaMemcpyHostToDevice, s), "rec reset");
+    ck(cudaStreamWaitEvent(s, side.drawn[slot], 0), "stream wait");
     const unsigned blocks = static_cast<unsigned>(B / kSegment);
-    launch_gen(sh.mod->gen_mt, 1, 320, s, g);
     launch_gen(sh.mod->gen_eval, blocks, 256, s, g);
     launch_gen(sh.mod->gen_scan, 1, 1024, s, g);
     launch_gen(sh.mod->gen_scatter, blocks, 256, s, g);
+    ck(cudaEventRecord(side.used[slot], s), "event record");
     ck(cudaMemcpyAsync(r, g.rec, sizeof r, cudaMemcpyDeviceToHost, s), "rec read");
+    bool prefetched = false;
+    if (acc_total > 0) {
+      const double rate = static_cast<double>(acc_total) / static_cast<double>(cand_total);
+      const double expect = static_cast<double>(done) + rate * static_cast<double>(B);
+      if (expect < static_cast<double>(n)) {
+        ck(cudaStreamWaitEvent(side.s, side.used[slot ^ 1], 0), "stream wait");
+        draw(slot ^ 1, round_up(1.2 * (static_cast<double>(n) - expect) / rate));
+        prefetched = true;
+      }
+    }
     ck(cudaStreamSynchronize(s), "generator batch");
     const uint64_t accepted = r[4];
     const uint64_t need = n - done;
@@ -210,6 +264,13 @@ void Model::generate(uint64_t n, uint64_t seed, uint32_t grid_points, double* ou
                   "density " + std::to_string(density) + " exceeds envelope " + std::to_string(envelope));
     }
     done += std::min(accepted, need);
+    cand_total += B;
+    acc_total += accepted;
+    if (done >= n) break;
+    if (!prefetched) {
+      const double rate = acc_total ? static_cast<double>(acc_total) / static_cast<double>(cand_total) : 0.0;
+      draw(slot ^ 1, rate > 0 ? round_up(1.2 * static_cast<double>(n - done) / rate) : full);
+    }
   }
   ck(cudaEventRecord(ev.b, s), "event record");
   ck(cudaMemcpyAsync(out, g.out, sizeof(double) * n * dims, cudaMemcpyDeviceToHost, s), "events D2H");
