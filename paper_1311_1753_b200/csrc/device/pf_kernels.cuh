@@ -555,9 +555,17 @@ __device__ __noinline__ pf_lacc pf_lane_fixup(const pf_args& a, int k, pf_u64 ba
 
 // this lane's accumulator over one staged sub-chunk for parameter set k.
 // FULL: all 32 * PF_EPT events are real (every sub-chunk but the data's last).
+#ifndef PF_LOG_FAST_SLOT
+struct pf_fk {};  // no fast path: nothing hoisted
+__device__ __forceinline__ pf_fk pf_fk_load(const double*, const double*, const double*) { return pf_fk{}; }
+#endif
+__device__ __forceinline__ pf_fk pf_fk_get(const pf_args& a, int k) {
+  return pf_fk_load(a.P + (pf_u64)k * PF_NP, a.S + (pf_u64)k * PF_SS, a.C);
+}
+
 template <bool FULL>
 __device__ __forceinline__ pf_lacc pf_stage_terms(const pf_args& a, int k, pf_u64 base, int lane,
-                                                const double* st, int n_valid) {
+                                                const double* st, int n_valid, const pf_fk& K) {
   const double* P = a.P + (pf_u64)k * PF_NP;
   const double* S = a.S + (pf_u64)k * PF_SS;
 #if !PF_BINNED && PF_LOGFORM
@@ -566,7 +574,7 @@ __device__ __forceinline__ pf_lacc pf_stage_terms(const pf_args& a, int k, pf_u6
 #ifdef PF_LOG_FAST_SLOT
   // per-call fast path: interval bounds over the data box (pf_stage_post)
   // proved every event's terms in range, so no per-event test at all
-  if (S[PF_LOG_FAST_SLOT] != 0.0) {
+  if (K.fast) {
 #pragma unroll pf_unroll
     for (int j = 0; j < PF_EPT; ++j) {
       const int i = 32 * j + lane;
@@ -576,7 +584,7 @@ __device__ __forceinline__ pf_lacc pf_stage_terms(const pf_args& a, int k, pf_u6
 #pragma unroll
       for (int q = 0; q < PF_NLOAD; ++q) ev[pf_load_col(q)] = st[q * PF_SUB + i];
       double Lv, fac[PF_NFAC_A];
-      pf_eval_event_log_fast(ev, P, S, Lv, fac);
+      pf_eval_event_log_fast(ev, K, Lv, fac);
       if (!FULL && i >= n_valid) {
         Lv = 0.0;
 #pragma unroll
@@ -876,6 +884,7 @@ extern "C" __global__ void __launch_bounds__(PF_EV_THREADS, PF_EVENT_MIN_BLOCKS)
 #ifdef PF_EVENT_TRACE
   const unsigned long long t_wait = pf_gtime();
 #endif
+  const pf_fk fk0 = pf_fk_get(a, 0);  // fast-path operands in registers for the whole pass
   for (int w = 0; w < W; ++w) {
     const int s = w % PF_NST;
     pf_mbar_wait(mybar + s, (unsigned)((w / PF_NST) & 1));
@@ -885,8 +894,9 @@ extern "C" __global__ void __launch_bounds__(PF_EV_THREADS, PF_EVENT_MIN_BLOCKS)
     const bool full = base + PF_SUB <= a.n_local;
     const int n_valid = full ? PF_SUB : (int)(a.n_local > base ? a.n_local - base : 0);
     for (int k = 0; k < a.K; ++k) {
-      pf_lacc t = full ? pf_stage_terms<true>(a, k, base, lane, my + s * PF_STAGE, n_valid)
-                       : pf_stage_terms<false>(a, k, base, lane, my + s * PF_STAGE, n_valid);
+      const pf_fk fk = k == 0 ? fk0 : pf_fk_get(a, k);
+      pf_lacc t = full ? pf_stage_terms<true>(a, k, base, lane, my + s * PF_STAGE, n_valid, fk)
+                       : pf_stage_terms<false>(a, k, base, lane, my + s * PF_STAGE, n_valid, fk);
       double* slot = accs + k * PF_LACC_N * PF_EV_THREADS + threadIdx.x;
       if (!first) {
         pf_lacc prev;
