@@ -467,8 +467,11 @@ __device__ __forceinline__ void pf_fac_accum(double& m, int& e, double v) {
 }
 
 // ----------------------------------------------------------------------------
-// DalitzPlotPdf pieces, every operation explicitly rounded (no contraction):
-// the C oracle (pf_oracle.c, -ffp-contract=off) evaluates the same sequence.
+// DalitzPlotPdf pieces.  The kinematic boundary and the per-call constants
+// are the C oracle's sequence (pf_oracle.c, -ffp-contract=off), explicitly
+// rounded, so no event changes side of the boundary; the per-event amplitude
+// uses pf_dalitz_res_fast (reciprocals by Newton-refined MUFU seeds), within
+// a few ulp of pf_dalitz_res.
 struct pf_cplx {
   double re, im;
 };
@@ -504,6 +507,53 @@ __device__ __forceinline__ pf_cplx pf_dalitz_res(double s, double quarter, doubl
   pf_cplx r;
   r.re = __dmul_rn(f, a);
   r.im = __dmul_rn(f, b);
+  return r;
+}
+
+// Fast reciprocal / reciprocal square root: the MUFU 64-bit seeds (about 22
+// bits) refined by two Newton steps each (quadratic convergence, ~1 ulp).
+// Used in the amplitude arithmetic, where the 1e-12 bar leaves room and the
+// IEEE sequences (__ddiv_rn / __dsqrt_rn, with their slow-path branches)
+// dominated the event cost; the kinematic boundary stays exact.
+__device__ __forceinline__ double pf_rcp_fast(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
+
+__device__ __forceinline__ double pf_rsqrt_fast(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x * y, y, 1.0);  // 1 - x y^2
+  y = fma(0.5 * y, e, y);
+  e = fma(-x * y, y, 1.0);
+  return fma(0.5 * y, e, y);
+}
+
+// pf_dalitz_res with the fast primitives: rsq = 1/sqrt(s) of the channel,
+// qt = 1/(4 s), sbr0 = sqrt(1 + R^2 q0^2) per call.  (B/B0)^2 and B/B0 share
+// one reciprocal square root of 1 + R^2 q^2.
+__device__ __forceinline__ pf_cplx pf_dalitz_res_fast(double s, double quarter, double rs, double Z, double m,
+                                                      double m2, double G, double iq0, double br0, double sbr0,
+                                                      double mi, double mj, double R2, int spin) {
+  const double q2 = pf_q2(s, quarter, mi, mj);
+  const double x = q2 > 0.0 ? q2 * pf_rsqrt_fast(q2) * iq0 : 0.0;
+  double bf2 = 1.0, ratio = x, sbf = 1.0;
+  if (spin == 1) {
+    const double ru = pf_rsqrt_fast(fma(R2, q2, 1.0));
+    bf2 = br0 * (ru * ru);
+    ratio = x * x * x;
+    sbf = sbr0 * ru;
+  }
+  const double gs = G * ratio * (m * rs) * bf2;
+  const double a = m2 - s, b = m * gs;
+  const double f = Z * sbf * pf_rcp_fast(fma(a, a, b * b));
+  pf_cplx r;
+  r.re = f * a;
+  r.im = f * b;
   return r;
 }
 
