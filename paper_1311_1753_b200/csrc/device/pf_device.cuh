@@ -574,6 +574,32 @@ __device__ __forceinline__ bool pf_dalitz_inside(double s12, double s13, double 
   return s13 >= lo && s13 <= hi;
 }
 
+// The same decision as pf_dalitz_inside, cheaply: the limits lo/hi of s13
+// come from the fast reciprocals.  With p >= 1e-3 E the fast and exact
+// sequences differ by < 5e-13 (e^2 + p^2), so a point farther than
+// 1e-11 (e^2 + p^2) from both limits is decided alike; closer points, and
+// p < 1e-3 E (ill-conditioned square root), take the exact sequence.
+__device__ __forceinline__ bool pf_dalitz_inside_fast(double s12, double s13, double M, double m1, double m2,
+                                                      double m3) {
+  const double a12 = __dadd_rn(m1, m2), b12 = __dsub_rn(M, m3);
+  if (!(s12 >= __dmul_rn(a12, a12) && s12 <= __dmul_rn(b12, b12))) return false;
+  const double ir = 0.5 * pf_rsqrt_fast(s12);  // 1 / (2 sqrt s12)
+  const double e1 = (s12 - m2 * m2 + m1 * m1) * ir;
+  const double e3 = (M * M - s12 - m3 * m3) * ir;
+  const double t1 = e1 * e1 - m1 * m1, t3 = e3 * e3 - m3 * m3;
+  // p = sqrt(t) is ill-conditioned where p << E (the edges of the s12 range):
+  // there the exact sequence decides
+  if (!(t1 >= 1e-6 * (e1 * e1)) || !(t3 >= 1e-6 * (e3 * e3))) return pf_dalitz_inside(s12, s13, M, m1, m2, m3);
+  const double p1 = t1 * pf_rsqrt_fast(t1), p3 = t3 * pf_rsqrt_fast(t3);
+  const double e = e1 + e3, pp = p1 + p3, pm = p1 - p3;
+  const double ee = e * e;
+  const double lo = ee - pp * pp, hi = ee - pm * pm;
+  const double tol = 1e-11 * (ee + pp * pp);
+  if (s13 < lo - tol || s13 > hi + tol) return false;
+  if (s13 > lo + tol && s13 < hi - tol) return true;
+  return pf_dalitz_inside(s12, s13, M, m1, m2, m3);
+}
+
 // ----------------------------------------------------------------------------
 // TMA bulk copies (cp.async.bulk, global -> shared) completed on mbarriers.
 __device__ __forceinline__ unsigned pf_smem_addr(const void* p) {

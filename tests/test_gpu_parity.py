@@ -302,3 +302,39 @@ def test_exchange_group_with_an_empty_shard():
     bm.group_join(1, 0, [bm.group_handle()])
     assert bm.eval_metric([0.4, -0.6, 5.0, 1.0]) == 0.0
     assert bm.eval_metric([0.3, -0.5, 5.1, 1.1]) == 0.0
+
+
+def test_c5_boundary_decisions_match_oracle():
+    """Events within a few ulp of the Dalitz-plot boundary (both s13 limits,
+    both s12 edges): the fast boundary test (pf_dalitz_inside_fast) decides
+    every one like the oracle's exactly rounded sequence — a single flip would
+    move the NLL by ~690 (floor) and the floor count."""
+    W = WORKLOADS["C5"]
+    obs, pdf = W.build(pf)
+    M, (m1, m2, m3) = W.M, W.ms
+    rng = np.random.default_rng(8)
+    (a12, b12), _ = W.box()
+    s12 = np.concatenate([rng.uniform(a12, b12, 3000),
+                          a12 * (1 + np.arange(1, 40) * 2.0 ** -52), b12 * (1 - np.arange(1, 40) * 2.0 ** -52)])
+    r12 = np.sqrt(s12)
+    e1 = (s12 - m2 * m2 + m1 * m1) / (2 * r12)
+    e3 = (M * M - s12 - m3 * m3) / (2 * r12)
+    p1 = np.sqrt(np.maximum(e1 * e1 - m1 * m1, 0))
+    p3 = np.sqrt(np.maximum(e3 * e3 - m3 * m3, 0))
+    lo = (e1 + e3) ** 2 - (p1 + p3) ** 2
+    hi = (e1 + e3) ** 2 - (p1 - p3) ** 2
+    pts = []
+    for k in range(-4, 5):
+        pts.append(np.stack([s12, lo * (1 + k * 2.0 ** -52)]))
+        pts.append(np.stack([s12, hi * (1 + k * 2.0 ** -52)]))
+    cols = np.concatenate(pts, axis=1)
+    _, (a13, b13) = W.box()
+    cols = cols[:, (cols[1] >= a13) & (cols[1] <= b13)]
+    ds = pf.UnbinnedDataSet.from_columns(obs, cols)
+    bm = pf.BoundModel(pdf, ds, pf.GridSpec(64))
+    o = oracle.Oracle(pdf, ds, 64)
+    pt = dict(W.start, **W.truth)
+    p = [pt[n.name] for n in bm.registry().parameters()]
+    got, want = bm.eval_metric(p), o.eval(p)
+    assert bm.log_floor_count() == o.floor_count() > 0
+    assert close(got, want), (got, want)
