@@ -247,6 +247,7 @@ extern "C" __global__ void __launch_bounds__(PF_THREADS) pf_pre_kernel(const __g
 // norm (large grids): one level, many blocks per midpoint sum; the last
 // block to arrive combines the block partials, applies Richardson and runs
 // the post stage.
+#define PF_NORM_RUN 32  // grid points per thread and run (>= 2-D boxes; engine.cpp build_tasks)
 extern "C" __global__ void __launch_bounds__(PF_THREADS) pf_norm_kernel(const __grid_constant__ pf_args a) {
   __shared__ pf_dd sm[PF_THREADS];
   __shared__ int s_last;
@@ -269,8 +270,14 @@ extern "C" __global__ void __launch_bounds__(PF_THREADS) pf_norm_kernel(const __
   pf_cnt cnt;
   pf_cnt_init(cnt);
   pf_dd acc = pf_dd_zero();
-  for (pf_u64 i = lo + threadIdx.x; i < hi; i += PF_THREADS)
-    acc = pf_dd_add_d(acc, pf_norm_point(T.node, i, T, P, S, a.C, cx, cnt));
+  if (T.dims >= 2 && T.per_block >= (pf_u64)PF_THREADS * PF_NORM_RUN) {
+    // runs of PF_NORM_RUN consecutive points per thread, walked row by row
+    for (pf_u64 i = lo + (pf_u64)threadIdx.x * PF_NORM_RUN; i < hi; i += (pf_u64)PF_THREADS * PF_NORM_RUN)
+      acc = pf_dd_add_d(acc, pf_norm_run(T.node, i, (int)min((pf_u64)PF_NORM_RUN, hi - i), T, P, S, a.C, cx, cnt));
+  } else {
+    for (pf_u64 i = lo + threadIdx.x; i < hi; i += PF_THREADS)
+      acc = pf_dd_add_d(acc, pf_norm_point(T.node, i, T, P, S, a.C, cx, cnt));
+  }
   {
     pf_dd s = pf_block_reduce(acc, sm);
     if (threadIdx.x == 0) part[blockIdx.x] = s;

@@ -403,8 +403,11 @@ void Model::build_tasks(uint32_t grid_points) {
         t.vol = vol;
         if (pairs) total *= static_cast<uint64_t>(nd.q);
         t.points = total;
-        // about 4096 raw evaluations per block, at most 4096 blocks per task
+        // about 4096 raw evaluations per block, at most 4096 blocks per task;
+        // boxes of >= 2 dimensions: runs of 32 points per thread
+        // (PF_NORM_RUN, walked row by row) for all 256 threads of a block
         uint64_t per = static_cast<uint64_t>(std::max(1.0, std::floor(4096.0 / cost)));
+        if (dims >= 2 && !pairs) per = std::max<uint64_t>(per, 256ull * 32ull);
         uint64_t nb = (total + per - 1) / per;
         if (nb > 4096) {
           nb = 4096;
