@@ -158,19 +158,18 @@ int pf_generate_events(const pf_graph* graph, const int32_t* obs, int32_t n_obs,
     d.values = row.data();
     pfb::Model m(*graph, d, grid_points, opt, /*generator=*/true);
     const auto& box = m.program().nodes[0].box;
-    std::vector<double> cols(box.size() * n_events);
-    m.generate(n_events, seed, grid_points, cols.data(), gen_ms);
-    for (int32_t c = 0; c < n_obs; ++c) {
-      int dim = -1;
+    std::vector<double*> dst(box.size(), nullptr);  // box dimension -> the caller's column
+    for (int32_t c = 0; c < n_obs; ++c)
       for (size_t b = 0; b < box.size(); ++b)
-        if (box[b].var == obs[c]) dim = static_cast<int>(b);
-      double* dst = out + static_cast<size_t>(c) * n_events;
-      if (dim >= 0) {
-        std::memcpy(dst, cols.data() + static_cast<size_t>(dim) * n_events, sizeof(double) * n_events);
-      } else {
-        std::fill(dst, dst + n_events, graph->variables[obs[c]].value);
-      }
-      if (last) last[c] = dst[n_events - 1];
+        if (box[b].var == obs[c]) dst[b] = out + static_cast<size_t>(c) * n_events;
+    m.generate(n_events, seed, grid_points, dst.data(), gen_ms);
+    for (int32_t c = 0; c < n_obs; ++c) {
+      double* col = out + static_cast<size_t>(c) * n_events;
+      bool in_box = false;
+      for (size_t b = 0; b < box.size(); ++b) in_box |= box[b].var == obs[c];
+      // an observable outside the PDF's box keeps its current value (add_event snapshot)
+      if (!in_box) std::fill(col, col + n_events, graph->variables[obs[c]].value);
+      if (last) last[c] = col[n_events - 1];
     }
   });
 }

@@ -171,8 +171,9 @@ class Model {
   int64_t debug_trace(uint64_t* out, int64_t n);
   BenchResult bench(const double* params, size_t n, int metric, int steps, bool flush);
   // generate_events (generate.hpp:33-86) at the parameters' current values:
-  // n events into out, column-major in root-box order (generate.cpp)
-  void generate(uint64_t n, uint64_t seed, uint32_t grid_points, double* out, double* gen_ms);
+  // n events; box dimension d is written to out[d] (host, n doubles; null:
+  // not copied) (generate.cpp)
+  void generate(uint64_t n, uint64_t seed, uint32_t grid_points, double* const* out, double* gen_ms);
 
   const Program& program() const { return pg_; }
   const Layout& layout() const { return L_; }

@@ -125,7 +125,7 @@ struct DevBuf {
 
 }  // namespace
 
-void Model::generate(uint64_t n, uint64_t seed, uint32_t grid_points, double* out, double* gen_ms) {
+void Model::generate(uint64_t n, uint64_t seed, uint32_t grid_points, double* const* out, double* gen_ms) {
   Shard& sh = shards_[0];
   if (!sh.mod->gen_max) throw Error("bad-model", "model was not built for generation");
   const Node& root = pg_.nodes[0];
@@ -273,7 +273,10 @@ void Model::generate(uint64_t n, uint64_t seed, uint32_t grid_points, double* ou
     }
   }
   ck(cudaEventRecord(ev.b, s), "event record");
-  ck(cudaMemcpyAsync(out, g.out, sizeof(double) * n * dims, cudaMemcpyDeviceToHost, s), "events D2H");
+  for (int d = 0; d < dims; ++d)  // straight into the caller's column of that observable
+    if (out[d])
+      ck(cudaMemcpyAsync(out[d], g.out + static_cast<size_t>(d) * n, sizeof(double) * n, cudaMemcpyDeviceToHost, s),
+         "events D2H");
   ck(cudaStreamSynchronize(s), "generator");
   float ms = 0;
   cudaEventElapsedTime(&ms, ev.a, ev.b);
