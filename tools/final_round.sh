@@ -2,7 +2,7 @@
 # One complete measurement round: GPU tests, every BASELINE config's bench line
 # and reference arm, ncu launch list + full captures, exchange paths, smoke.
 # Usage (on the GPU box): bash tools/final_round.sh TAG   -> gpurun_out/TAG_*
-T=${1:-r1e}
+T=${1:-r1f}
 O=gpurun_out
 nproc > $O/${T}_host.txt; lscpu | grep -E "Model name|Thread|Core|Socket" >> $O/${T}_host.txt
 python -m pytest tests -m gpu -q > $O/${T}_pytest_gpu.txt 2>&1
@@ -27,3 +27,7 @@ for c in C1 C2 C3 C4 C5; do
 done
 ncu --set full --clock-control none --import-source on -k regex:"pf_setup" -s 3 -c 1 -o $O/${T}_c2_setup \
   --force-overwrite python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-fit > $O/${T}_ncu_setup.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"pf_norm" -s 1 -c 1 -o $O/${T}_c5_norm \
+  --force-overwrite python bench.py --config C5 --steps 2 --warmup 3 --no-cpu-baseline --no-fit > $O/${T}_ncu_c5norm.log 2>&1
+python tools/gen_probe.py 10000000 1000000 > $O/${T}_generate_1e7.json 2> $O/${T}_generate.err
+python tools/gen_probe.py 100000000 0 > $O/${T}_generate_1e8.json 2>> $O/${T}_generate.err
