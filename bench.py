@@ -119,7 +119,7 @@ def peaks():
 def ncu_summary_path(config):
     """the committed ncu --set full capture of this config's event kernel
     (tools/ncu_summary.py output under profiles/)"""
-    return os.path.join(ROOT, "profiles", f"r1e_{config.lower()}_event_ncu.txt")
+    return os.path.join(ROOT, "profiles", f"r1f_{config.lower()}_event_ncu.txt")
 
 
 _SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}

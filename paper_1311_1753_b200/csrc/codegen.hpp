@@ -7,6 +7,7 @@
 // per-event work is the arithmetic itself.
 #pragma once
 
+#include <cstdint>
 #include <string>
 #include <vector>
 
@@ -46,7 +47,9 @@ struct Layout {
 };
 
 // binned: chi-squared evaluator (content/volume columns after the obs).
-Layout generate(const Program& pg, bool binned);
+// n_events (0: unknown) lets small data sets use short chunks, so that the
+// event pass spreads over every SM.
+Layout generate(const Program& pg, bool binned, uint64_t n_events = 0);
 
 // Embedded library headers (pf_device.cuh, pf_kernels.cuh).
 const char* device_header_source();

@@ -96,7 +96,7 @@ struct pf_args {
   int gworld;           // ranks in the group
   int grank;            // this rank
   int npin;             // K = 1: parameters passed inline (pin[0..npin))
-  int pad1;
+  int s_smem;            // S staged in the event pass's shared memory (models with conv tables)
   double pin[PF_MAX_INLINE];
 };
 

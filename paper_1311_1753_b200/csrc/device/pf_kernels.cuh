@@ -572,9 +572,9 @@ __device__ __forceinline__ pf_fk pf_fk_get(const pf_args& a, int k) {
 
 template <bool FULL>
 __device__ __forceinline__ pf_lacc pf_stage_terms(const pf_args& a, int k, pf_u64 base, int lane,
-                                                const double* st, int n_valid, const pf_fk& K) {
+                                                const double* st, int n_valid, const pf_fk& K,
+                                                const double* S) {
   const double* P = a.P + (pf_u64)k * PF_NP;
-  const double* S = a.S + (pf_u64)k * PF_SS;
 #if !PF_BINNED && PF_LOGFORM
   pf_lform A;
   pf_lform_init(A);
@@ -892,6 +892,13 @@ extern "C" __global__ void __launch_bounds__(PF_EV_THREADS, PF_EVENT_MIN_BLOCKS)
   const unsigned long long t_wait = pf_gtime();
 #endif
   const pf_fk fk0 = pf_fk_get(a, 0);  // fast-path operands in registers for the whole pass
+  // convolution models: the per-call state (model and resolution tables) in
+  // shared memory, read per (event, tau) pair
+  double* sS = reinterpret_cast<double*>(fxs + a.K * PF_FX_DIGITS * PF_EV_THREADS);
+  if (a.s_smem) {
+    for (int i = threadIdx.x; i < a.K * PF_SS; i += PF_EV_THREADS) sS[i] = a.S[i];
+    __syncthreads();
+  }
   for (int w = 0; w < W; ++w) {
     const int s = w % PF_NST;
     pf_mbar_wait(mybar + s, (unsigned)((w / PF_NST) & 1));
@@ -902,8 +909,9 @@ extern "C" __global__ void __launch_bounds__(PF_EV_THREADS, PF_EVENT_MIN_BLOCKS)
     const int n_valid = full ? PF_SUB : (int)(a.n_local > base ? a.n_local - base : 0);
     for (int k = 0; k < a.K; ++k) {
       const pf_fk fk = k == 0 ? fk0 : pf_fk_get(a, k);
-      pf_lacc t = full ? pf_stage_terms<true>(a, k, base, lane, my + s * PF_STAGE, n_valid, fk)
-                       : pf_stage_terms<false>(a, k, base, lane, my + s * PF_STAGE, n_valid, fk);
+      const double* Sk = (a.s_smem ? sS : a.S) + (pf_u64)k * PF_SS;
+      pf_lacc t = full ? pf_stage_terms<true>(a, k, base, lane, my + s * PF_STAGE, n_valid, fk, Sk)
+                       : pf_stage_terms<false>(a, k, base, lane, my + s * PF_STAGE, n_valid, fk, Sk);
       double* slot = accs + k * PF_LACC_N * PF_EV_THREADS + threadIdx.x;
       if (!first) {
         pf_lacc prev;

@@ -53,12 +53,27 @@ ModuleCache& cache() {
 
 // TMA stage ring (PF_EV_WARPS x PF_NST stages x PF_NLOAD x 32 PF_EPT doubles)
 // plus the per-lane chunk and fixed-point accumulators of K parameter sets
+// Models with convolution tables read the per-call state S per (event, tau)
+// pair: the event pass copies it into shared memory when it fits
+// (PF_S_SMEM; the kernel's pointer then resolves to LDS, not L1).
+bool event_s_staged(const Layout& L, int K) {
+  return !L.conv_tables.empty() && static_cast<size_t>(K) * L.ss * sizeof(double) <= 96 * 1024;
+}
+
 size_t event_smem(const Layout& L, int K) {
   const size_t stages = static_cast<size_t>(kEventWarps) * L.nst * L.load_cols.size() * 32 *
                         static_cast<size_t>(L.ept) * sizeof(double);
   // per lane and parameter set: a chunk accumulator (pf_lacc, lacc_n
   // doubles) and an exact fixed-point accumulator (6 x 8 B)
-  return stages + static_cast<size_t>(K) * 32 * kEventWarps * (8 * L.lacc_n + 48);
+  size_t bytes = stages + static_cast<size_t>(K) * 32 * kEventWarps * (8 * L.lacc_n + 48);
+  if (event_s_staged(L, K)) bytes += static_cast<size_t>(K) * L.ss * sizeof(double);
+  return bytes;
+}
+
+size_t event_smem_max(const Layout& L) {
+  size_t m = 0;
+  for (int K = 1; K <= kMaxBatch; ++K) m = std::max(m, event_smem(L, K));
+  return m;
 }
 
 namespace {
@@ -91,7 +106,7 @@ const Module* load_module(const Layout& L, int device) {
     ck(cudaLibraryGetKernel(&m->gen_scatter, m->lib, "pf_gen_scatter_kernel"), "get pf_gen_scatter_kernel");
   }
   ck(cudaKernelSetAttributeForDevice(m->event, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(event_smem(L, kMaxBatch)), device),
+                                     static_cast<int>(event_smem_max(L)), device),
      "event kernel smem attribute");
   c.modules.emplace(key, m);
   return m;
@@ -190,7 +205,7 @@ Model::Model(const pf_graph& g, const pf_data& d, uint32_t grid_points, const pf
   n_events_ = d.n_events;
   total_content_ = d.total_content;
   pg_ = finalize(g, d.n_obs, d.obs, binned_ ? 2 : 0);
-  L_ = pfb::generate(pg_, binned_);
+  L_ = pfb::generate(pg_, binned_, d.n_events);
   if (generator) {
     L_.source = "#define PF_GEN 1\n" + L_.source;
     L_.structure_key = L_.source;
@@ -459,6 +474,7 @@ Args Model::base_args(Shard& sh, int K) {
   a.gworld = group_world_;
   a.grank = group_rank_;
   a.rec = sh.d_rec;
+  a.s_smem = event_s_staged(L_, K) ? 1 : 0;
   a.total_content = total_content_;
   // norm-stage clamps are counted once (shard 0); the others discard them
   const bool counts_norm = (&sh == &shards_[0]) && shard_index_ == 0;

@@ -88,7 +88,7 @@ struct Args {
   int gworld;
   int grank;
   int npin;
-  int pad1;
+  int s_smem;  // the event pass stages S in shared memory (event_s_staged)
   double pin[64];
 };
 
@@ -146,6 +146,7 @@ struct BenchResult {
 
 void subtree_range(uint64_t n, int shard_count, int index, uint64_t* lo, uint64_t* hi);
 size_t event_smem(const Layout& L, int K);
+bool event_s_staged(const Layout& L, int K);
 int sm_count(int device);
 
 class Model {
