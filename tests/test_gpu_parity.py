@@ -339,18 +339,3 @@ def test_c5_boundary_decisions_match_oracle():
     assert bm.log_floor_count() == o.floor_count() > 0
     assert close(got, want), (got, want)
 
-
-def test_chunk_layouts_give_identical_results(monkeypatch):
-    """Small data sets use one-sub-chunk chunks (codegen.cpp); the default
-    layout (4 x 512-event sub-chunks) must give the bit-identical NLL on the
-    same data (the exact accumulator is independent of the chunking), and
-    both must match the reference golden value."""
-    x, pdf = mixture()
-    ds = pf.UnbinnedDataSet.from_columns([x], 10.0 * oracle.mt64_uniform(31, 1_000_000))
-    p = [0.4, -0.6, 5, 1]
-    small = pf.BoundModel(pdf, ds).eval_metric(p)
-    monkeypatch.setenv("PFB200_NSUB", "4")
-    monkeypatch.setenv("PFB200_EPT", "16")
-    large = pf.BoundModel(pdf, ds).eval_metric(p)
-    assert small == large
-    assert close(small, 3218448.5501374062)
