@@ -909,9 +909,21 @@ extern "C" __global__ void __launch_bounds__(PF_EV_THREADS, PF_EVENT_MIN_BLOCKS)
     const int n_valid = full ? PF_SUB : (int)(a.n_local > base ? a.n_local - base : 0);
     for (int k = 0; k < a.K; ++k) {
       const pf_fk fk = k == 0 ? fk0 : pf_fk_get(a, k);
-      const double* Sk = (a.s_smem ? sS : a.S) + (pf_u64)k * PF_SS;
-      pf_lacc t = full ? pf_stage_terms<true>(a, k, base, lane, my + s * PF_STAGE, n_valid, fk, Sk)
-                       : pf_stage_terms<false>(a, k, base, lane, my + s * PF_STAGE, n_valid, fk, Sk);
+      pf_lacc t;
+#ifdef PF_S_SMEM
+      // separate instantiations, so the staged copy is read with LDS (the
+      // pointer's address space is known), not generic loads
+      if (a.s_smem) {
+        const double* Sk = sS + (pf_u64)k * PF_SS;
+        t = full ? pf_stage_terms<true>(a, k, base, lane, my + s * PF_STAGE, n_valid, fk, Sk)
+                 : pf_stage_terms<false>(a, k, base, lane, my + s * PF_STAGE, n_valid, fk, Sk);
+      } else
+#endif
+      {
+        const double* Sk = a.S + (pf_u64)k * PF_SS;
+        t = full ? pf_stage_terms<true>(a, k, base, lane, my + s * PF_STAGE, n_valid, fk, Sk)
+                 : pf_stage_terms<false>(a, k, base, lane, my + s * PF_STAGE, n_valid, fk, Sk);
+      }
       double* slot = accs + k * PF_LACC_N * PF_EV_THREADS + threadIdx.x;
       if (!first) {
         pf_lacc prev;
