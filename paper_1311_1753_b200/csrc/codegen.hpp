@@ -41,6 +41,9 @@ struct Layout {
   int n_poly = 0;
   std::vector<double> constants;  // C buffer contents (boundaries, conv L/h)
   std::vector<ConvTable> conv_tables;
+  // convolutions with a Gaussian resolution: their normalisation grid is
+  // evaluated per grid point (window + term recurrence), not per (point, tau) pair
+  std::vector<int> conv_windowed;
   std::vector<std::vector<int>> level_nodes;  // normalised nodes per level
   std::string source;         // generated CUDA source (without library headers)
   std::string structure_key;  // cache key of the compiled module

@@ -252,7 +252,7 @@ Model::Model(const pf_graph& g, const pf_data& d, uint32_t grid_points, const pf
   double norm_work = 0;
   for (const Task& t : tasks_) {
     const Node& nd = pg_.nodes[t.node];
-    const bool pairs = nd.kind == PF_CONVOLUTION && nd.box.size() == 1;
+    const bool pairs = nd.kind == PF_CONVOLUTION && nd.box.size() == 1 && !conv_windowed(t.node);
     norm_work += static_cast<double>(t.points) *
                  (pairs ? 1.0 + subtree_cost(pg_, nd.children[1]) : subtree_cost(pg_, t.node));
   }
@@ -396,7 +396,7 @@ void Model::build_tasks(uint32_t grid_points) {
       if (dims > 8) throw Error("bad-graph", nd.name + ": more than 8 box dimensions");
       // a convolution's grid runs over (point, tau_j) pairs (codegen.cpp
       // emit_norm_point): Q elements per point, each one resolution call
-      const bool pairs = nd.kind == PF_CONVOLUTION && dims == 1;
+      const bool pairs = nd.kind == PF_CONVOLUTION && dims == 1 && !conv_windowed(node);
       const double cost = pairs ? 1.0 + subtree_cost(pg_, nd.children[1]) : subtree_cost(pg_, node);
       for (int fine = 0; fine < 2; ++fine) {
         Task t;
@@ -423,6 +423,8 @@ void Model::build_tasks(uint32_t grid_points) {
         // (PF_NORM_RUN, walked row by row) for all 256 threads of a block
         uint64_t per = static_cast<uint64_t>(std::max(1.0, std::floor(4096.0 / cost)));
         if (dims >= 2 && !pairs) per = std::max<uint64_t>(per, 256ull * 32ull);
+        // a windowed convolution point is one thread's loop: a point per thread
+        if (conv_windowed(node)) per = std::max<uint64_t>(per, 256ull);
         uint64_t nb = (total + per - 1) / per;
         if (nb > 4096) {
           nb = 4096;

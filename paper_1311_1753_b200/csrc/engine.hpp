@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <map>
 #include <memory>
@@ -200,6 +201,9 @@ class Model {
   Args base_args(Shard& s, int K);
   void build_tasks(uint32_t grid_points);
   std::string error_message(uint32_t code_node) const;
+  bool conv_windowed(int node) const {
+    return std::find(L_.conv_windowed.begin(), L_.conv_windowed.end(), node) != L_.conv_windowed.end();
+  }
   [[noreturn]] void throw_device_error(uint32_t code_node) const;
   size_t setup_smem_bytes() const {
     return sizeof(double) * (std::max(L_.np, 1) + std::max(L_.ss, 1));
