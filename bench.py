@@ -116,10 +116,17 @@ def peaks():
         return 6650.0, "fallback"
 
 
+NCU_TAGS = ("r1h", "r1g", "r1f", "r1e")  # newest first
+
+
 def ncu_summary_path(config):
-    """the committed ncu --set full capture of this config's event kernel
-    (tools/ncu_summary.py output under profiles/)"""
-    return os.path.join(ROOT, "profiles", f"r1f_{config.lower()}_event_ncu.txt")
+    """the newest committed ncu --set full capture of this config's event
+    kernel (tools/ncu_summary.py output under profiles/)"""
+    for tag in NCU_TAGS:
+        p = os.path.join(ROOT, "profiles", f"{tag}_{config.lower()}_event_ncu.txt")
+        if os.path.exists(p):
+            return p
+    return os.path.join(ROOT, "profiles", f"{NCU_TAGS[0]}_{config.lower()}_event_ncu.txt")
 
 
 _SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
