@@ -54,6 +54,11 @@ struct pf_gen_args {
   pf_u64 remaining;     // events still needed
   pf_u64* mt;           // 312-word generator state
   pf_u64 rounds;        // twists this launch
+  // jump-ahead draw (pf_mt_jump_kernel)
+  const pf_u64* jpoly;  // [segment][312]: x^(k J) mod phi, little-endian bit words
+  pf_u64* mt_next;      // the window after the batch (the next batch's base)
+  pf_u64 jump_words;    // J: words per segment
+  pf_u64 u_off;         // first word of this batch's segments in u
 };
 
 __device__ __forceinline__ double pf_gen_density(const pf_gen_args& g, double* ev, pf_ctx& cx) {
@@ -162,6 +167,97 @@ extern "C" __global__ void __launch_bounds__(160) pf_mt_kernel(const __grid_cons
   if (own) {
     g.mt[t] = a;
     g.mt[t + PF_MT_M] = b;
+  }
+}
+
+// Jump-ahead draw: block k writes words [u_off + k J, u_off + (k + 1) J) of
+// the batch, starting from the window T^(k J)(base) (T: the generator's
+// one-word window map; base = g.mt, a window in the image of T).  The start
+// window is g_k(T) base with g_k = x^(k J) mod phi (tools/gen_mt_jump.py),
+// evaluated by Horner over 156 coefficients at a time:
+//   acc <- T^156(acc) ^ sum_m g_(i-m) T^(155-m)(base),
+// where T^156 is one dependency-free half-twist and T^j(base) is the window
+// of base's own stream at offset j (<= 155, so 467 words of it suffice).
+// Then the block twists its window J / 312 times like pf_mt_kernel.  The last
+// block leaves the window after the batch in g.mt_next.
+extern "C" __global__ void __launch_bounds__(320) pf_mt_jump_kernel(const __grid_constant__ pf_gen_args g) {
+  __shared__ pf_u64 bs[PF_MT_N + PF_MT_M];    // base stream, words 0 .. 467
+  __shared__ pf_u64 acc[2][PF_MT_N];
+  __shared__ pf_u64 sa[2][PF_MT_M + 1], sb[2][PF_MT_M + 1];
+  const int t = threadIdx.x;
+  const int k = blockIdx.x;
+  for (int i = t; i < PF_MT_N; i += blockDim.x) {
+    bs[i] = g.mt[i];
+    acc[0][i] = 0ull;
+  }
+  __syncthreads();
+  if (t < PF_MT_M) bs[PF_MT_N + t] = pf_mt_twist(bs[t], bs[t + 1], bs[t + PF_MT_M]);
+  __syncthreads();
+  const pf_u64* gk = g.jpoly + (pf_u64)k * PF_MT_N;
+  int cur = 0;
+  for (int i0 = 128 * PF_MT_M - 1; i0 >= 0; i0 -= PF_MT_M) {  // 19968 >= deg phi + 1
+    // coefficients i0 - 155 .. i0: bits of gk[] (uniform across the block)
+    const int lo = i0 - (PF_MT_M - 1);
+    pf_u64 w0 = gk[lo >> 6], w1 = (lo >> 6) + 1 < PF_MT_N ? gk[(lo >> 6) + 1] : 0ull,
+           w2 = (lo >> 6) + 2 < PF_MT_N ? gk[(lo >> 6) + 2] : 0ull,
+           w3 = (lo >> 6) + 3 < PF_MT_N ? gk[(lo >> 6) + 3] : 0ull;
+    const int sh = lo & 63;
+    if (sh) {  // bits lo .. lo + 155 into (w0, w1, w2) from bit 0
+      w0 = (w0 >> sh) | (w1 << (64 - sh));
+      w1 = (w1 >> sh) | (w2 << (64 - sh));
+      w2 = (w2 >> sh) | (w3 << (64 - sh));
+    }
+    if (t < PF_MT_N) {
+      const pf_u64* A = acc[cur];
+      pf_u64 v = t < PF_MT_M ? A[t + PF_MT_M] : pf_mt_twist(A[t - PF_MT_M], A[t - PF_MT_M + 1], A[t]);
+      // bit b of (w0, w1, w2) is coefficient lo + b = i0 - m with m = 155 - b:
+      // window offset 155 - m = b
+#pragma unroll 4
+      for (int b = 0; b < PF_MT_M; ++b) {
+        const pf_u64 wd = b < 64 ? w0 : (b < 128 ? w1 : w2);
+        if ((wd >> (b & 63)) & 1ull) v ^= bs[b + t];
+      }
+      acc[cur ^ 1][t] = v;
+    }
+    cur ^= 1;
+    __syncthreads();
+  }
+  // segment k: J words from the window acc[cur] (two-phase twists, as pf_mt_kernel)
+  const bool own = t < PF_MT_M;
+  pf_u64 a = own ? acc[cur][t] : 0ull, b = own ? acc[cur][t + PF_MT_M] : 0ull;
+  int c2 = 0;
+  if (own) {
+    sa[0][t] = a;
+    sb[0][t] = b;
+  }
+  if (t == 0) sa[0][PF_MT_M] = b;
+  __syncthreads();
+  pf_u64* out = (pf_u64*)g.u + g.u_off + (pf_u64)k * g.jump_words;
+  const pf_u64 rounds = g.jump_words / PF_MT_N;
+  for (pf_u64 r = 0; r < rounds; ++r) {
+    pf_u64* o = out + r * PF_MT_N;
+    pf_u64 n1 = 0ull;
+    if (own) {
+      n1 = pf_mt_twist(a, sa[c2][t + 1], b);
+      sa[c2 ^ 1][t] = n1;
+      o[t] = n1;
+    }
+    __syncthreads();
+    if (own) {
+      const pf_u64 bn = t + 1 < PF_MT_M ? sb[c2][t + 1] : sa[c2 ^ 1][0];
+      const pf_u64 n2 = pf_mt_twist(b, bn, n1);
+      sb[c2 ^ 1][t] = n2;
+      if (t == 0) sa[c2 ^ 1][PF_MT_M] = n2;
+      o[t + PF_MT_M] = n2;
+      a = n1;
+      b = n2;
+    }
+    c2 ^= 1;
+    __syncthreads();
+  }
+  if (k == (int)gridDim.x - 1 && own) {
+    g.mt_next[t] = a;
+    g.mt_next[t + PF_MT_M] = b;
   }
 }
 

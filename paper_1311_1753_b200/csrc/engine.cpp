@@ -101,6 +101,7 @@ const Module* load_module(const Layout& L, int device) {
   if (L.source.rfind("#define PF_GEN 1\n", 0) == 0) {
     ck(cudaLibraryGetKernel(&m->gen_max, m->lib, "pf_gen_max_kernel"), "get pf_gen_max_kernel");
     ck(cudaLibraryGetKernel(&m->gen_mt, m->lib, "pf_mt_kernel"), "get pf_mt_kernel");
+    ck(cudaLibraryGetKernel(&m->gen_mt_jump, m->lib, "pf_mt_jump_kernel"), "get pf_mt_jump_kernel");
     ck(cudaLibraryGetKernel(&m->gen_eval, m->lib, "pf_gen_eval_kernel"), "get pf_gen_eval_kernel");
     ck(cudaLibraryGetKernel(&m->gen_scan, m->lib, "pf_gen_scan_kernel"), "get pf_gen_scan_kernel");
     ck(cudaLibraryGetKernel(&m->gen_scatter, m->lib, "pf_gen_scatter_kernel"), "get pf_gen_scatter_kernel");

@@ -98,8 +98,8 @@ struct Module {
   cudaKernel_t setup = nullptr, pre = nullptr, norm = nullptr, event = nullptr, final = nullptr,
                publish = nullptr;
   // generator modules only (PF_GEN, pf_generate.cuh)
-  cudaKernel_t gen_max = nullptr, gen_mt = nullptr, gen_eval = nullptr, gen_scan = nullptr,
-               gen_scatter = nullptr;
+  cudaKernel_t gen_max = nullptr, gen_mt = nullptr, gen_mt_jump = nullptr, gen_eval = nullptr,
+               gen_scan = nullptr, gen_scatter = nullptr;
 };
 
 // NVRTC compile of (library headers + generated source) for sm_100a.

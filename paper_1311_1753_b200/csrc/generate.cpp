@@ -17,6 +17,7 @@
 // samples against the reference).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -57,7 +58,13 @@ struct GenArgs {  // pf_gen_args (pf_generate.cuh); layouts must match
   uint64_t remaining;
   uint64_t* mt;
   uint64_t rounds;
+  const uint64_t* jpoly;
+  uint64_t* mt_next;
+  uint64_t jump_words;
+  uint64_t u_off;
 };
+
+#include "mt_jump_table.inc"  // tools/gen_mt_jump.py
 
 constexpr uint64_t kSegment = 256 * 8;  // PF_GEN_SEGMENT
 constexpr uint64_t kMtN = 312;
@@ -192,32 +199,67 @@ void Model::generate(uint64_t n, uint64_t seed, uint32_t grid_points, double* co
     return std::min(full, unit * static_cast<uint64_t>(std::min(u, 1e12)));
   };
 
-  DevBuf b_u[2], b_flags, b_cnt, b_base, b_fail, b_out, b_mt;
-  double* u[2] = {b_u[0].alloc<double>(sizeof(double) * full * w), b_u[1].alloc<double>(sizeof(double) * full * w)};
-  g.flags = b_flags.alloc<unsigned char>(full);
-  g.block_count = b_cnt.alloc<uint32_t>(sizeof(uint32_t) * (full / kSegment));
-  g.block_base = b_base.alloc<uint32_t>(sizeof(uint32_t) * (full / kSegment));
-  g.fail_density = b_fail.alloc<double>(sizeof(double) * full);
+  // the stream is drawn by jumps (every batch: 128 segments of J words, each
+  // from its own jumped window, pf_mt_jump_kernel) when a candidate's words
+  // divide a twist; otherwise by the one-CTA sequential kernel
+  const bool jump = kMtN % w == 0 && !std::getenv("PFB200_MT_SEQUENTIAL");
+  const uint64_t seg_words = static_cast<uint64_t>(kMtJumpSegments) * kMtJumpWords;
+  const uint64_t cap = jump ? (kMtN + seg_words) / w : full;  // candidates per batch, at most
+
+  DevBuf b_u[2], b_flags, b_cnt, b_base, b_fail, b_out, b_mt, b_mt2, b_poly;
+  double* u[2] = {b_u[0].alloc<double>(sizeof(double) * cap * w), b_u[1].alloc<double>(sizeof(double) * cap * w)};
+  const uint64_t cap_blocks = (cap + kSegment - 1) / kSegment;
+  g.flags = b_flags.alloc<unsigned char>(cap);
+  g.block_count = b_cnt.alloc<uint32_t>(sizeof(uint32_t) * cap_blocks);
+  g.block_base = b_base.alloc<uint32_t>(sizeof(uint32_t) * cap_blocks);
+  g.fail_density = b_fail.alloc<double>(sizeof(double) * cap);
   g.out = b_out.alloc<double>(sizeof(double) * n * dims);
   g.out_stride = n;
-  g.mt = b_mt.alloc<uint64_t>(sizeof(uint64_t) * kMtN);
+  uint64_t* mt_cur = b_mt.alloc<uint64_t>(sizeof(uint64_t) * kMtN);
+  uint64_t* mt_other = jump ? b_mt2.alloc<uint64_t>(sizeof(uint64_t) * kMtN) : nullptr;
+  g.mt = mt_cur;
   std::vector<uint64_t> mt(kMtN);
   mt_seed(seed, mt.data());
-  ck(cudaMemcpyAsync(g.mt, mt.data(), sizeof(uint64_t) * kMtN, cudaMemcpyHostToDevice, s), "mt seed");
+  ck(cudaMemcpyAsync(mt_cur, mt.data(), sizeof(uint64_t) * kMtN, cudaMemcpyHostToDevice, s), "mt seed");
+  if (jump) {
+    g.jpoly = b_poly.alloc<uint64_t>(sizeof(uint64_t) * kMtN * kMtJumpSegments);
+    ck(cudaMemcpyAsync(const_cast<uint64_t*>(g.jpoly), kMtJumpPoly, sizeof(uint64_t) * kMtN * kMtJumpSegments,
+                       cudaMemcpyHostToDevice, s),
+       "jump table");
+    g.jump_words = kMtJumpWords;
+  }
 
-  // the stream of batch b + 1 is drawn (second stream, one SM) while batch b
-  // is evaluated; batch sizes follow the measured acceptance so the stream
-  // drawn past the last needed candidate stays small
+  // the stream of batch b + 1 is drawn (second stream) while batch b is
+  // evaluated; sequential draws size their batches by the measured
+  // acceptance so the stream drawn past the last needed candidate stays small
   Side side(sh.device);
   uint64_t size[2] = {round_up(4.0 * static_cast<double>(n)), 0};
   ck(cudaEventRecord(side.ready, s), "event record");  // the seeded state
   ck(cudaStreamWaitEvent(side.s, side.ready, 0), "stream wait");
+  int draws = 0;
   auto draw = [&](int slot, uint64_t B) {
     GenArgs m = g;
     m.u = u[slot];
-    m.rounds = B * w / kMtN;
-    size[slot] = B;
-    launch_gen(sh.mod->gen_mt, 1, 160, side.s, m);
+    if (jump) {
+      uint64_t words = 0;
+      if (draws == 0) {  // the seeded window is not in the image of T: one plain twist first
+        m.mt = mt_cur;
+        m.rounds = 1;
+        launch_gen(sh.mod->gen_mt, 1, 160, side.s, m);
+        words = kMtN;
+      }
+      m.mt = mt_cur;
+      m.mt_next = mt_other;
+      m.u_off = words;
+      launch_gen(sh.mod->gen_mt_jump, static_cast<unsigned>(kMtJumpSegments), 320, side.s, m);
+      std::swap(mt_cur, mt_other);
+      size[slot] = (words + seg_words) / w;
+    } else {
+      m.rounds = B * w / kMtN;
+      size[slot] = B;
+      launch_gen(sh.mod->gen_mt, 1, 160, side.s, m);
+    }
+    ++draws;
     ck(cudaEventRecord(side.drawn[slot], side.s), "event record");
   };
   draw(0, size[0]);
@@ -232,7 +274,7 @@ void Model::generate(uint64_t n, uint64_t seed, uint32_t grid_points, double* co
     uint64_t r[8] = {0, ~0ull, ~0ull, ~0ull, 0, 0, 0, 0};
     ck(cudaMemcpyAsync(g.rec, r, sizeof r, cudaMemcpyHostToDevice, s), "rec reset");
     ck(cudaStreamWaitEvent(s, side.drawn[slot], 0), "stream wait");
-    const unsigned blocks = static_cast<unsigned>(B / kSegment);
+    const unsigned blocks = static_cast<unsigned>((B + kSegment - 1) / kSegment);
     launch_gen(sh.mod->gen_eval, blocks, 256, s, g);
     launch_gen(sh.mod->gen_scan, 1, 1024, s, g);
     launch_gen(sh.mod->gen_scatter, blocks, 256, s, g);

@@ -337,3 +337,23 @@ def test_generate_events_rejects_empty_request_without_a_gpu():
     pdf = pf.exp_pdf("e", x, pf.new_parameter("a", -0.5, 0.1, -5, 5))
     with pytest.raises(pf.Error, match="bad-arity: generate_events: n_events"):
         pf.generate_events(pdf, [x], 0, 1)
+
+
+def test_mt_jump_table_jumps_the_reference_stream():
+    """csrc/mt_jump_table.inc (tools/gen_mt_jump.py): applying g_k (Horner in
+    blocks of 156 coefficients, the GPU generator's algorithm) to a window of
+    the mt19937_64 stream lands exactly k J words further on."""
+    import importlib.util
+    import re as _re
+    spec = importlib.util.spec_from_file_location("gen_mt_jump", os.path.join(ROOT, "tools", "gen_mt_jump.py"))
+    gj = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(gj)
+    text = open(os.path.join(ROOT, "paper_1311_1753_b200", "csrc", "mt_jump_table.inc")).read()
+    rows = _re.findall(r"\{([0-9a-fx,ul]+)\}", text)
+    assert len(rows) == gj.SEGMENTS + 1
+    k = 3
+    words = [int(w.rstrip("ul"), 16) for w in rows[k].split(",")]
+    g = sum(w << (64 * i) for i, w in enumerate(words))
+    base = gj.stream(gj.seed_state(20260823), gj.N)  # a window in the image of T
+    far = base + gj.stream(base, k * gj.JUMP + gj.N)
+    assert gj.apply_poly(g, base) == far[k * gj.JUMP: k * gj.JUMP + gj.N]
