@@ -573,6 +573,44 @@ __device__ __forceinline__ bool pf_dalitz_inside(double s12, double s13, double 
   return s13 >= lo && s13 <= hi;
 }
 
+// Per-channel quantities shared by every resonance of the channel (same s,
+// same daughters): q = |p*| of the split, and for spin 1 the Blatt-Weisskopf
+// reciprocal root 1/sqrt(1 + R^2 q^2) and its square.
+struct pf_dalitz_ch {
+  double s, rs, q, ru, ru2;
+};
+
+__device__ __forceinline__ pf_dalitz_ch pf_dalitz_channel(double s, double rs, double mi, double mj, double R2) {
+  pf_dalitz_ch c;
+  c.s = s;
+  c.rs = rs;
+  const double sp = mi + mj, sm = mi - mj;
+  const double q2 = fmax(fma(-sp, sp, s) * fma(-sm, sm, s) * (0.25 * (rs * rs)), 0.0);
+  c.q = q2 > 0.0 ? q2 * pf_rsqrt_fast(q2) : 0.0;
+  c.ru = pf_rsqrt_fast(fma(R2, q2, 1.0));
+  c.ru2 = c.ru * c.ru;
+  return c;
+}
+
+// one resonance of a channel: pf_dalitz_res_fast with the channel's shared terms
+__device__ __forceinline__ pf_cplx pf_dalitz_res_ch(const pf_dalitz_ch& c, double Z, double m, double m2, double G,
+                                                    double iq0, double br0, double sbr0, int spin) {
+  const double x = c.q * iq0;
+  double bf2 = 1.0, ratio = x, sbf = 1.0;
+  if (spin == 1) {
+    bf2 = br0 * c.ru2;
+    ratio = x * x * x;
+    sbf = sbr0 * c.ru;
+  }
+  const double gs = G * ratio * (m * c.rs) * bf2;
+  const double a = m2 - c.s, b = m * gs;
+  const double f = Z * sbf * pf_rcp_fast(fma(a, a, b * b));
+  pf_cplx r;
+  r.re = f * a;
+  r.im = f * b;
+  return r;
+}
+
 // The same decision as pf_dalitz_inside, cheaply: the limits lo/hi of s13
 // come from the fast reciprocals.  With p >= 1e-3 E the fast and exact
 // sequences differ by < 5e-13 (e^2 + p^2), so a point farther than
