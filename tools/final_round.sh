@@ -2,7 +2,7 @@
 # One complete measurement round: GPU tests, every BASELINE config's bench line
 # and reference arm, ncu launch list + full captures, exchange paths, smoke.
 # Usage (on the GPU box): bash tools/final_round.sh TAG   -> gpurun_out/TAG_*
-T=${1:-r1f}
+T=${1:-r1i}
 O=gpurun_out
 nproc > $O/${T}_host.txt; lscpu | grep -E "Model name|Thread|Core|Socket" >> $O/${T}_host.txt
 python -m pytest tests -m gpu -q > $O/${T}_pytest_gpu.txt 2>&1
