@@ -326,8 +326,9 @@ PF_API int pf_fit(pf_model* model, int32_t metric, const pf_fit_config* config, 
  * accepted event for the PDF's box observables, their current value
  * otherwise (the reference sets Variable::value per accepted event, :79).
  * Runs on options->device (null: device 0).  gen_ms (optional): device time
- * of the generation.  Errors: bad-arity (n_events < 1), the norm and raw
- * errors of the PDF, envelope-failure (generate.hpp:65-76). */
+ * of the batch loop (draw, evaluate, compact; buffer allocation excluded).
+ * Errors: bad-arity (n_events < 1), the norm and raw errors of the PDF,
+ * envelope-failure (generate.hpp:65-76). */
 PF_API int pf_generate_events(const pf_graph* graph, const int32_t* obs, int32_t n_obs,
                               uint64_t n_events, uint64_t seed, uint32_t grid_points,
                               const pf_options* options, double* out, double* last, double* gen_ms,

@@ -149,8 +149,7 @@ void Model::generate(uint64_t n, uint64_t seed, uint32_t grid_points, double* co
 
   ck(cudaSetDevice(sh.device), "cudaSetDevice");
   cudaStream_t s = sh.stream;
-  Events ev;
-  ck(cudaEventRecord(ev.a, s), "event record");
+  Events ev;  // gen_ms: the batch loop (draw, evaluate, compact), after the buffers exist
 
   GenArgs g;
   std::memset(&g, 0, sizeof g);
@@ -262,6 +261,7 @@ void Model::generate(uint64_t n, uint64_t seed, uint32_t grid_points, double* co
     ++draws;
     ck(cudaEventRecord(side.drawn[slot], side.s), "event record");
   };
+  ck(cudaEventRecord(ev.a, s), "event record");
   draw(0, size[0]);
   uint64_t done = 0, cand_total = 0, acc_total = 0;
   for (int b = 0;; ++b) {
