@@ -188,3 +188,26 @@ def test_ten_million_events_mixture_fraction():
     p = f_exp + g
     emp = float(np.mean(x < 2.0))
     assert abs(emp - p) < 5 * math.sqrt(p * (1 - p) / x.size)
+
+
+def test_sequential_stream_path_gives_the_same_sample(monkeypatch):
+    """PFB200_MT_SEQUENTIAL forces the one-CTA stream (the path for candidates
+    whose word count does not divide a twist): same sample as the jump-ahead
+    draw and as the reference"""
+    pdf, obs, n, seed, grid = CASES["prod2d"](pf)
+    jumped = pf.generate_events(pdf, obs, n, seed, pf.GridSpec(grid)).columns()
+    monkeypatch.setenv("PFB200_MT_SEQUENTIAL", "1")
+    seq = pf.generate_events(pdf, obs, n, seed, pf.GridSpec(grid)).columns()
+    assert np.array_equal(jumped, seq)
+    assert hashlib.sha256(np.ascontiguousarray(seq).tobytes()).hexdigest() == GOLDEN["prod2d"]["sha256"]
+
+
+def test_four_dimensional_sample_vs_restatement():
+    """4 observables: 5 words per candidate (does not divide 312), so the
+    sequential stream; checked against the oracle restatement"""
+    obs = [pf.new_observable(f"x{i}", 0, 5) for i in range(4)]
+    pars = [pf.new_parameter(f"a{i}", -0.1 + 0.02 * i, 0.1, -5, 5) for i in range(4)]  # gentle slopes:
+    pdf = pf.prod_pdf("p4", [pf.exp_pdf(f"e{i}", obs[i], pars[i]) for i in range(4)])  # the 16^4 grid's
+    got = pf.generate_events(pdf, obs, 3000, 41, pf.GridSpec(16)).columns()  # max stays inside the envelope
+    want = restated_generate(pf, pdf, obs, 3000, 41, 16)
+    assert np.array_equal(got, want)
