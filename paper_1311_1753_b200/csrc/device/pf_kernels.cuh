@@ -147,13 +147,28 @@ extern "C" __global__ void __launch_bounds__(PF_SETUP_THREADS) pf_setup_kernel(c
     double x[PF_SETUP_MAXQ];
 #pragma unroll
     for (int q = 0; q < PF_SETUP_MAXQ; ++q) x[q] = 0.0;
-    for (int q = 0; q < nl; ++q) {
+    // the level's midpoints as one index space (task q owns [off[q], off[q+1])):
+    // a thread's few points are independent evaluations whose latencies
+    // overlap, instead of one short loop per task
+    pf_u64 off[PF_SETUP_MAXQ + 1];
+    off[0] = 0;
+#pragma unroll
+    for (int q = 0; q < PF_SETUP_MAXQ; ++q) off[q + 1] = off[q] + (q < nl ? tk[t0 + q].points : 0ull);
+#pragma unroll 2
+    for (pf_u64 g = rank * PF_SETUP_THREADS + threadIdx.x; g < off[PF_SETUP_MAXQ];
+         g += PF_SETUP_THREADS * PF_SETUP_CLUSTER) {
+      int q = 0;
+      pf_u64 first = 0;  // (constant indices only: off[] stays in registers)
+#pragma unroll
+      for (int qq = 1; qq < PF_SETUP_MAXQ; ++qq)
+        if (g >= off[qq]) {
+          q = qq;
+          first = off[qq];
+        }
       const pf_task& T = tk[t0 + q];
-      double acc = 0.0;
-      for (pf_u64 i = rank * PF_SETUP_THREADS + threadIdx.x; i < T.points;
-           i += PF_SETUP_THREADS * PF_SETUP_CLUSTER)
-        acc += pf_norm_point(T.node, i, T, P, S, a.C, cx, cnt);
-      x[q] = acc;
+      const double v = pf_norm_point(T.node, g - first, T, P, S, a.C, cx, cnt);
+#pragma unroll
+      for (int qq = 0; qq < PF_SETUP_MAXQ; ++qq) x[qq] += qq == q ? v : 0.0;
     }
     PF_TRACE("points");
     // warp trees of all the level's sums together
