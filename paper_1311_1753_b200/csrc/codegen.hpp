@@ -35,6 +35,7 @@ struct Layout {
   int nst = 3;                // TMA stages per event warp (PF_NST)
   int setup_maxq = 8;         // most midpoint sums in one level (PF_SETUP_MAXQ)
   int lacc_n = 2;             // doubles of the per-lane chunk accumulator (PF_LACC_N)
+  int unroll = 8;             // events interleaved per lane in the event loop (PF_UNROLL)
   int data_range_base = -1;   // C slots: (min, max) per data column, filled at bind time
   std::vector<int> load_cols; // data columns read per event
   std::vector<int> poly_index; // node -> clamp counter index (-1 otherwise)
