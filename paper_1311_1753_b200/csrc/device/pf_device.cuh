@@ -637,6 +637,47 @@ __device__ __forceinline__ bool pf_dalitz_inside_fast(double s12, double s13, do
   return pf_dalitz_inside(s12, s13, M, m1, m2, m3);
 }
 
+// pf_dalitz_inside_fast split for a grid row (s12 fixed): the s12 side once
+// per row, then per point the same decision as pf_dalitz_inside_fast.
+struct pf_dalitz_row {
+  bool in12, exact;
+  double lo, hi, tol;
+};
+
+__device__ __forceinline__ pf_dalitz_row pf_dalitz_row_limits(double s12, double M, double m1, double m2, double m3) {
+  pf_dalitz_row R;
+  R.exact = false;
+  R.lo = R.hi = R.tol = 0.0;
+  const double a12 = __dadd_rn(m1, m2), b12 = __dsub_rn(M, m3);
+  R.in12 = s12 >= __dmul_rn(a12, a12) && s12 <= __dmul_rn(b12, b12);
+  if (!R.in12) return R;
+  const double ir = 0.5 * pf_rsqrt_fast(s12);
+  const double e1 = (s12 - m2 * m2 + m1 * m1) * ir;
+  const double e3 = (M * M - s12 - m3 * m3) * ir;
+  const double t1 = e1 * e1 - m1 * m1, t3 = e3 * e3 - m3 * m3;
+  if (!(t1 >= 1e-6 * (e1 * e1)) || !(t3 >= 1e-6 * (e3 * e3))) {
+    R.exact = true;
+    return R;
+  }
+  const double p1 = t1 * pf_rsqrt_fast(t1), p3 = t3 * pf_rsqrt_fast(t3);
+  const double e = e1 + e3, pp = p1 + p3, pm = p1 - p3;
+  const double ee = e * e;
+  R.lo = ee - pp * pp;
+  R.hi = ee - pm * pm;
+  R.tol = 1e-11 * (ee + pp * pp);
+  return R;
+}
+
+__device__ __forceinline__ bool pf_dalitz_row_inside(const pf_dalitz_row& R, double s12, double s13, double M,
+                                                     double m1, double m2, double m3) {
+  if (!R.in12) return false;
+  if (!R.exact) {
+    if (s13 < R.lo - R.tol || s13 > R.hi + R.tol) return false;
+    if (s13 > R.lo + R.tol && s13 < R.hi - R.tol) return true;
+  }
+  return pf_dalitz_inside(s12, s13, M, m1, m2, m3);
+}
+
 // ----------------------------------------------------------------------------
 // TMA bulk copies (cp.async.bulk, global -> shared) completed on mbarriers.
 __device__ __forceinline__ unsigned pf_smem_addr(const void* p) {
