@@ -97,6 +97,7 @@ struct pf_args {
   int grank;            // this rank
   int npin;             // K = 1: parameters passed inline (pin[0..npin))
   int s_smem;            // S staged in the event pass's shared memory (models with conv tables)
+  long long* big;       // K x PF_BIG_STRIDE: wide accumulator of chunk sums >= 2^62 (pf_big_add)
   double pin[PF_MAX_INLINE];
 };
 
@@ -293,6 +294,45 @@ __device__ __forceinline__ void pf_fxl_add(pf_fxl& A, double x) {
     A.d[i] += sg * v;
   }
   if (poison) A.d[PF_FX_DIGITS - 1] += 0x4000000000000000ll;
+}
+
+// Wide accumulator for the rare chunk sums |x| >= 2^62 (chi-squared far from
+// the data: the reference's long-double sum has no such range limit,
+// engine.hpp:57-87): value = sum_i b_i 2^(32 i), exact for every finite
+// |x| >= 2^52.  Global atomics, out of line: never on the common path.
+// Per parameter set PF_BIG_STRIDE words: [0, PF_BIG_DIGITS) accumulating
+// digits and PF_BIG_COUNT their add count (both reset by the finalizing warp),
+// [PF_BIG_SNAP, +PF_BIG_DIGITS) the last call's digits and PF_BIG_SNAP_COUNT
+// its count, which the host reads when the published result is NaN.
+#define PF_BIG_DIGITS 34
+#define PF_BIG_COUNT 40
+#define PF_BIG_SNAP 64
+#define PF_BIG_SNAP_COUNT 104
+#define PF_BIG_STRIDE 128
+
+__device__ __noinline__ void pf_big_add(long long* big, double x) {
+  const pf_u64 bits = (pf_u64)__double_as_longlong(x);
+  const pf_u64 m = (bits & 0xfffffffffffffull) | 0x10000000000000ull;
+  const int p = (int)((bits >> 52) & 0x7ff) - 1075;  // LSB position, >= 10 here
+  const int q = p >> 5, s = p & 31;
+  const pf_u64 d0 = (m << s) & 0xffffffffull;
+  const pf_u64 d1 = (s ? (m >> (32 - s)) : (m >> 32)) & 0xffffffffull;
+  const pf_u64 d2 = s ? (m >> (64 - s)) : 0ull;
+  const bool neg = (bits >> 63) != 0;
+  const long long v[3] = {(long long)d0, (long long)d1, (long long)d2};
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+    if (v[i]) atomicAdd((unsigned long long*)(big + q + i), (unsigned long long)(neg ? -v[i] : v[i]));
+  atomicAdd((unsigned long long*)(big + PF_BIG_COUNT), 1ull);
+}
+
+// a chunk sum into the lane's accumulator, or (|x| >= 2^62, finite) the wide one
+__device__ __forceinline__ void pf_fxl_add_w(pf_fxl& A, double x, long long* big) {
+  const double ax = fabs(x);
+  if (ax >= 0x1p62 && ax <= 1.7976931348623157e308)
+    pf_big_add(big, x);
+  else
+    pf_fxl_add(A, x);
 }
 
 // Warp-wide integer sum of the lanes' accumulators into the global one.

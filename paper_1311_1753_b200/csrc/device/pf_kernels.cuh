@@ -725,12 +725,13 @@ __device__ __forceinline__ pf_lacc pf_stage_terms(const pf_args& a, int k, pf_u6
 // value is bitwise the single-device one.  A peer missing for 5 s reports
 // PF_E_GROUP_TIMEOUT instead of hanging.
 __device__ __noinline__ void pf_group_exchange(const pf_args& a, int k, int lane, long long* d, pf_u32& normerr,
-                                                pf_u64& nonfinite, pf_u64& evterr) {
+                                                pf_u64& nonfinite, pf_u64& evterr, int& gbig) {
   long long g[PF_FX_DIGITS];
 #pragma unroll
   for (int i = 0; i < PF_FX_DIGITS; ++i) g[i] = __shfl_sync(0xffffffffu, d[i], 0);
   const pf_u32 nerr = __shfl_sync(0xffffffffu, normerr, 0);
-  const int flag = __shfl_sync(0xffffffffu, (int)(nonfinite != ~0ull || evterr != ~0ull), 0);
+  // bit 0: an error or non-finite term, bit 1: wide (>= 2^62) chunk sums
+  const int flag = __shfl_sync(0xffffffffu, (int)(nonfinite != ~0ull || evterr != ~0ull) | (gbig ? 2 : 0), 0);
   const unsigned long long seq = (unsigned long long)(a.done[1 + k] + 1u);
   if (lane < a.gworld) {  // send: lane q writes this rank's record into rank q's buffer
     long long* dst = a.peers[lane] + ((pf_u64)k * PF_GROUP_MAX + a.grank) * 16;
@@ -779,7 +780,8 @@ __device__ __noinline__ void pf_group_exchange(const pf_args& a, int k, int lane
   }
   if (lane == 0) {
     normerr = timeout ? ((0xffffffu << 8) | PF_E_GROUP_TIMEOUT) : min(normerr, qerr);
-    if (qflag && nonfinite == ~0ull && evterr == ~0ull) nonfinite = 0;  // a peer's term was non-finite
+    if ((qflag & 1) && nonfinite == ~0ull && evterr == ~0ull) nonfinite = 0;  // a peer's term was non-finite
+    gbig = (qflag & 2) != 0;  // some rank's sum left the fixed-point range: NaN everywhere
   }
 }
 
@@ -813,15 +815,29 @@ __device__ void pf_finalize_warp0(const pf_args& a, int lane) {
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) d[i] += __shfl_down_sync(0xffffffffu, d[i], off);
       }
-      if (a.peers) pf_group_exchange(a, k, lane, d, normerr, nonfinite, evterr);
+      // chunk sums beyond the fixed-point range: snapshot the wide digits for
+      // the host (which then combines them with d) and reset them
+      long long* bg = a.big + (pf_u64)k * PF_BIG_STRIDE;
+      const long long nbig = (long long)__ldcg((const unsigned long long*)(bg + PF_BIG_COUNT));
+      if (nbig) {
+        for (int i = lane; i < PF_BIG_DIGITS; i += 32) {
+          bg[PF_BIG_SNAP + i] = (long long)__ldcg((const unsigned long long*)(bg + i));
+          bg[i] = 0ll;
+        }
+      }
+      int gbig = nbig != 0;
+      if (a.peers) pf_group_exchange(a, k, lane, d, normerr, nonfinite, evterr, gbig);
       pf_out* o = a.hout + k;
       if (lane == 0) {
+        bg[PF_BIG_COUNT] = 0ll;
+        bg[PF_BIG_SNAP_COUNT] = nbig;
         long long* dp = a.dpart + (pf_u64)k * 8;  // the device copy, for a stream-ordered collective
 #pragma unroll
         for (int i = 0; i < PF_FX_DIGITS; ++i) dp[i] = d[i];
         dp[6] = (long long)normerr;
-        dp[7] = (nonfinite != ~0ull || evterr != ~0ull) ? 1 : 0;
-        o->result = pf_fx_round(d);
+        dp[7] = ((nonfinite != ~0ull || evterr != ~0ull) ? 1 : 0) | (gbig ? 2 : 0);
+        // NaN: the host adds the wide digits (Model::wait_results)
+        o->result = gbig ? __longlong_as_double(0x7ff8000000000000ll) : pf_fx_round(d);
 #pragma unroll
         for (int i = 0; i < PF_FX_DIGITS; ++i) o->fx[i] = d[i];
         o->floor_count = floors;
@@ -962,8 +978,9 @@ extern "C" __global__ void __launch_bounds__(PF_EV_THREADS, PF_EVENT_MIN_BLOCKS)
         pf_fxl A;
 #pragma unroll
         for (int i = 0; i < PF_FX_DIGITS; ++i) A.d[i] = fxs[(k * PF_FX_DIGITS + i) * PF_EV_THREADS + threadIdx.x];
-        pf_fxl_add(A, t.hi);
-        pf_fxl_add(A, t.lo);
+        long long* big = a.big + (pf_u64)k * PF_BIG_STRIDE;
+        pf_fxl_add_w(A, t.hi, big);
+        pf_fxl_add_w(A, t.lo, big);
 #pragma unroll
         for (int i = 0; i < PF_FX_DIGITS; ++i) fxs[(k * PF_FX_DIGITS + i) * PF_EV_THREADS + threadIdx.x] = A.d[i];
       }

@@ -310,6 +310,8 @@ Model::Model(const pf_graph& g, const pf_data& d, uint32_t grid_points, const pf
     ck(cudaMemset(sh.d_recv, 0, sizeof(int64_t) * 16 * kMaxGroup * kMaxBatch), "memset group receive");
     ck(cudaMalloc(&sh.d_part, sizeof(int64_t) * 8 * kMaxBatch), "cudaMalloc partial");
     ck(cudaMemset(sh.d_part, 0, sizeof(int64_t) * 8 * kMaxBatch), "memset partial");
+    ck(cudaMalloc(&sh.d_big, sizeof(int64_t) * kBigStride * kMaxBatch), "cudaMalloc wide digits");
+    ck(cudaMemset(sh.d_big, 0, sizeof(int64_t) * kBigStride * kMaxBatch), "memset wide digits");
     const size_t bins = sizeof(int64_t) * kMaxBatch * kFxBins * 16;
     ck(cudaMalloc(&sh.d_fxbins, bins), "cudaMalloc fxbins");
     ck(cudaMemset(sh.d_fxbins, 0, bins), "memset fxbins");
@@ -366,6 +368,7 @@ Model::~Model() {
     cudaFree(sh.d_done);
     cudaFree(sh.d_fxbins);
     cudaFree(sh.d_part);
+    cudaFree(sh.d_big);
     for (void* p : sh.ipc_mapped) cudaIpcCloseMemHandle(p);
     cudaFree(sh.d_peers);
     cudaFree(sh.d_recv);
@@ -473,6 +476,7 @@ Args Model::base_args(Shard& sh, int K) {
   a.done = sh.d_done;
   a.fxbins = sh.d_fxbins;
   a.dpart = sh.d_part;
+  a.big = sh.d_big;
   a.peers = sh.d_peers;
   a.gworld = group_world_;
   a.grank = group_rank_;
@@ -691,6 +695,8 @@ void Model::wait_results(int K, std::vector<Raw>& out, bool partial_only) {
       out[k].fx[i] = s;
     }
     out[k].value = shards_.size() == 1 ? shards_[0].h_out[k].result : fx_round(out[k].fx);
+    for (Shard& sh : shards_) out[k].wide |= std::isnan(sh.h_out[k].result) && nonfinite == ~0ull;
+    if (out[k].wide && !partial_only) out[k].value = wide_value(k);
     if (!partial_only) {
       // any non-finite term makes the reference's sum non-finite
       // (engine.hpp:210-216); the device neutralised it and kept its index
@@ -705,6 +711,33 @@ void Model::wait_results(int K, std::vector<Raw>& out, bool partial_only) {
       for (size_t i = 0; i < pg_.nodes.size(); ++i)
         if (L_.poly_index[i] >= 0) clamp_total_[i] += sh.h_clamp[L_.poly_index[i]];
   }
+}
+
+// Rare path: some chunk sums were >= 2^62 (pf_big_add), beyond the six
+// fixed-point digits.  The shards' wide digits (2^(32 j)) and fixed-point
+// digits (2^(32 i - 128)) are added exactly on one 2^-128 grid and rounded
+// once, so the value is still the correctly rounded exact sum of the chunk
+// sums.  A poisoned fixed-point top digit (a non-finite chunk sum) gives NaN.
+double Model::wide_value(int k) {
+  if (group_world_ > 1)  // the exchanged digits are the group's, the wide ones only this rank's
+    throw Error("metric-overflow", "chunk sums exceed the 2^63 range of the exact cross-rank digits");
+  constexpr int D = 4 + kBigDigits + 2;
+  int64_t acc[D] = {};
+  std::vector<int64_t> snap(kBigStride);
+  for (Shard& sh : shards_) {
+    const int64_t* fx = sh.h_out[k].fx;
+    if (fx[5] >= (1ll << 61) || fx[5] <= -(1ll << 61)) return std::numeric_limits<double>::quiet_NaN();
+    for (int i = 0; i < 6; ++i) acc[i] += fx[i];
+    if (!std::isnan(sh.h_out[k].result)) continue;
+    ck(cudaSetDevice(sh.device), "cudaSetDevice");
+    ck(cudaStreamSynchronize(sh.stream), "evaluation");
+    ck(cudaMemcpy(snap.data(), sh.d_big + static_cast<size_t>(k) * kBigStride, sizeof(int64_t) * kBigStride,
+                  cudaMemcpyDeviceToHost),
+       "wide digits");
+    if (snap[kBigSnapCount] == 0) continue;
+    for (int j = 0; j < kBigDigits; ++j) acc[4 + j] += snap[kBigSnap + j];
+  }
+  return fx_round_n(acc, D);
 }
 
 // BoundModel::eval_metric (engine.hpp:165-218)
@@ -766,6 +799,8 @@ void Model::eval_partial(const double* params, size_t n, int metric, int64_t* fx
     *penalty = 1;
     return;
   }
+  if (out[0].wide)
+    throw Error("metric-overflow", "a shard's chunk sums exceed the 2^63 range of the exact cross-shard digits");
   for (int i = 0; i < 6; ++i) fx[i] = out[0].fx[i];
 }
 
@@ -932,9 +967,10 @@ BenchResult Model::bench(const double* params, size_t n, int metric, int steps, 
 
 namespace pfb {
 
-double fx_round(const int64_t* acc) {
-  constexpr int D = 6;
-  uint32_t dig[D];
+double fx_round(const int64_t* acc) { return fx_round_n(acc, 6); }
+
+double fx_round_n(const int64_t* acc, int D) {
+  uint32_t dig[64];
   int64_t carry = 0;
   for (int i = 0; i < D; ++i) {
     const int64_t v = acc[i] + carry;

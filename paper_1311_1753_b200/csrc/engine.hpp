@@ -23,6 +23,8 @@ constexpr int kEventBlocksPerSM = 8;     // resident event blocks per SM (PF_EVE
 constexpr int kMaxGroup = 16;              // PF_GROUP_MAX: ranks of a peer-memory exchange group
 constexpr int kFxBins = 32;               // PF_FX_BINS (x 16 int64 per bin)
 constexpr double kSmallNormWork = 65536; // raw evaluations: single-CTA setup path
+// wide accumulator of chunk sums >= 2^62 (pf_device.cuh PF_BIG_*)
+constexpr int kBigDigits = 34, kBigSnap = 64, kBigSnapCount = 104, kBigStride = 128;
 
 // host mirrors of the device structs (pf_device.cuh); layouts must match
 struct KRec {
@@ -56,6 +58,8 @@ static_assert(sizeof(Out) == 88, "pf_out layout");
 // Correctly rounded double of a superaccumulator (digits d_i 2^(32 i - 128));
 // host twin of pf_fx_round (pf_device.cuh).  NaN when poisoned.
 double fx_round(const int64_t* fx);
+// the same for D digits d_i 2^(32 i - 128) (D <= 64)
+double fx_round_n(const int64_t* fx, int D);
 
 struct Args {
   const double* hP;
@@ -90,6 +94,7 @@ struct Args {
   int grank;
   int npin;
   int s_smem;  // the event pass stages S in shared memory (event_s_staged)
+  int64_t* big;  // kMaxBatch x kBigStride wide accumulator (pf_big_add)
   double pin[64];
 };
 
@@ -122,6 +127,7 @@ struct Shard {
   uint32_t seq[kMaxBatch] = {};  // completion sequence the host expects next, per k
   int64_t* d_fxbins = nullptr;  // kMaxBatch x kFxBins x 16 binned digits of the event pass
   int64_t* d_part = nullptr;    // kMaxBatch x 8: exact digits + error words of the last call (device)
+  int64_t* d_big = nullptr;     // kMaxBatch x kBigStride wide accumulator + last-call snapshot
   int64_t* d_recv = nullptr;    // group exchange: kMaxBatch x kMaxGroup x 16 receive slots
   int64_t** d_peers = nullptr;  // group exchange: device array of every rank's d_recv (IPC-mapped)
   std::vector<void*> ipc_mapped;
@@ -189,6 +195,7 @@ class Model {
  private:
   struct Raw {  // per-k outcome of one device pass
     bool penalty = false;
+    bool wide = false;  // chunk sums beyond the fixed-point digits (value from wide_value)
     double value = 0;
     int64_t fx[6] = {0, 0, 0, 0, 0, 0};
   };
@@ -197,6 +204,7 @@ class Model {
   void run(const double* params, int K, std::vector<Raw>& out, bool partial_only);
   void launch_graphs(const double* params, int K);
   void wait_results(int K, std::vector<Raw>& out, bool partial_only);
+  double wide_value(int k);
   cudaGraphExec_t graph_for(Shard& s, int K);
   Args base_args(Shard& s, int K);
   void build_tasks(uint32_t grid_points);

@@ -339,3 +339,48 @@ def test_c5_boundary_decisions_match_oracle():
     assert bm.log_floor_count() == o.floor_count() > 0
     assert close(got, want), (got, want)
 
+
+
+def test_c4_batch_is_bitwise_sequential():
+    """Convolution models stage the per-call state in shared memory (K x S
+    must fit); a batch of parameter sets, including a resolution width that
+    disables the term recurrence, equals the sequential calls bit for bit"""
+    W = WORKLOADS["C4"]
+    obs, pdf = W.build(pf)
+    ds = W.data(pf, obs, 3000, seed=5)
+    bm = pf.BoundModel(pdf, ds, pf.GridSpec(W.grid))
+    names = [p.name for p in bm.registry().parameters()]
+    pts = [W.start, W.truth, dict(m=2.9, w=0.35, rm=0.01, rs=0.06), dict(m=3.1, w=0.15, rm=-0.02, rs=0.0001)]
+    P = np.array([[pt[n] for n in names] for pt in pts])
+    batch = bm.eval_metric_batch(P, pf.MetricKind.ChiSquared)
+    seq = np.array([bm.eval_metric(list(p), pf.MetricKind.ChiSquared) for p in P])
+    assert np.array_equal(batch, seq)
+    ref = oracle.Reference(pdf, ds, W.grid) if oracle.Reference.available() else oracle.Oracle(pdf, ds, W.grid)
+    for p, got in zip(P, batch):
+        assert close(got, ref.eval(list(p), 1)), (p, got)
+
+
+def test_c4_wide_sums_and_nonfinite_index_match_reference():
+    """chi-squared far from the data: chunk sums beyond 2^62 go through the
+    wide accumulator (value still the reference's), and a non-finite term
+    reports the reference's first offending bin (engine.hpp:210-216)"""
+    W = WORKLOADS["C4"]
+    obs, pdf = W.build(pf)
+    ds = W.data(pf, obs, 3000, seed=5)
+    bm = pf.BoundModel(pdf, ds, pf.GridSpec(W.grid))
+    ref = oracle.Reference(pdf, ds, W.grid) if oracle.Reference.available() else oracle.Oracle(pdf, ds, W.grid)
+    wide = [2.5, 0.05, 0.2, 0.0001]
+    got = bm.eval_metric(wide, pf.MetricKind.ChiSquared)
+    want = ref.eval(wide, 1)
+    assert want > 2.0 ** 64 and close(got, want), (got, want)
+    truth = [W.truth[p.name] for p in bm.registry().parameters()]
+    batch = bm.eval_metric_batch(np.array([wide, truth]), pf.MetricKind.ChiSquared)
+    assert batch[0] == got and close(batch[1], ref.eval(truth, 1))
+    bad = [3.5, 0.05, -0.2, 1e-5]
+    with pytest.raises(Exception) as want_err:
+        ref.eval(bad, 1)
+    with pytest.raises(pf.Error) as got_err:
+        bm.eval_metric(bad, pf.MetricKind.ChiSquared)
+    assert str(got_err.value) == str(want_err.value)
+    # the wide digits were reset: the next call is the plain one again
+    assert bm.eval_metric(truth, pf.MetricKind.ChiSquared) == batch[1]
