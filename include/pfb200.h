@@ -204,7 +204,11 @@ PF_API int pf_eval_metric_batch(pf_model* model, const double* params, size_t k,
 
 /* The metric is accumulated EXACTLY in a fixed-point superaccumulator of
  * PF_FX_DIGITS signed 64-bit digits (value = sum_i d_i 2^(32 i - 128)) and
- * rounded once, so it does not depend on summation order or sharding. */
+ * rounded once, so it does not depend on summation order or sharding.
+ * Chunk sums of 2^62 or more (chi-squared far from the data) go to a wider
+ * device-side accumulator that pf_eval_metric / pf_eval_metric_batch fold in
+ * on the host; the partial and exchange-group paths carry only the six
+ * digits and fail such a call with "metric-overflow". */
 #define PF_FX_DIGITS 6
 
 /* This process's shard accumulator (PF_FX_DIGITS digits), for multi-process
@@ -217,7 +221,8 @@ PF_API int pf_eval_partial(pf_model* model, const double* params, size_t n_param
  * at once (*penalty set, nothing enqueued, when the parameters are invalid).
  * The event pass also writes a device record of 8 int64 at
  * pf_model_partial_device(): the PF_FX_DIGITS exact digits, the norm error
- * word (~0u when none) and a nonzero flag on a non-finite term or event error.
+ * word (~0u when none) and a flag word: bit 0 a non-finite term or event
+ * error, bit 1 chunk sums beyond the six digits (see PF_FX_DIGITS).
  * A collective enqueued on pf_model_stream() (cudaStream_t as an integer)
  * after the launch sees the record. */
 PF_API int pf_eval_launch(pf_model* model, const double* params, size_t n_params, int32_t metric,
