@@ -384,3 +384,22 @@ def test_c4_wide_sums_and_nonfinite_index_match_reference():
     assert str(got_err.value) == str(want_err.value)
     # the wide digits were reset: the next call is the plain one again
     assert bm.eval_metric(truth, pf.MetricKind.ChiSquared) == batch[1]
+
+
+def test_c4_wide_sums_on_the_partial_path_raise_metric_overflow():
+    """the cross-process partials carry only the six fixed-point digits: a
+    shard whose chunk sums leave their range fails loudly (metric-overflow)
+    instead of returning a wrong partial; in-range calls stay exact"""
+    W = WORKLOADS["C4"]
+    obs, pdf = W.build(pf)
+    ds = W.data(pf, obs, 3000, seed=5)
+    ref = oracle.Reference(pdf, ds, W.grid) if oracle.Reference.available() else oracle.Oracle(pdf, ds, W.grid)
+    shards = [pf.BoundModel(pdf, ds, pf.GridSpec(W.grid), shard_index=r, shard_count=2) for r in range(2)]
+    truth = [W.truth[p.name] for p in shards[0].registry().parameters()]
+    parts = [bm.eval_partial(truth, pf.MetricKind.ChiSquared)[0] for bm in shards]
+    assert close(pf.combine_partials(parts), ref.eval(truth, 1))
+    with pytest.raises(pf.Error, match="metric-overflow"):
+        for bm in shards:
+            bm.eval_partial([2.5, 0.05, 0.2, 0.0001], pf.MetricKind.ChiSquared)
+    parts2 = [bm.eval_partial(truth, pf.MetricKind.ChiSquared)[0] for bm in shards]
+    assert [list(p) for p in parts2] == [list(p) for p in parts]
