@@ -116,7 +116,7 @@ def peaks():
         return 6650.0, "fallback"
 
 
-NCU_TAGS = ("r1l", "r1j", "r1i", "r1h", "r1g", "r1f", "r1e")  # newest first
+NCU_TAGS = ("r1m", "r1l", "r1j", "r1i", "r1h", "r1g", "r1f", "r1e")  # newest first
 
 
 def ncu_summary_path(config):
