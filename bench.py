@@ -156,43 +156,98 @@ def ncu_traffic(config):
     return total
 
 
-def cpu_side(W, pf, obs, pdf, cols, metric, fit=True, steps=3):
-    """The reference (oracle/_ref, all host threads) — or, for ArgusPdf
-    models it cannot express, the C restatement (oracle port, one thread) —
-    on a bounded sample of the same workload: per-call throughput and one
-    full fit from the start point."""
+def workload_config(W, n_local, n_total, world, exchange=None):
+    """the `config` dict of BOTH arms (ours and --impl reference): byte-identical
+    for the same workload and GPU count"""
+    return {"workload": f"{W.name}: {W.description}, {n_local} {W.unit}/GPU, grid {W.grid}, "
+                        f"params at the fit start",
+            f"{W.unit}_per_gpu": n_local, f"global_{W.unit}": n_total,
+            "data": data_description(W),
+            "l2": "flushed (256 MiB device write) before every timed step",
+            "parallelism": f"dp{world}",
+            "exchange": exchange}
+
+
+def data_description(W):
+    if W.name == "C2":
+        return ("reference generate_events(AddPdf at truth m=5 s=0.8 a=-0.6 f=0.3, seed 11 + rank) "
+                "(generate.hpp:33-86; GPU arm: the bit-identical GPU generator)")
+    return f"synthetic ({W.name}, numpy PCG64 seed 11 + rank; {W.description})"
+
+
+def _at_truth(W, pf):
+    obs, pdf = W.build(pf)
+    for v in pf.GraphDesc(pdf, obs).vars:
+        if v.name in W.truth:
+            v.value = W.truth[v.name]
+    return obs, pdf
+
+
+def workload_columns(W, pf, n, seed, device=None):
+    """the event columns of a workload.  C2: the reference's own generator
+    (generate.hpp:33-86, mt19937_64 seed) at the truth point -- on the GPU for
+    our arm (pf.generate_events reproduces the reference stream bit for bit,
+    tests/test_gpu_generate.py), oracle/_ref's generate_events for the
+    reference arm; the other configs: numpy (workloads.py)."""
+    if W.name != "C2":
+        return W.columns(n, seed=seed)
+    obs, pdf = _at_truth(W, pf)
+    if device is None:
+        import oracle
+        return oracle.ref_generate(pdf, obs, n, seed, W.grid)
+    ds = pf.generate_events(pdf, obs, n, seed, pf.GridSpec(W.grid), device=device)
+    return np.ascontiguousarray(pf.to_event_table(ds)[0])
+
+
+def cpu_side(W, pf, obs, pdf, ds_full, metric, gpu_value=None, steps=3):
+    """The CPU legs, rank 0 at N = 1 (test infrastructure: oracle/ only as the
+    checker and the CPU baseline, never as the measured path):
+      cpu_baseline -- the reference (oracle/_ref, all host threads) or, for
+                      the PDFs it cannot express (ArgusPdf, DalitzPlotPdf),
+                      the C restatement with its event loop on all host
+                      threads, timed on a bounded sample of the same data;
+      parity       -- ONE evaluation of the same (reference or port) on the
+                      FULL benchmarked data at the benchmarked parameters,
+                      against the GPU's metric value (north_star bar: 1e-12)."""
     import oracle
     threads = os.cpu_count() or 1
+    n_full = ds_full.n_bins() if W.unit == "bins" else ds_full.n_events()
     if W.unit == "bins":
-        sample = min(cols.shape[-1], 100_000)
-        ds = W.data(pf, obs, sample)
+        sample = min(n_full, 100_000)
+        ds = W.data(pf, obs, sample) if sample < n_full else ds_full
     else:
-        sample = min(cols.shape[-1], 2_000_000 if W.name != "C5" else 200_000)
-        ds = pf.UnbinnedDataSet.from_columns(obs, cols[..., :sample])
+        sample = min(n_full, 2_000_000)
+        ds = ds_full if sample == n_full else pf.UnbinnedDataSet.from_columns(
+            obs, np.ascontiguousarray(pf.to_event_table(ds_full)[:, :sample]))
     use_ref = oracle.Reference.available() and W.has_reference
-    if use_ref:
-        kind, ev = "reference", oracle.Reference(pdf, ds, W.grid)
-        call = lambda p: ev.eval(p, metric, threads)  # noqa: E731
-    else:
-        kind, ev, threads = "port", oracle.Oracle(pdf, ds, W.grid), 1
-        call = lambda p: ev.eval(p, metric)  # noqa: E731
+    make = (lambda d: oracle.Reference(pdf, d, W.grid)) if use_ref else (lambda d: oracle.Oracle(pdf, d, W.grid))
+    kind = "reference" if use_ref else "port"
+    ev = make(ds)
+    call = lambda e, p: e.eval(p, metric, threads)  # noqa: E731
     p0 = [W.start[n] for n in ev.param_names()]
-    call(p0)
+    call(ev, p0)
     t = time.perf_counter()
     for k in range(steps):
         p = list(p0)
         p[0] += 1e-9 * (k + 1)  # jitter: the normalisation recomputes, as in FD probes
-        call(p)
+        call(ev, p)
     dt = (time.perf_counter() - t) / steps
     out = {"value": sample / dt, "unit": f"{W.unit}/s", "cores": threads, "kind": kind,
-           "sample": f"{sample} {W.unit} of the same synthetic data, {steps} eval_metric calls "
-                     f"({W.name}, grid {W.grid}), params jittered 1e-9 per call",
+           "sample": f"{sample} {W.unit} of the same data, {steps} eval_metric calls "
+                     f"({W.name}, grid {W.grid}), params jittered 1e-9 per call, {threads} host threads"
+                     + (" (Backend::with_threads)" if use_ref else " (C restatement, event loop threaded)"),
            "evals_per_s": 1.0 / dt, "ms_per_eval": dt * 1e3}
-    if fit and use_ref:
-        r = ev.fit(metric, threads)
-        out["fit"] = {"wall_s": r["wall_time_s"], "calls": int(r["calls"]), "status": int(r["status"]),
-                      "units": sample}
-    return out, ds
+    parity = None
+    if gpu_value is not None:
+        del ev
+        full = make(ds_full) if ds is not ds_full else make(ds)
+        t = time.perf_counter()
+        ref_value = call(full, p0)
+        parity = {"ref_value": ref_value, "gpu_value": gpu_value,
+                  "rel": abs(gpu_value - ref_value) / max(abs(ref_value), 1e-300),
+                  "units": n_full, "kind": kind, "ref_s": time.perf_counter() - t,
+                  "bar": 1e-12}
+    return out, parity
 
 
 def fit_leg(W, pf, obs, pdf, cols, device):
@@ -223,8 +278,33 @@ def fit_leg(W, pf, obs, pdf, cols, device):
     return out
 
 
+def sizes(W, args, world, rank):
+    """(events or bins on this rank, total over ranks)"""
+    if W.scaling == "weak":
+        n_local = args.events or W.default_n
+        return n_local, n_local * world
+    n_total = args.events or W.default_n
+    return n_total // world + (1 if rank < n_total % world else 0), n_total
+
+
+def exchange_description(args, multi):
+    if not multi:
+        return None
+    if args.exchange == "p2p":
+        return ("p2p: exact digit records stored over NVLink into every rank's buffer by the event pass "
+                "(CUDA IPC), summed on device")
+    return "nccl: device records all-gathered on the model stream"
+
+
 def run_reference(args):
-    """--impl reference: the reference's BoundModel::eval_metric on host cores."""
+    """--impl reference: the reference's BoundModel::eval_metric on host cores.
+
+    Only the reference (oracle/_ref/libparfit_ref.so, compiled from the
+    unmodified headers) or, for PDFs the reference lacks, the C restatement
+    runs here: libpfb200.so is never loaded in this process (the product's
+    ctypes binding is lazy and only the pure-Python model description is
+    used)."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -235,41 +315,50 @@ def run_reference(args):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libparfit_ref.so not built"}))
         return
     obs, pdf = W.build(pf)
-    n = args.events or W.default_n
+    n_local, n_total = sizes(W, args, world, rank)
+    n = n_local
     if W.unit == "bins":
-        n = min(n, 100_000)  # one reference chi-squared call on 1e6 bins x Q=1024 takes ~7 s on 8 threads
+        n = min(n, 100_000)  # one reference chi-squared call on 1e6 bins x Q=1024 takes ~5 s on 16 threads
     elif not W.has_reference:
-        n = min(n, 2_000_000 if W.name == "C3" else 200_000)
-    ds = W.data(pf, obs, n)
+        n = min(n, 2_000_000)
+    if W.unit == "bins":
+        ds = W.data(pf, obs, n)
+    else:
+        ds = pf.UnbinnedDataSet.from_columns(obs, workload_columns(W, pf, n, 11))
     threads = os.cpu_count() or 1
     if not W.has_reference:  # ArgusPdf / DalitzPlotPdf: the C restatement stands in
-        kind, ev, threads = "port", oracle.Oracle(pdf, ds, W.grid), 1
-        call = lambda p: ev.eval(p, W.metric)  # noqa: E731
+        kind, ev = "port", oracle.Oracle(pdf, ds, W.grid)
+        call = lambda p: ev.eval(p, W.metric, threads)  # noqa: E731
     else:
         kind, ev = "reference", oracle.Reference(pdf, ds, W.grid)
         call = lambda p: ev.eval(p, W.metric, threads)  # noqa: E731
     p0 = [W.start[nm] for nm in ev.param_names()]
+    metric_value = call(p0)
     for _ in range(args.warmup):
         call(p0)
     t = time.perf_counter()
     for k in range(args.steps):
         p = list(p0)
-        p[0] += 1e-9 * (k + 1)
+        p[0] += 1e-9 * (k + 1)  # jitter: the normalisation recomputes, as in FD probes
         call(p)
     dt = (time.perf_counter() - t) / args.steps
     val = n / dt
     metric_name = "NLL events/sec" if W.metric == 0 else "chi2 bins/sec"
+    sample = (f"{n} {W.unit} (rank 0's data{'' if n == n_local else ', a bounded prefix'}), "
+              f"{args.steps} eval_metric calls, params jittered 1e-9 per call")
     line = {
         "impl": "reference", "metric": metric_name, "value": val, "unit": f"{W.unit}/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
         "higher_is_better": True, "scaling": W.scaling, "vs_baseline": None, "dtype": "f64",
-        "data": f"synthetic ({W.name}, numpy PCG64 seed 11)",
-        "config": {"workload": f"{W.name}: {W.description}, {n} {W.unit}, grid {W.grid}",
-                   "parallelism": f"{threads} host threads" + (" (Backend::with_threads)" if kind == "reference"
-                                                                else " (C restatement)")},
+        "data": data_description(W),
+        "config": workload_config(W, n_local, n_total, world,
+                                  exchange_description(args, world > 1 or args.force_exchange)),
         "evals_per_s": 1.0 / dt,
+        "metric_value": metric_value, "metric_value_units": n,
         "cpu_baseline": {"value": val, "unit": f"{W.unit}/s", "cores": threads, "kind": kind,
-                         "sample": f"{n} {W.unit}, {args.steps} eval_metric calls"},
+                         "sample": sample,
+                         "threads": f"{threads} host threads" + (" (Backend::with_threads)" if kind == "reference"
+                                                                  else " (C restatement, event loop threaded)")},
         "e2e": {"value": val, "unit": f"{W.unit}/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -311,19 +400,14 @@ def main():
 
     from paper_1311_1753_b200 import parfit as pf
     obs, pdf = W.build(pf)
-    if W.scaling == "weak":
-        n_local = args.events or W.default_n
-        n_total = n_local * world
-    else:
-        n_total = args.events or W.default_n
-        n_local = n_total // world + (1 if rank < n_total % world else 0)
+    n_local, n_total = sizes(W, args, world, rank)
     # every rank owns its own events (seed per rank); the exact digits of the
     # ranks' partial sums are combined, so the order of combination is free
     if W.unit == "bins":
         ds = W.data(pf, obs, n_local, seed=11 + rank)
         cols = None
     else:
-        cols = W.columns(n_local, seed=11 + rank)
+        cols = workload_columns(W, pf, n_local, 11 + rank, device=local)
         ds = pf.UnbinnedDataSet.from_columns(obs, cols)
     bm = pf.BoundModel(pdf, ds, pf.GridSpec(W.grid), pf.Backend.gpus(1, local))
     params = W.params(bm)
@@ -463,15 +547,8 @@ def main():
         "metric": metric_name, "value": n_total / (ms_step * 1e-3), "unit": f"{W.unit}/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
         "higher_is_better": True, "scaling": W.scaling, "vs_baseline": None, "dtype": "f64",
-        "data": f"synthetic ({W.name}, numpy PCG64 seed 11 + rank; {W.description})",
-        "config": {"workload": f"{W.name}: {W.description}, {n_local} {W.unit}/GPU, grid {W.grid}, "
-                               f"params at the fit start",
-                   f"{W.unit}_per_gpu": n_local, f"global_{W.unit}": n_total,
-                   "l2": "flushed (256 MiB device write) before every timed step",
-                   "parallelism": f"dp{world}",
-                   "exchange": (("p2p: exact digit records stored over NVLink into every rank's buffer by "
-                                 "the event pass (CUDA IPC), summed on device") if args.exchange == "p2p" else
-                                "nccl: device records all-gathered on the model stream") if multi else None},
+        "data": data_description(W),
+        "config": workload_config(W, n_local, n_total, world, exchange_description(args, multi)),
         "evals_per_s": 1e3 / ms_step,
         "metric_value": value,
         "gpu_launches": int(launches),
@@ -506,9 +583,7 @@ def main():
         line["fit"] = fit_leg(W, pf, obs, pdf, cols, local)
     if world == 1 and not args.no_cpu_baseline:
         try:
-            if cols is None:
-                cols = np.zeros((1, n_local))  # binned: the sample is regenerated
-            line["cpu_baseline"], _ = cpu_side(W, pf, obs, pdf, cols, W.metric, fit=False)
+            line["cpu_baseline"], line["parity"] = cpu_side(W, pf, obs, pdf, ds, W.metric, gpu_value=value)
         except Exception as e:  # the baseline is reported, never required
             line["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
     print(json.dumps(line))

@@ -42,6 +42,9 @@ def _olib():
         L.po_eval.restype = C.c_int
         L.po_eval.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.c_size_t, C.c_int,
                               C.POINTER(C.c_double), C.c_char_p]
+        L.po_eval_mt.restype = C.c_int
+        L.po_eval_mt.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.c_size_t, C.c_int, C.c_int,
+                                 C.POINTER(C.c_double), C.c_char_p]
         L.po_n_params.argtypes = [C.c_void_p]
         L.po_param_variable.argtypes = [C.c_void_p, C.c_int]
         L.po_n_nodes.argtypes = [C.c_void_p]
@@ -140,11 +143,12 @@ class Oracle:
         return [self.desc.vars[self.L.po_param_variable(self.h, i)].name
                 for i in range(self.L.po_n_params(self.h))]
 
-    def eval(self, params, metric=0):
+    def eval(self, params, metric=0, threads=1):
+        """threads > 1: the event loop on that many POSIX threads (bit-identical)"""
         p = np.ascontiguousarray(params, dtype=np.float64)
         out = C.c_double()
         err = C.create_string_buffer(512)
-        if self.L.po_eval(self.h, _dp(p), p.size, metric, C.byref(out), err):
+        if self.L.po_eval_mt(self.h, _dp(p), p.size, metric, int(threads), C.byref(out), err):
             raise OracleError(err.value.decode())
         return out.value
 

@@ -17,6 +17,7 @@
  */
 #include <math.h>
 #include <stdint.h>
+#include <pthread.h>
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
@@ -578,8 +579,57 @@ void po_norms(void* h, double* norms, double* errs, int* valid, int n) {
   }
 }
 
-/* BoundModel::eval_metric (engine.hpp:165-218) */
-int po_eval(void* h, const double* p, size_t n, int metric, double* out, char* err) {
+/* The event loop of eval_metric (engine.hpp:184-209) over events [lo, hi) on
+   a private copy of the model state: raw() bumps clamp counters and records
+   errors in the model, so every worker thread owns a copy of the node array
+   and error slot; terms go to disjoint slots of the shared terms array.  The
+   reduce stays serial and in the reference's fixed order, so the result does
+   not depend on the thread count. */
+typedef struct {
+  omodel mc;             /* private copy (nodes copied too) */
+  const double* p;
+  int metric;
+  double norm;
+  uint64_t lo, hi;
+  uint64_t floors;
+  uint64_t err_event;    /* first erroring event, or UINT64_MAX */
+} po_work;
+
+static void* po_event_range(void* arg) {
+  po_work* w = arg;
+  omodel* m = &w->mc;
+  double* evt = calloc((size_t)m->ncols + 1, sizeof(double));
+  const int nc = m->ndata + (m->binned ? 2 : 0);
+  w->floors = 0;
+  w->err_event = UINT64_MAX;
+  for (uint64_t e = w->lo; e < w->hi; ++e) {
+    for (int c = 0; c < nc; ++c) evt[c] = m->values[(uint64_t)c * m->n + e];
+    if (w->metric == PF_NLL) {
+      double v = raw(m, 0, evt, w->p) / w->norm;
+      if (v < KLOGFLOOR) {
+        v = KLOGFLOOR;
+        w->floors++;
+      }
+      m->terms[e] = -log(v);
+    } else {
+      double content = evt[m->ndata], volume = evt[m->ndata + 1];
+      double mu = m->total * (raw(m, 0, evt, w->p) / w->norm) * volume;
+      double diff = content - mu;
+      m->terms[e] = diff * diff / (mu > KCHISQEPS ? mu : KCHISQEPS);
+    }
+    if (m->err_code) {
+      w->err_event = e;
+      break;
+    }
+  }
+  free(evt);
+  return NULL;
+}
+
+/* BoundModel::eval_metric (engine.hpp:165-218); threads > 1 splits the event
+   loop over that many POSIX threads (the reference's Backend::with_threads,
+   engine.hpp:98-130), bit-identical to threads = 1 */
+int po_eval_mt(void* h, const double* p, size_t n, int metric, int threads, double* out, char* err) {
   omodel* m = h;
   m->err_code = 0;
   m->err_msg[0] = 0;
@@ -605,31 +655,43 @@ int po_eval(void* h, const double* p, size_t n, int metric, double* out, char* e
     *out = KPENALTY;
     return 0;
   }
-  const double norm = m->nodes[0].norm;
-  double* evt = calloc((size_t)m->ncols + 1, sizeof(double));
-  const int nc = m->ndata + (m->binned ? 2 : 0);
-  for (uint64_t e = 0; e < m->n; ++e) {
-    for (int c = 0; c < nc; ++c) evt[c] = m->values[(uint64_t)c * m->n + e];
-    if (metric == PF_NLL) {
-      double v = raw(m, 0, evt, p) / norm;
-      if (v < KLOGFLOOR) {
-        v = KLOGFLOOR;
-        m->floor_count++;
-      }
-      m->terms[e] = -log(v);
-    } else {
-      double content = evt[m->ndata], volume = evt[m->ndata + 1];
-      double mu = m->total * (raw(m, 0, evt, p) / norm) * volume;
-      double diff = content - mu;
-      m->terms[e] = diff * diff / (mu > KCHISQEPS ? mu : KCHISQEPS);
-    }
-    if (m->err_code) {
-      free(evt);
-      snprintf(err, 512, "%s", m->err_msg);
-      return 1;
-    }
+  if (threads < 1) threads = 1;
+  if ((uint64_t)threads > m->n / 4096 + 1) threads = (int)(m->n / 4096 + 1);
+  po_work* w = calloc((size_t)threads, sizeof(po_work));
+  pthread_t* tid = calloc((size_t)threads, sizeof(pthread_t));
+  for (int t = 0; t < threads; ++t) {
+    w[t].mc = *m;
+    w[t].mc.nodes = malloc(sizeof(onode) * (size_t)m->nn);
+    memcpy(w[t].mc.nodes, m->nodes, sizeof(onode) * (size_t)m->nn);
+    w[t].p = p;
+    w[t].metric = metric;
+    w[t].norm = m->nodes[0].norm;
+    w[t].lo = m->n * (uint64_t)t / (uint64_t)threads;
+    w[t].hi = m->n * (uint64_t)(t + 1) / (uint64_t)threads;
+    if (threads > 1) pthread_create(&tid[t], NULL, po_event_range, &w[t]);
   }
-  free(evt);
+  if (threads == 1) po_event_range(&w[0]);
+  else
+    for (int t = 0; t < threads; ++t) pthread_join(tid[t], NULL);
+  int rc = 0;
+  for (int t = 0; t < threads; ++t) {
+    m->floor_count += w[t].floors;
+  }
+  /* clamp counters: every copy started from the model's value */
+  for (int i = 0; i < m->nn; ++i) {
+    uint64_t tot = 0;
+    for (int t = 0; t < threads; ++t) tot += w[t].mc.nodes[i].clamp;
+    m->nodes[i].clamp = tot - (uint64_t)(threads - 1) * m->nodes[i].clamp;
+  }
+  for (int t = 0; t < threads && !rc; ++t)
+    if (w[t].err_event != UINT64_MAX) { /* the first error in event order */
+      snprintf(err, 512, "%s", w[t].mc.err_msg);
+      rc = 1;
+    }
+  for (int t = 0; t < threads; ++t) free(w[t].mc.nodes);
+  free(w);
+  free(tid);
+  if (rc) return 1;
   double r = po_reduce(m->terms, m->n);
   if (!isfinite(r)) {
     for (uint64_t e = 0; e < m->n; ++e)
@@ -642,6 +704,10 @@ int po_eval(void* h, const double* p, size_t n, int metric, double* out, char* e
   }
   *out = r;
   return 0;
+}
+
+int po_eval(void* h, const double* p, size_t n, int metric, double* out, char* err) {
+  return po_eval_mt(h, p, n, metric, 1, out, err);
 }
 
 /* raw/density of the root at explicit points (column-major, ncols_data) */

@@ -145,4 +145,30 @@ def _load():
     return lib
 
 
-lib = _load()
+class _LazyLib:
+    """libpfb200.so, dlopened on the first native call (not at import): the
+    pure-Python model and data description types (pdf trees, data sets,
+    GraphDesc) stay usable without mapping the product library, so the
+    reference arm of bench.py and the oracle never load it.  A missing
+    library still fails loudly, at the first call that needs it."""
+
+    _lib = None
+
+    def _get(self):
+        if _LazyLib._lib is None:
+            _LazyLib._lib = _load()
+        return _LazyLib._lib
+
+    def __getattr__(self, name):
+        return getattr(self._get(), name)
+
+    def __getitem__(self, name):
+        return self._get()[name]
+
+
+def loaded() -> bool:
+    """True once libpfb200.so has been dlopened by this process"""
+    return _LazyLib._lib is not None
+
+
+lib = _LazyLib()

@@ -1033,9 +1033,9 @@ class BoundModel:
                        and params.flags.c_contiguous) else np.ascontiguousarray(params, dtype=np.float64).ravel()
         if self._call is None:  # argument objects reused by every call (the hot path of a fit)
             out, info, st = C.c_double(), _abi.pf_eval_info(), _abi.pf_status()
-            self._call = (out, info, st, C.byref(out), C.byref(info), C.byref(st))
-        out, info, st, r_out, r_info, r_st = self._call
-        rc = _eval_fast(self._h, p.ctypes.data, p.size, int(metric), r_out, r_info, r_st)
+            self._call = (out, info, st, C.byref(out), C.byref(info), C.byref(st), _eval_fast_bound())
+        out, info, st, r_out, r_info, r_st, fn = self._call
+        rc = fn(self._h, p.ctypes.data, p.size, int(metric), r_out, r_info, r_st)
         self._evaluated()
         if rc:
             _raise(st)
@@ -1108,9 +1108,17 @@ class BoundModel:
 
 # pf_eval_metric bound a second time with plain-address arguments: the
 # per-call path of BoundModel.eval_metric skips ctypes pointer conversions
-_eval_fast = lib["pf_eval_metric"]
-_eval_fast.restype = C.c_int
-_eval_fast.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]
+_eval_fast_fn = None
+
+
+def _eval_fast_bound():
+    global _eval_fast_fn
+    if _eval_fast_fn is None:
+        fn = lib["pf_eval_metric"]
+        fn.restype = C.c_int
+        fn.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]
+        _eval_fast_fn = fn
+    return _eval_fast_fn
 
 
 def combine_partials(parts) -> float:

@@ -22,13 +22,11 @@ from paper_1311_1753_b200.workloads import WORKLOADS  # noqa: E402
 def test_cpu_side_leg(name):
     W = WORKLOADS[name]
     obs, pdf = W.build(pf)
-    if W.unit == "bins":
-        cols = np.zeros((1, 300))
-    else:
-        cols = W.columns(3000, seed=2)
-    out, _ = bench.cpu_side(W, pf, obs, pdf, cols, W.metric, fit=False, steps=1)
+    ds = W.data(pf, obs, 300 if W.unit == "bins" else 3000, seed=2)
+    out, parity = bench.cpu_side(W, pf, obs, pdf, ds, W.metric, gpu_value=1.0, steps=1)
     assert out["value"] > 0 and out["unit"] == f"{W.unit}/s"
     assert out["kind"] in ("reference", "port") and out["cores"] >= 1
+    assert parity["units"] == (300 if W.unit == "bins" else 3000) and np.isfinite(parity["ref_value"])
     if name == "C3":
         assert out["kind"] == "port"  # ArgusPdf: no reference code
 
@@ -47,3 +45,28 @@ def test_reference_arm_json(name):
         assert key in line, key
     assert line["impl"] == "reference" and line["value"] > 0
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["d2h_bytes_per_step"] == 0
+    assert np.isfinite(line["metric_value"])
+
+
+def test_reference_arm_never_maps_the_product_library():
+    """the reference arm times the reference alone: libpfb200.so must not be
+    mapped into its process (the product binding is lazy)"""
+    if not oracle.Reference.available():
+        pytest.skip("oracle/_ref not built")
+    code = ("import sys, runpy; sys.argv = ['bench.py', '--impl', 'reference', '--config', 'C2', "
+            "'--events', '3000', '--steps', '1', '--warmup', '0']; "
+            "runpy.run_path('bench.py', run_name='__main__'); "
+            "maps = open('/proc/self/maps').read(); "
+            "print('PRODUCT_MAPPED' if 'libpfb200' in maps else 'CLEAN', 'REF' if 'libparfit_ref' in maps else 'NOREF')")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr
+    assert r.stdout.strip().splitlines()[-1] == "CLEAN REF", r.stdout
+
+
+def test_both_arms_share_one_config_dict():
+    """the driver compares `config` of the two arms byte for byte"""
+    W = WORKLOADS["C2"]
+    a = json.dumps(bench.workload_config(W, 10_000_000, 10_000_000, 1, None), sort_keys=True)
+    b = json.dumps(bench.workload_config(W, *bench.sizes(W, bench.argparse.Namespace(events=0), 1, 0), 1, None),
+                   sort_keys=True)
+    assert a == b
