@@ -65,9 +65,20 @@ class _Builder:
         if r < 0.93:  # mapped over two halves of x
             mid = 0.5 * (x.lower + x.upper)
             return pf.mapped_pdf(self.name("m"), [x.lower, mid, x.upper], [self.leaf(x), self.leaf(x)])
-        return pf.convolution_pdf(self.name("c"), self.leaf(x, ("exp", "bw")),
+        # convolution: steep models (|alpha| sigma up to ~5, the regime where a
+        # fixed resolution window would drop the dominant terms) and
+        # polynomials that clamp inside the quadrature table
+        k = self.rng.choice(("steep", "bw", "poly"))
+        lo, hi = x.lower, x.upper
+        if k == "steep":
+            model = pf.exp_pdf(self.name("e"), x, self.par(-12.0, 6.0))
+        elif k == "poly":
+            model = pf.polynomial_pdf(self.name("q"), x, [self.par(-0.5, 1.5), self.par(-0.6, 0.3)])
+        else:
+            model = self.leaf(x, ("bw",))
+        return pf.convolution_pdf(self.name("c"), model,
                                   pf.gaussian_pdf(self.name("g"), x, self.par(-0.05, 0.05, 0.0),
-                                                  self.par(0.1, 0.4)), 32)
+                                                  self.par(0.05, 0.4)), int(self.rng.choice([32, 256])))
 
     def point(self, order):
         lookup = {v.name: (lo, hi) for v, lo, hi in self.defs}
@@ -115,3 +126,6 @@ def test_random_model_vs_oracle(seed):
             if valid[0]:
                 assert abs(nodes[0].cached_norm() - norms[0]) <= REL * abs(norms[0]), (seed, p)
         assert bm.log_floor_count() == want_model.floor_count()
+        for i, nd in enumerate(nodes):  # PolynomialPdf clamps, per raw call (pdf.hpp:313-316)
+            if isinstance(nd, pf.PolynomialPdf):
+                assert nd.clamp_count() == want_model.clamp_count(i), (seed, nd.name)

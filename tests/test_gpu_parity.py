@@ -229,6 +229,83 @@ def test_c4_binned_convolution_vs_reference():
         assert close(got, want), (pt, got, want)
 
 
+def _conv_model(alpha, sigma, lo=0.0, hi=10.0, q=1024, mean=0.0):
+    x = pf.new_observable("x", lo, hi)
+    a = pf.new_parameter("a", alpha, 0.1, -50, 50)
+    m = pf.new_parameter("rm", mean, 0.01, -1, 1)
+    s = pf.new_parameter("rs", sigma, 0.01, 0.01, 5)
+    return x, pf.convolution_pdf("cv", pf.exp_pdf("e", x, a), pf.gaussian_pdf("res", x, m, s), q)
+
+
+@pytest.mark.parametrize("alpha,sigma,hi", [(-10.0, 0.4, 10.0), (-20.0, 0.2, 10.0), (-10.0, 1.0, 20.0),
+                                            (-5.0, 0.3, 10.0), (8.0, 0.5, 10.0)])
+def test_conv_steep_model_vs_reference(alpha, sigma, hi):
+    """ConvolutionPdf sums all Q quadrature points (pdf.hpp:476-493).  A
+    lifetime (x) resolution model whose table spans e^100 needs far more than
+    a fixed +-9 sigma window (2e-7 per event at alpha = -10,
+    sigma = 0.4); the per-call window is chosen from the table's dynamic range
+    and checked per event.  Unbinned NLL and binned chi2, vs oracle/_ref."""
+    x, pdf = _conv_model(alpha, sigma, hi=hi)
+    rng = np.random.default_rng(5)
+    ds = pf.UnbinnedDataSet.from_columns([x], hi * rng.random(20011))
+    bm = pf.BoundModel(pdf, ds)
+    ref = oracle.Reference(pdf, ds) if oracle.Reference.available() else oracle.Oracle(pdf, ds)
+    p = bm.registry().export_values()
+    got, want = bm.eval_metric(p), ref.eval(p, 0)
+    assert close(got, want), (got, want, abs(got - want) / abs(want))
+    assert bm.log_floor_count() == ref.floor_count()
+    # binned chi2 of the same model (C4's metric)
+    b = pf.BinnedDataSet([x], [3001])
+    xc = (np.arange(3001) + 0.5) * hi / 3001
+    b.set_contents(np.floor(1e6 * np.exp(alpha * xc / 4) / np.exp(alpha * xc / 4).sum()) + 1)
+    bb = pf.BoundModel(pdf, b)
+    rb = oracle.Reference(pdf, b) if oracle.Reference.available() else oracle.Oracle(pdf, b)
+    got, want = bb.eval_metric(p, pf.MetricKind.ChiSquared), rb.eval(p, 1)
+    assert close(got, want), (got, want, abs(got - want) / abs(want))
+
+
+def test_conv_resolution_mean_far_outside_the_quadrature_range():
+    """x - m outside [L, U] by more than the window: every term is a far tail
+    (the reference still sums them, e^-50-scale, not 0)"""
+    x, pdf = _conv_model(-1.0, 0.05, hi=4.0, mean=0.9)
+    rng = np.random.default_rng(6)
+    ds = pf.UnbinnedDataSet.from_columns([x], 4.0 * rng.random(5003))
+    bm = pf.BoundModel(pdf, ds)
+    ref = oracle.Reference(pdf, ds) if oracle.Reference.available() else oracle.Oracle(pdf, ds)
+    p = bm.registry().export_values()
+    got, want = bm.eval_metric(p), ref.eval(p, 0)
+    assert close(got, want), (got, want)
+    assert bm.log_floor_count() == ref.floor_count()
+
+
+@pytest.mark.parametrize("binned", [False, True])
+def test_conv_polynomial_clamp_counter_per_raw_call(binned):
+    """PolynomialPdf counts every raw() that clamps (pdf.hpp:313-316); inside a
+    convolution the reference calls it for every (raw call, tau_j) pair, events
+    and normalisation grid points alike (pdf.hpp:484-491)"""
+    x = pf.new_observable("x", 0.0, 10.0)
+    c0 = pf.new_parameter("c0", 1.0, 0.1, -5, 5)
+    c1 = pf.new_parameter("c1", -0.15, 0.01, -5, 5)
+    m = pf.new_parameter("rm", 0.0, 0.01, -1, 1)
+    s = pf.new_parameter("rs", 0.3, 0.01, 0.01, 5)
+    poly = pf.polynomial_pdf("p", x, [c0, c1])
+    pdf = pf.convolution_pdf("cv", poly, pf.gaussian_pdf("res", x, m, s), 256)
+    rng = np.random.default_rng(7)
+    if binned:
+        ds = pf.BinnedDataSet([x], [1000])
+        ds.set_contents(np.floor(100 * rng.random(1000)) + 1)
+    else:
+        ds = pf.UnbinnedDataSet.from_columns([x], 6.0 * rng.random(4001))
+    bm = pf.BoundModel(pdf, ds)
+    ref = oracle.Reference(pdf, ds) if oracle.Reference.available() else oracle.Oracle(pdf, ds)
+    metric = 1 if binned else 0
+    for k in range(2):
+        p = bm.registry().export_values()
+        got, want = bm.eval_metric(p, pf.MetricKind(metric)), ref.eval(p, metric)
+        assert close(got, want), (got, want)
+        assert poly.clamp_count() == ref.clamp_count(1) > 0, (k, poly.clamp_count(), ref.clamp_count(1))
+
+
 def test_c5_dalitz_vs_oracle():
     """C5 shape: DalitzPlotPdf, 4 isobars, 2-D normalisation grid (128 here so
     the oracle's walk stays short).  No reference code: parity against the C
