@@ -361,10 +361,8 @@ constexpr int pf_unroll = PF_UNROLL;
 #define PF_STAGE (PF_NLOAD * PF_SUB)  // doubles per stage
 
 // One event's term for the rare-path rescans (errors / non-finite terms).
-__device__ __noinline__ pf_u32 pf_event_flags(const pf_args& a, int k, const double* st, int i,
-                                              double* v_out) {
-  const double* P = a.P + (pf_u64)k * PF_NP;
-  const double* S = a.S + (pf_u64)k * PF_SS;
+__device__ __noinline__ pf_u32 pf_event_flags(const pf_args& a, const double* P, const double* S,
+                                              const double* st, int i, double* v_out) {
   pf_ctx cx;
   cx.err = 0;
   pf_cnt cnt;  // scratch: rescans do not count clamps twice
@@ -380,13 +378,13 @@ __device__ __noinline__ pf_u32 pf_event_flags(const pf_args& a, int k, const dou
 
 // Rare path, out of line: the first event (in this lane's order) that raised
 // an error or produced a non-finite term is found by re-evaluating.
-__device__ __noinline__ void pf_rescan(const pf_args& a, int k, pf_u64 base, int lane,
-                                       const double* st, int n_valid, bool want_err) {
+__device__ __noinline__ void pf_rescan(const pf_args& a, int k, const double* P, const double* S,
+                                       pf_u64 base, int lane, const double* st, int n_valid, bool want_err) {
   for (int j = 0; j < PF_EPT; ++j) {
     const int i = 32 * j + lane;
     if (i >= n_valid) break;
     double v;
-    const pf_u32 err = pf_event_flags(a, k, st, i, &v);
+    const pf_u32 err = pf_event_flags(a, P, S, st, i, &v);
     if (want_err) {
       if (err) {
         atomicMin(&a.rec[k].first_event_error, ((a.event_offset + base + i) << 24) | (pf_u64)err);
@@ -532,10 +530,8 @@ __device__ __forceinline__ pf_lacc pf_lform_pack(const pf_lform& A) {
 // log form is unusable, e.g. a negative mixture coefficient).  The lane's
 // sub-chunk is recomputed with the reference's linear form for exactly those
 // events (engine.hpp:186-195: floor 1e-300 counted, non-finite index kept).
-__device__ __noinline__ pf_lacc pf_lane_fixup(const pf_args& a, int k, pf_u64 base, int lane,
-                                              const double* st, int n_valid) {
-  const double* P = a.P + (pf_u64)k * PF_NP;
-  const double* S = a.S + (pf_u64)k * PF_SS;
+__device__ __noinline__ pf_lacc pf_lane_fixup(const pf_args& a, int k, const double* P, const double* S,
+                                              pf_u64 base, int lane, const double* st, int n_valid) {
   pf_ctx cx;
   cx.err = 0;
   pf_cnt cnt;
@@ -567,8 +563,8 @@ __device__ __noinline__ pf_lacc pf_lane_fixup(const pf_args& a, int k, pf_u64 ba
       A.lsum += pf_log(v);
     }
   }
-  if (cx.err) pf_rescan(a, k, base, lane, st, n_valid, true);
-  if (bad) pf_rescan(a, k, base, lane, st, n_valid, false);
+  if (cx.err) pf_rescan(a, k, P, S, base, lane, st, n_valid, true);
+  if (bad) pf_rescan(a, k, P, S, base, lane, st, n_valid, false);
   if (floors) atomicAdd(&a.rec[k].floor_count, (pf_u64)floors);
   pf_cnt_flush(cnt, a.clamp);
   return pf_lform_pack(A);
@@ -588,8 +584,7 @@ __device__ __forceinline__ pf_fk pf_fk_get(const pf_args& a, int k) {
 template <bool FULL>
 __device__ __forceinline__ pf_lacc pf_stage_terms(const pf_args& a, int k, pf_u64 base, int lane,
                                                 const double* st, int n_valid, const pf_fk& K,
-                                                const double* S) {
-  const double* P = a.P + (pf_u64)k * PF_NP;
+                                                const double* P, const double* S) {
 #if !PF_BINNED && PF_LOGFORM
   pf_lform A;
   pf_lform_init(A);
@@ -640,7 +635,7 @@ __device__ __forceinline__ pf_lacc pf_stage_terms(const pf_args& a, int k, pf_u6
     allok = allok && ok;
     pf_lform_add(A, Lv, fac);
   }
-  if (!allok) return pf_lane_fixup(a, k, base, lane, st, FULL ? PF_SUB : n_valid);
+  if (!allok) return pf_lane_fixup(a, k, P, S, base, lane, st, FULL ? PF_SUB : n_valid);
   return pf_lform_pack(A);
 #else
   pf_ctx cx;
@@ -699,8 +694,8 @@ __device__ __forceinline__ pf_lacc pf_stage_terms(const pf_args& a, int k, pf_u6
     pf_prod_mul(acc, v);
 #endif
   }
-  if (cx.err) pf_rescan(a, k, base, lane, st, FULL ? PF_SUB : n_valid, true);
-  if (bad) pf_rescan(a, k, base, lane, st, FULL ? PF_SUB : n_valid, false);
+  if (cx.err) pf_rescan(a, k, P, S, base, lane, st, FULL ? PF_SUB : n_valid, true);
+  if (bad) pf_rescan(a, k, P, S, base, lane, st, FULL ? PF_SUB : n_valid, false);
   if (floors) atomicAdd(&a.rec[k].floor_count, (pf_u64)floors);
   pf_cnt_flush(cnt, a.clamp);
   pf_lacc x;
@@ -791,7 +786,7 @@ __device__ __noinline__ void pf_group_exchange(const pf_args& a, int k, int lane
 // the record straight into mapped host memory; one system fence, then the
 // completion words.  Used by the event pass's last block and by the publish
 // kernel of a shard without events (whose bins are zero).
-__device__ void pf_finalize_warp0(const pf_args& a, int lane) {
+__device__ void pf_finalize_warp0(const pf_args& a, int lane, const double* S0 = nullptr) {
   static_assert(PF_FX_BINS == 32, "one bin per lane of warp 0");
   {
     for (int k = 0; k < a.K; ++k) {
@@ -845,7 +840,7 @@ __device__ void pf_finalize_warp0(const pf_args& a, int lane) {
         o->first_event_error = evterr;
         o->norm_error = normerr;
       }
-      const double* S = a.S + (pf_u64)k * PF_SS;
+      const double* S = S0 ? S0 : a.S + (pf_u64)k * PF_SS;
       for (int i = lane; i < 3 * a.n_nodes; i += 32) a.hnorms[(pf_u64)k * 3 * a.n_nodes + i] = S[i];
 #if PF_NPOLY > 0
       if (k == a.K - 1)
@@ -940,20 +935,21 @@ extern "C" __global__ void __launch_bounds__(PF_EV_THREADS, PF_EVENT_MIN_BLOCKS)
     const int n_valid = full ? PF_SUB : (int)(a.n_local > base ? a.n_local - base : 0);
     for (int k = 0; k < a.K; ++k) {
       const pf_fk fk = k == 0 ? fk0 : pf_fk_get(a, k);
+      const double* Pk = a.P + (pf_u64)k * PF_NP;
       pf_lacc t;
 #ifdef PF_S_SMEM
       // separate instantiations, so the staged copy is read with LDS (the
       // pointer's address space is known), not generic loads
       if (a.s_smem) {
         const double* Sk = sS + (pf_u64)k * PF_SS;
-        t = full ? pf_stage_terms<true>(a, k, base, lane, my + s * PF_STAGE, n_valid, fk, Sk)
-                 : pf_stage_terms<false>(a, k, base, lane, my + s * PF_STAGE, n_valid, fk, Sk);
+        t = full ? pf_stage_terms<true>(a, k, base, lane, my + s * PF_STAGE, n_valid, fk, Pk, Sk)
+                 : pf_stage_terms<false>(a, k, base, lane, my + s * PF_STAGE, n_valid, fk, Pk, Sk);
       } else
 #endif
       {
         const double* Sk = a.S + (pf_u64)k * PF_SS;
-        t = full ? pf_stage_terms<true>(a, k, base, lane, my + s * PF_STAGE, n_valid, fk, Sk)
-                 : pf_stage_terms<false>(a, k, base, lane, my + s * PF_STAGE, n_valid, fk, Sk);
+        t = full ? pf_stage_terms<true>(a, k, base, lane, my + s * PF_STAGE, n_valid, fk, Pk, Sk)
+                 : pf_stage_terms<false>(a, k, base, lane, my + s * PF_STAGE, n_valid, fk, Pk, Sk);
       }
       double* slot = accs + k * PF_LACC_N * PF_EV_THREADS + threadIdx.x;
       if (!first) {

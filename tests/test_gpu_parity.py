@@ -306,6 +306,43 @@ def test_conv_polynomial_clamp_counter_per_raw_call(binned):
         assert poly.clamp_count() == ref.clamp_count(1) > 0, (k, poly.clamp_count(), ref.clamp_count(1))
 
 
+def _folded_poly_models():
+    x = pf.new_observable("x", 0.0, 4.0)
+    y = pf.new_observable("y", 0.0, 2.0)
+    c0 = pf.new_parameter("c0", 1.0, 0.1, -5, 5)
+    c1 = pf.new_parameter("c1", -0.4, 0.1, -5, 5)
+    a = pf.new_parameter("a", -1.0, 0.1, -5, 5)
+    b = pf.new_parameter("b", -0.5, 0.1, -5, 5)
+    f = pf.new_parameter("f", 0.5, 0.01, 0, 1)
+    g = pf.new_parameter("g", 0.3, 0.01, 0, 1)
+    poly = pf.polynomial_pdf("p", x, [c0, c1])
+    inner = pf.add_pdf("in", [poly, pf.exp_pdf("e", x, a)], [f])
+    yield "folded-add", pf.add_pdf("out", [inner, pf.exp_pdf("e2", x, b)], [g]), [x]
+    poly2 = pf.polynomial_pdf("p2", x, [c0, c1])
+    yield "separable-product", pf.prod_pdf("pr", [poly2, pf.exp_pdf("ey", y, b)]), [x, y]
+
+
+@pytest.mark.parametrize("case", ["folded-add", "separable-product"])
+def test_polynomial_clamps_under_folded_normalisations(case):
+    """the reference walks the grid of every normalised node, folded or not
+    (pdf.hpp:148-176), so a polynomial's clamps count once per reference raw
+    call on those grids too; this engine folds AddPdf / separable ProdPdf
+    norms from the children's sums and scales the children's counts"""
+    name, pdf, obs = [m for m in _folded_poly_models() if m[0] == case][0]
+    rng = np.random.default_rng(9)
+    ds = pf.UnbinnedDataSet.from_columns(obs, np.stack([o.lower + (o.upper - o.lower) * rng.random(3001)
+                                                        for o in obs]))
+    bm = pf.BoundModel(pdf, ds, pf.GridSpec(64))
+    ref = oracle.Reference(pdf, ds, 64) if oracle.Reference.available() else oracle.Oracle(pdf, ds, 64)
+    nodes = pf.GraphDesc(pdf, obs).preorder()
+    p = bm.registry().export_values()
+    got, want = bm.eval_metric(p), ref.eval(p, 0)
+    assert close(got, want), (got, want)
+    for i, nd in enumerate(nodes):
+        if isinstance(nd, pf.PolynomialPdf):
+            assert nd.clamp_count() == ref.clamp_count(i) > 0, (nd.name(), nd.clamp_count(), ref.clamp_count(i))
+
+
 def test_c5_dalitz_vs_oracle():
     """C5 shape: DalitzPlotPdf, 4 isobars, 2-D normalisation grid (128 here so
     the oracle's walk stays short).  No reference code: parity against the C
