@@ -98,6 +98,9 @@ struct pf_args {
   int npin;             // K = 1: parameters passed inline (pin[0..npin))
   int s_smem;            // S staged in the event pass's shared memory (models with conv tables)
   long long* big;       // K x PF_BIG_STRIDE: wide accumulator of chunk sums >= 2^62 (pf_big_add)
+  pf_u32* ticket;       // fused pass: dynamic chunk counter (self-resetting)
+  int fused;            // 1: this launch is the single fused kernel (setup in every CTA)
+  int pad1;
   double pin[PF_MAX_INLINE];
 };
 

@@ -79,23 +79,17 @@ __device__ __forceinline__ double pf_dsmem_load(const double* p, unsigned rank) 
   return v;
 }
 // ---------------------------------------------------------------------------
-// setup: call records, pre stage and EVERY normalisation level for one
-// parameter set in one thread-block cluster of PF_SETUP_CLUSTER CTAs (small
-// grids).  Midpoint sums at n and 2n (pdf.hpp:148-176): thread t of CTA c
-// sums points c * 512 + t, + 512 * PF_SETUP_CLUSTER, ... in double-double; a
-// fixed-shape block reduction gives each CTA's partial, and every CTA adds
-// the partials of all ranks (read over DSMEM) in rank order, so all CTAs hold
-// identical norms and stage constants for the next level.  Rank 0 writes the
-// per-call state to global memory for the event pass.
-extern "C" __global__ void __launch_bounds__(PF_SETUP_THREADS) pf_setup_kernel(const __grid_constant__ pf_args a) {
-  // parameters and the per-call state live in shared memory while the CTA
-  // works (every S read/write is an LDS/STS, not an L2 round trip); the task
-  // table is staged too.  The state is written to global memory at the end.
-  extern __shared__ __align__(16) double pf_sdyn[];
+// The setup work of one parameter set, shared by the setup kernel (a cluster
+// of CL CTAs splitting the grid points) and the fused kernel (every CTA
+// computes all of it, CL = 1): P and S in shared memory on return, identical
+// in every CTA.  Grid-point clamps go to `cnt`, stage clamps to `cnt_stage`.
+template <int CL>
+__device__ __forceinline__ void pf_setup_core(const pf_args& a, int k, unsigned rank, double* P, double* S,
+                                              pf_krec* r, bool init_rec, pf_ctx& cx, pf_cnt& cnt,
+                                              pf_cnt& cnt_stage) {
   // this CTA's warp partials per task, double-buffered by level parity
   __shared__ double wpart[2][PF_SETUP_MAXQ][PF_SETUP_THREADS / 32];
   __shared__ pf_task tk[16];
-  pf_pdl_trigger();  // let the event kernel start streaming its data now
 #ifdef PF_SETUP_TRACE
   __shared__ long long trs[32];
   __shared__ const char* trn[32];
@@ -105,13 +99,6 @@ extern "C" __global__ void __launch_bounds__(PF_SETUP_THREADS) pf_setup_kernel(c
 #else
 #define PF_TRACE(tag)
 #endif
-  const unsigned rank = PF_SETUP_CLUSTER > 1 ? pf_cluster_rank() : 0u;
-  const int k = blockIdx.x / PF_SETUP_CLUSTER;
-#ifdef PF_EVENT_TRACE
-  if (threadIdx.x == 0 && blockIdx.x == 0) pf_trace_buf[4095 * 6 + 0] = pf_gtime();
-#endif
-  double* P = pf_sdyn;
-  double* S = pf_sdyn + PF_NP;
   // K = 1: parameters arrive inline in the kernel arguments (constant bank,
   // updated per call on the instantiated graph); batches read mapped memory
   for (int i = threadIdx.x; i < PF_NP; i += blockDim.x)
@@ -120,18 +107,11 @@ extern "C" __global__ void __launch_bounds__(PF_SETUP_THREADS) pf_setup_kernel(c
   const int nt = min(a.n_tasks, 16);
   for (int i = threadIdx.x; i < nt * (int)(sizeof(pf_task) / 8); i += blockDim.x)
     reinterpret_cast<pf_u64*>(tk)[i] = reinterpret_cast<const pf_u64*>(a.tasks)[i];
-  pf_krec* r = a.rec + k;
-  if (threadIdx.x == 0 && rank == 0) pf_rec_init(r);
+  if (init_rec && threadIdx.x == 0 && rank == 0) pf_rec_init(r);
   pf_math_init();  // includes __syncthreads
   // the record is initialised before any CTA of the cluster reports into it
-  if (PF_SETUP_CLUSTER > 1) pf_cluster_sync();
+  if (CL > 1) pf_cluster_sync();
   PF_TRACE("init");
-  pf_ctx cx;
-  cx.err = 0;
-  pf_cnt cnt;        // clamps met on this CTA's grid points
-  pf_cnt_init(cnt);
-  pf_cnt cnt_stage;  // clamps met in the pre/post stages (every CTA runs them; rank 0 reports)
-  pf_cnt_init(cnt_stage);
   pf_stage_pre(k, P, S, a.C, cx, cnt_stage, threadIdx.x, blockDim.x);
   PF_TRACE("pre");
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -155,8 +135,7 @@ extern "C" __global__ void __launch_bounds__(PF_SETUP_THREADS) pf_setup_kernel(c
 #pragma unroll
     for (int q = 0; q < PF_SETUP_MAXQ; ++q) off[q + 1] = off[q] + (q < nl ? tk[t0 + q].points : 0ull);
 #pragma unroll 2
-    for (pf_u64 g = rank * PF_SETUP_THREADS + threadIdx.x; g < off[PF_SETUP_MAXQ];
-         g += PF_SETUP_THREADS * PF_SETUP_CLUSTER) {
+    for (pf_u64 g = rank * PF_SETUP_THREADS + threadIdx.x; g < off[PF_SETUP_MAXQ]; g += PF_SETUP_THREADS * CL) {
       int q = 0;
       pf_u64 first = 0;  // (constant indices only: off[] stays in registers)
 #pragma unroll
@@ -184,7 +163,7 @@ extern "C" __global__ void __launch_bounds__(PF_SETUP_THREADS) pf_setup_kernel(c
     // warp partials of every rank visible cluster-wide (double-buffered by
     // level parity: a rank cannot overwrite a buffer another rank may still
     // read without first passing the next level's barrier)
-    if (PF_SETUP_CLUSTER > 1)
+    if (CL > 1)
       pf_cluster_sync();
     else
       __syncthreads();
@@ -195,14 +174,13 @@ extern "C" __global__ void __launch_bounds__(PF_SETUP_THREADS) pf_setup_kernel(c
     if (2 * warp < nl) {
       const int q = 2 * warp + (lane >> 4);
       const double* src = &wpart[level & 1][q][lane & 15];
-      double v[PF_SETUP_CLUSTER];
+      double v[CL];
 #pragma unroll
-      for (int rk = 0; rk < PF_SETUP_CLUSTER; ++rk)
-        v[rk] = PF_SETUP_CLUSTER > 1 ? pf_dsmem_load(src, (unsigned)rk) : *src;
+      for (int rk = 0; rk < CL; ++rk) v[rk] = CL > 1 ? pf_dsmem_load(src, (unsigned)rk) : *src;
 #pragma unroll
-      for (int w = 1; w < PF_SETUP_CLUSTER; w <<= 1)
+      for (int w = 1; w < CL; w <<= 1)
 #pragma unroll
-        for (int rk = 0; rk + w < PF_SETUP_CLUSTER; rk += 2 * w) v[rk] += v[rk + w];
+        for (int rk = 0; rk + w < CL; rk += 2 * w) v[rk] += v[rk + w];
       double y = v[0];
 #pragma unroll
       for (int d = 8; d > 0; d >>= 1) y += __shfl_down_sync(0xffffffffu, y, d);
@@ -217,6 +195,42 @@ extern "C" __global__ void __launch_bounds__(PF_SETUP_THREADS) pf_setup_kernel(c
     PF_TRACE("post");
     t0 = t1;
   }
+#ifdef PF_SETUP_TRACE
+  if (threadIdx.x == 0 && blockIdx.x == 0)
+    for (int i = 0; i < ntr; ++i) printf("setup %-8s %lld\n", trn[i], trs[i]);
+#endif
+#undef PF_TRACE
+}
+
+// ---------------------------------------------------------------------------
+// setup: call records, pre stage and EVERY normalisation level for one
+// parameter set in one thread-block cluster of PF_SETUP_CLUSTER CTAs (small
+// grids).  Midpoint sums at n and 2n (pdf.hpp:148-176): thread t of CTA c
+// sums points c * 512 + t, + 512 * PF_SETUP_CLUSTER, ... ; a fixed-shape
+// block reduction gives each CTA's partial, and every CTA adds the partials
+// of all ranks (read over DSMEM) in rank order, so all CTAs hold identical
+// norms and stage constants for the next level.  Rank 0 writes the per-call
+// state to global memory for the event pass.
+extern "C" __global__ void __launch_bounds__(PF_SETUP_THREADS) pf_setup_kernel(const __grid_constant__ pf_args a) {
+  // parameters and the per-call state live in shared memory while the CTA
+  // works (every S read/write is an LDS/STS, not an L2 round trip)
+  extern __shared__ __align__(16) double pf_sdyn[];
+  pf_pdl_trigger();  // let the event kernel start streaming its data now
+  const unsigned rank = PF_SETUP_CLUSTER > 1 ? pf_cluster_rank() : 0u;
+  const int k = blockIdx.x / PF_SETUP_CLUSTER;
+#ifdef PF_EVENT_TRACE
+  if (threadIdx.x == 0 && blockIdx.x == 0) pf_trace_buf[4095 * 6 + 0] = pf_gtime();
+#endif
+  double* P = pf_sdyn;
+  double* S = pf_sdyn + PF_NP;
+  pf_krec* r = a.rec + k;
+  pf_ctx cx;
+  cx.err = 0;
+  pf_cnt cnt;        // clamps met on this CTA's grid points
+  pf_cnt_init(cnt);
+  pf_cnt cnt_stage;  // clamps met in the pre/post stages (every CTA runs them; rank 0 reports)
+  pf_cnt_init(cnt_stage);
+  pf_setup_core<PF_SETUP_CLUSTER>(a, k, rank, P, S, r, true, cx, cnt, cnt_stage);
   if (cx.err) atomicMin(&r->norm_error, cx.err);
   pf_cnt_flush(cnt, a.clamp);
   if (rank == 0) pf_cnt_flush(cnt_stage, a.clamp);
@@ -227,11 +241,6 @@ extern "C" __global__ void __launch_bounds__(PF_SETUP_THREADS) pf_setup_kernel(c
     for (int i = threadIdx.x; i < PF_SS; i += blockDim.x) gS[i] = S[i];
     for (int i = threadIdx.x; i < PF_NP; i += blockDim.x) gP[i] = P[i];
   }
-  PF_TRACE("store");
-#ifdef PF_SETUP_TRACE
-  if (threadIdx.x == 0 && blockIdx.x == 0)
-    for (int i = 0; i < ntr; ++i) printf("setup %-8s %lld\n", trn[i], trs[i]);
-#endif
 #ifdef PF_EVENT_TRACE
   if (threadIdx.x == 0 && blockIdx.x == 0) pf_trace_buf[4095 * 6 + 1] = pf_gtime();
 #endif
@@ -653,6 +662,9 @@ __device__ __forceinline__ pf_lacc pf_stage_terms(const pf_args& a, int k, pf_u6
 #pragma unroll pf_unroll
   for (int j = 0; j < PF_EPT; ++j) {
     const int i = 32 * j + lane;
+    // padding events (the column tail up to a whole chunk) are not evaluated:
+    // they would count clamps the reference never sees
+    if (!FULL && i >= n_valid) continue;
     double ev[PF_NCOLS];
 #pragma unroll
     for (int q = 0; q < PF_NCOLS; ++q) ev[q] = 0.0;
@@ -802,6 +814,12 @@ __device__ void pf_finalize_warp0(const pf_args& a, int lane, const double* S0 =
         nonfinite = __ldcg(&r->first_nonfinite);
         evterr = __ldcg(&r->first_event_error);
         normerr = __ldcg(&r->norm_error);
+        // self-resetting: the fused pass has no kernel that initialises it
+        pf_krec* rw = a.rec + k;
+        rw->floor_count = 0ull;
+        rw->first_nonfinite = ~0ull;
+        rw->first_event_error = ~0ull;
+        rw->norm_error = ~0u;
       }
 #pragma unroll
       for (int i = 0; i < PF_FX_DIGITS; ++i) bin[i] = 0ll;  // self-resetting
@@ -1037,6 +1055,146 @@ extern "C" __global__ void __launch_bounds__(PF_EV_THREADS, PF_EVENT_MIN_BLOCKS)
 #ifdef PF_EVENT_TRACE
   if (threadIdx.x == 0) pf_trace_buf[4094 * 6 + 2] = pf_gtime();
 #endif
+}
+
+
+// ---------------------------------------------------------------------------
+// Fused pass (K = 1, small normalisation grids): ONE kernel per call.  Every
+// CTA (one per SM, 16 warps) first issues the TMA copies of its warps' first
+// stages, then computes the whole setup (parameters, pre stage, every
+// normalisation level, post stage) in its own shared memory while those
+// copies are in flight -- the setup work is a few thousand raw evaluations,
+// cheaper to repeat per SM than to hand over through a second grid -- and
+// then streams its chunks.  Chunks (fixed event ranges: the reduction unit,
+// so the result does not depend on the schedule) are taken dynamically from
+// a self-resetting ticket counter, two ahead, so every warp of every SM stays
+// busy to the end.  Lane accumulators live in registers; one exact block
+// total per CTA; the last CTA rounds and publishes (pf_finalize_warp0).
+#ifndef PF_FUSED_WARPS
+#define PF_FUSED_WARPS 16
+#endif
+#define PF_FUSED_THREADS (32 * PF_FUSED_WARPS)
+
+extern "C" __global__ void __launch_bounds__(PF_FUSED_THREADS, 1) pf_fused_kernel(const __grid_constant__ pf_args a) {
+  static_assert(PF_FUSED_THREADS == PF_SETUP_THREADS, "the setup core strides by PF_SETUP_THREADS");
+  extern __shared__ __align__(16) unsigned char pf_dyn[];
+  __shared__ __align__(8) pf_u64 bars[PF_FUSED_WARPS * PF_NST];
+  __shared__ long long bfx[PF_FUSED_WARPS][PF_FX_DIGITS];
+  __shared__ int s_last;
+  double* stages = reinterpret_cast<double*>(pf_dyn);
+  double* P = stages + PF_FUSED_WARPS * PF_NST * PF_STAGE;
+  double* S = P + PF_NP;
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  double* my = stages + warp * PF_NST * PF_STAGE;
+  pf_u64* mybar = bars + warp * PF_NST;
+  const int nw = gridDim.x * PF_FUSED_WARPS;
+  const int gw = blockIdx.x * PF_FUSED_WARPS + warp;
+  const int nch = a.n_chunks;
+  // lane 0's chunk schedule: the current and next chunk, and the ticket for
+  // the one after (chunk ids >= nch mean "no more work")
+  int c_cur = gw, c_nxt = gw + nw, c_pend = nch;
+  if (lane == 0) {
+    for (int s = 0; s < PF_NST; ++s) pf_mbar_init(mybar + s, 1);
+    pf_fence_mbar_init();
+    if (c_nxt < nch) c_pend = 2 * nw + (int)atomicAdd(a.ticket, 1u);
+  }
+  // sub-chunk v of this warp (v / PF_NSUB chunks after the current one, 0 or 1)
+  auto issue = [&](int v, int vbase) {
+    if (lane == 0) {
+      const int c = (v / PF_NSUB) == vbase ? c_cur : c_nxt;
+      if (c < nch) {
+        const int st = v % PF_NST;
+        const pf_u64 base = (pf_u64)c * (PF_SUB * PF_NSUB) + (pf_u64)(v % PF_NSUB) * PF_SUB;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        pf_mbar_expect_tx(mybar + st, PF_STAGE * 8);
+#pragma unroll
+        for (int q = 0; q < PF_NLOAD; ++q)
+          pf_tma_load(my + st * PF_STAGE + q * PF_SUB, a.data + (pf_u64)pf_load_col(q) * a.col_stride + base,
+                      PF_SUB * 8, mybar + st);
+      }
+    }
+  };
+  static_assert(PF_NST <= PF_NSUB, "the fused ring runs at most one chunk ahead");
+  for (int v = 0; v < PF_NST; ++v) issue(v, 0);
+  // the setup, redundantly in every CTA, while the first stages stream in
+  pf_krec* r = a.rec;
+  pf_ctx cx;
+  cx.err = 0;
+  pf_cnt cnt_grid, cnt_stage;
+  pf_cnt_init(cnt_grid);
+  pf_cnt_init(cnt_stage);
+  pf_setup_core<1>(a, 0, 0u, P, S, r, false, cx, cnt_grid, cnt_stage);
+  if (blockIdx.x == 0) {  // one CTA reports what every CTA found
+    if (cx.err) atomicMin(&r->norm_error, cx.err);
+    pf_cnt_flush(cnt_grid, a.clamp);
+    pf_cnt_flush(cnt_stage, a.clamp);
+    double* gS = a.S;
+    double* gP = (double*)a.P;
+    for (int i = threadIdx.x; i < PF_SS; i += blockDim.x) gS[i] = S[i];
+    for (int i = threadIdx.x; i < PF_NP; i += blockDim.x) gP[i] = P[i];
+  }
+  __syncthreads();  // P and S complete (the setup core ends with a barrier too)
+  const pf_fk fk = pf_fk_load(P, S, a.C);
+  pf_fxl F;
+#pragma unroll
+  for (int i = 0; i < PF_FX_DIGITS; ++i) F.d[i] = 0;
+  long long* big = a.big;
+  pf_lacc acc;
+  int w = 0;  // sub-chunks consumed by this warp
+  while (__shfl_sync(0xffffffffu, c_cur, 0) < nch) {
+    const int c = __shfl_sync(0xffffffffu, c_cur, 0);
+    const int vb = w / PF_NSUB;
+    for (int j = 0; j < PF_NSUB; ++j, ++w) {
+      const int st = w % PF_NST;
+      pf_mbar_wait(mybar + st, (unsigned)((w / PF_NST) & 1));
+      const pf_u64 base = (pf_u64)c * (PF_SUB * PF_NSUB) + (pf_u64)j * PF_SUB;
+      const bool full = base + PF_SUB <= a.n_local;
+      const int n_valid = full ? PF_SUB : (int)(a.n_local > base ? a.n_local - base : 0);
+      const pf_lacc t = full ? pf_stage_terms<true>(a, 0, base, lane, my + st * PF_STAGE, n_valid, fk, P, S)
+                             : pf_stage_terms<false>(a, 0, base, lane, my + st * PF_STAGE, n_valid, fk, P, S);
+      acc = j == 0 ? t : pf_lacc_merge(acc, t);
+      __syncwarp();
+      issue(w + PF_NST, vb);  // refills the stage just read
+    }
+    // chunk done: its exact value into the lane's fixed-point accumulator
+    const pf_dd tv = pf_lacc_terms(acc, P);
+    pf_fxl_add_w(F, tv.hi, big);
+    pf_fxl_add_w(F, tv.lo, big);
+    if (lane == 0) {  // next chunk; take the ticket after it
+      c_cur = c_nxt;
+      c_nxt = c_pend;
+      c_pend = nch;
+      if (c_nxt < nch) c_pend = 2 * nw + (int)atomicAdd(a.ticket, 1u);
+    }
+  }
+  // block total (exact integer digits), ONE binned atomic set per CTA
+  pf_fxl_warp_sum(F);
+  if (lane == 0)
+#pragma unroll
+    for (int i = 0; i < PF_FX_DIGITS; ++i) bfx[warp][i] = F.d[i];
+  __syncthreads();
+  if (threadIdx.x < PF_FX_DIGITS) {
+    long long v = 0;
+#pragma unroll
+    for (int ww = 0; ww < PF_FUSED_WARPS; ++ww) v += bfx[ww][threadIdx.x];
+    if (v)
+      atomicAdd((unsigned long long*)(a.fxbins + (pf_u64)(blockIdx.x % PF_FX_BINS) * PF_FX_BIN_STRIDE + threadIdx.x),
+                (unsigned long long)v);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(a.done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (threadIdx.x == 0) {
+    *a.done = 0u;     // self-resetting (every CTA has arrived)
+    *a.ticket = 0u;   // every ticket has been taken and consumed
+  }
+  if (warp == 0) pf_finalize_warp0(a, lane, S);
 }
 
 // ---------------------------------------------------------------------------

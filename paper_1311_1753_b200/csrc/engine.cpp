@@ -70,6 +70,13 @@ size_t event_smem(const Layout& L, int K) {
   return bytes;
 }
 
+// fused kernel: every warp's TMA ring, then P and S of the one parameter set
+size_t fused_smem(const Layout& L) {
+  return static_cast<size_t>(kFusedWarps) * L.nst * L.load_cols.size() * 32 * static_cast<size_t>(L.ept) *
+             sizeof(double) +
+         sizeof(double) * (std::max(L.np, 1) + std::max(L.ss, 1));
+}
+
 size_t event_smem_max(const Layout& L) {
   size_t m = 0;
   for (int K = 1; K <= kMaxBatch; ++K) m = std::max(m, event_smem(L, K));
@@ -98,6 +105,7 @@ const Module* load_module(const Layout& L, int device) {
   ck(cudaLibraryGetKernel(&m->pre, m->lib, "pf_pre_kernel"), "get pf_pre_kernel");
   ck(cudaLibraryGetKernel(&m->norm, m->lib, "pf_norm_kernel"), "get pf_norm_kernel");
   ck(cudaLibraryGetKernel(&m->event, m->lib, "pf_event_kernel"), "get pf_event_kernel");
+  ck(cudaLibraryGetKernel(&m->fused, m->lib, "pf_fused_kernel"), "get pf_fused_kernel");
   if (L.source.rfind("#define PF_GEN 1\n", 0) == 0) {
     ck(cudaLibraryGetKernel(&m->gen_max, m->lib, "pf_gen_max_kernel"), "get pf_gen_max_kernel");
     ck(cudaLibraryGetKernel(&m->gen_mt, m->lib, "pf_mt_kernel"), "get pf_mt_kernel");
@@ -109,6 +117,10 @@ const Module* load_module(const Layout& L, int device) {
   ck(cudaKernelSetAttributeForDevice(m->event, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(event_smem_max(L)), device),
      "event kernel smem attribute");
+  if (fused_smem(L) <= 200 * 1024)
+    ck(cudaKernelSetAttributeForDevice(m->fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(fused_smem(L)), device),
+       "fused kernel smem attribute");
   c.modules.emplace(key, m);
   return m;
 }
@@ -316,6 +328,18 @@ Model::Model(const pf_graph& g, const pf_data& d, uint32_t grid_points, const pf
     ck(cudaMalloc(&sh.d_fxbins, bins), "cudaMalloc fxbins");
     ck(cudaMemset(sh.d_fxbins, 0, bins), "memset fxbins");
     ck(cudaMalloc(&sh.d_rec, sizeof(KRec) * kMaxBatch), "cudaMalloc rec");
+    {  // the records' reset state (pf_rec_init); every call's finalizer restores it
+      std::vector<KRec> init(kMaxBatch);
+      for (KRec& r : init) {
+        std::memset(&r, 0, sizeof r);
+        r.first_nonfinite = ~0ull;
+        r.first_event_error = ~0ull;
+        r.norm_error = ~0u;
+      }
+      ck(cudaMemcpy(sh.d_rec, init.data(), sizeof(KRec) * kMaxBatch, cudaMemcpyHostToDevice), "init rec");
+    }
+    ck(cudaMalloc(&sh.d_ticket, sizeof(uint32_t)), "cudaMalloc ticket");
+    ck(cudaMemset(sh.d_ticket, 0, sizeof(uint32_t)), "memset ticket");
     ck(cudaMalloc(&sh.d_clamp, sizeof(uint64_t) * 2 * std::max(L_.n_poly, 1)), "cudaMalloc clamp");
     ck(cudaMemset(sh.d_clamp, 0, sizeof(uint64_t) * 2 * std::max(L_.n_poly, 1)), "memset clamp");
     ck(cudaHostAlloc(reinterpret_cast<void**>(&sh.h_out), sizeof(Out) * kMaxBatch, cudaHostAllocMapped),
@@ -373,6 +397,7 @@ Model::~Model() {
     cudaFree(sh.d_peers);
     cudaFree(sh.d_recv);
     cudaFree(sh.d_rec);
+    cudaFree(sh.d_ticket);
     cudaFree(sh.d_clamp);
     cudaFreeHost(sh.h_out);
     cudaFreeHost(sh.h_norms);
@@ -477,6 +502,7 @@ Args Model::base_args(Shard& sh, int K) {
   a.fxbins = sh.d_fxbins;
   a.dpart = sh.d_part;
   a.big = sh.d_big;
+  a.ticket = sh.d_ticket;
   a.peers = sh.d_peers;
   a.gworld = group_world_;
   a.grank = group_rank_;
@@ -507,7 +533,19 @@ cudaGraphExec_t Model::graph_for(Shard& sh, int K) {
     occ = kEventBlocksPerSM;
   cudaGraph_t graph;
   ck(cudaStreamBeginCapture(sh.stream, cudaStreamCaptureModeThreadLocal), "begin capture");
-  if (small_norms_) {
+  const bool fused = K == 1 && fused_ok(sh);
+  if (K == 1) sh.fused = false;
+  if (fused) {
+    // ONE kernel: setup in every CTA, then the event pass (pf_fused_kernel)
+    Args f = a;
+    f.clamp = sh.d_clamp;
+    f.fused = 1;
+    launch(sh.mod->fused, dim3(sm_count(sh.device)), dim3(32 * kFusedWarps), fused_smem(L_), sh.stream, f);
+    ++kernels;
+    sh.event_args = f;
+    sh.event_grid = sm_count(sh.device);
+    sh.fused = true;
+  } else if (small_norms_) {
     launch(sh.mod->setup, dim3(K * L_.setup_cluster), dim3(512), setup_smem_bytes(), sh.stream, a, false,
            L_.setup_cluster);
     ++kernels;
@@ -525,7 +563,8 @@ cudaGraphExec_t Model::graph_for(Shard& sh, int K) {
   }
   Args e = a;
   e.clamp = sh.d_clamp;
-  if (sh.n_local > 0) {
+  if (fused) {
+  } else if (sh.n_local > 0) {
     // one warp per chunk, 2-warp blocks: the block scheduler balances SMs
     // persistent grid: one wave of 2-warp blocks; every warp strides over
     // many chunks, so its TMA ring streams without restarts
@@ -562,6 +601,16 @@ cudaGraphExec_t Model::graph_for(Shard& sh, int K) {
   sh.kernels_per_graph = kernels;
   sh.graphs.emplace(K, exec);
   return exec;
+}
+
+// The single-kernel path: small normalisation grids (the setup runs in every
+// CTA), a ring that runs at most one chunk ahead, shared memory that fits,
+// and events on this shard.  PFB200_FUSED=0 selects the two-kernel graph.
+bool Model::fused_ok(const Shard& sh) const {
+  if (const char* env = std::getenv("PFB200_FUSED"))
+    if (std::atoi(env) == 0) return false;
+  return small_norms_ && sh.n_local > 0 && L_.nst <= L_.nsub && fused_smem(L_) <= 200 * 1024 &&
+         L_.setup_maxq <= 8;
 }
 
 void Model::check_call(size_t n, int metric) const {
@@ -621,10 +670,11 @@ void Model::launch_graphs(const double* params, int K) {
     if (K == 1 && sh.graph1) {
       cudaKernelNodeParams kp = {};
       const bool setup = small_norms_;
-      kp.func = reinterpret_cast<void*>(setup ? sh.mod->setup : sh.mod->pre);
-      kp.gridDim = dim3(setup ? L_.setup_cluster : 1);
-      kp.blockDim = dim3(setup ? 512 : 256);
-      kp.sharedMemBytes = setup ? static_cast<unsigned>(setup_smem_bytes()) : 0u;
+      kp.func = reinterpret_cast<void*>(sh.fused ? sh.mod->fused : setup ? sh.mod->setup : sh.mod->pre);
+      kp.gridDim = dim3(sh.fused ? sm_count(sh.device) : setup ? L_.setup_cluster : 1);
+      kp.blockDim = dim3(sh.fused ? 32 * kFusedWarps : setup ? 512 : 256);
+      kp.sharedMemBytes = sh.fused ? static_cast<unsigned>(fused_smem(L_))
+                                   : setup ? static_cast<unsigned>(setup_smem_bytes()) : 0u;
       Args inl = sh.first_args;
       inl.npin = L_.np;
       std::memcpy(inl.pin, params, sizeof(double) * L_.np);
@@ -940,9 +990,16 @@ BenchResult Model::bench(const double* params, size_t n, int metric, int steps, 
     for (int i = 0; i < steps; ++i) {
       if (flush) ck(cudaMemsetAsync(sh.d_scratch, i & 0xff, scratch_bytes, sh.stream), "flush");
       Args a = sh.event_args;
+      if (sh.fused) {  // the whole call is this one kernel: parameters inline, as in the graph
+        a.npin = L_.np;
+        std::memcpy(a.pin, params, sizeof(double) * L_.np);
+      }
       ck(cudaEventRecord(e0, sh.stream), "record");
-      launch(sh.mod->event, dim3(sh.event_grid), dim3(32 * kEventWarps), event_smem(L_, 1), sh.stream,
-             a, false);
+      if (sh.fused)
+        launch(sh.mod->fused, dim3(sh.event_grid), dim3(32 * kFusedWarps), fused_smem(L_), sh.stream, a, false);
+      else
+        launch(sh.mod->event, dim3(sh.event_grid), dim3(32 * kEventWarps), event_smem(L_, 1), sh.stream,
+               a, false);
       ck(cudaEventRecord(e1, sh.stream), "record");
       ck(cudaEventSynchronize(e1), "sync");
       ++g_launches;

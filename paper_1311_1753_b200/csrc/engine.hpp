@@ -95,13 +95,16 @@ struct Args {
   int npin;
   int s_smem;  // the event pass stages S in shared memory (event_s_staged)
   int64_t* big;  // kMaxBatch x kBigStride wide accumulator (pf_big_add)
+  uint32_t* ticket;  // fused pass: dynamic chunk counter
+  int fused;
+  int pad1;
   double pin[64];
 };
 
 struct Module {
   cudaLibrary_t lib = nullptr;
   cudaKernel_t setup = nullptr, pre = nullptr, norm = nullptr, event = nullptr, final = nullptr,
-               publish = nullptr;
+               publish = nullptr, fused = nullptr;
   // generator modules only (PF_GEN, pf_generate.cuh)
   cudaKernel_t gen_max = nullptr, gen_mt = nullptr, gen_mt_jump = nullptr, gen_eval = nullptr,
                gen_scan = nullptr, gen_scatter = nullptr;
@@ -143,6 +146,8 @@ struct Shard {
   cudaGraph_t graph1 = nullptr;       // K = 1 template graph (kept for node updates)
   cudaGraphNode_t first_node = nullptr;
   int event_grid = 1;
+  bool fused = false;          // K = 1 graph is the single fused kernel
+  uint32_t* d_ticket = nullptr;  // fused pass: dynamic chunk counter
   void* d_scratch = nullptr;  // L2 flush buffer (bench only)
 };
 
@@ -153,6 +158,8 @@ struct BenchResult {
 
 void subtree_range(uint64_t n, int shard_count, int index, uint64_t* lo, uint64_t* hi);
 size_t event_smem(const Layout& L, int K);
+size_t fused_smem(const Layout& L);
+constexpr int kFusedWarps = 16;  // PF_FUSED_WARPS
 bool event_s_staged(const Layout& L, int K);
 int sm_count(int device);
 
@@ -213,6 +220,7 @@ class Model {
     return std::find(L_.conv_windowed.begin(), L_.conv_windowed.end(), node) != L_.conv_windowed.end();
   }
   [[noreturn]] void throw_device_error(uint32_t code_node) const;
+  bool fused_ok(const Shard& sh) const;
   size_t setup_smem_bytes() const {
     return sizeof(double) * (std::max(L_.np, 1) + std::max(L_.ss, 1));
   }
