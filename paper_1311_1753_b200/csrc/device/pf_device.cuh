@@ -416,11 +416,17 @@ __device__ __forceinline__ double pf_fx_round(const long long* acc) {
 #include "pf_exp_table.cuh"
 
 __shared__ double2 pf_exp_tab[128];
+#ifdef PF_QFAST
+__shared__ double pf_exp2_1024[1024];  // 2^(j/1024) (pf_qfast_terms)
+#endif
 
 // every kernel calls this before the first pf_exp (includes __syncthreads)
 __device__ __forceinline__ void pf_math_init() {
   for (int i = threadIdx.x; i < 128; i += blockDim.x)
     pf_exp_tab[i] = make_double2(pf_exp_tab_g[2 * i], pf_exp_tab_g[2 * i + 1]);
+#ifdef PF_QFAST
+  for (int i = threadIdx.x; i < 1024; i += blockDim.x) pf_exp2_1024[i] = pf_exp2_1024_g[i];
+#endif
   __syncthreads();
 }
 

@@ -87,8 +87,8 @@ template <int CL>
 __device__ __forceinline__ void pf_setup_core(const pf_args& a, int k, unsigned rank, double* P, double* S,
                                               pf_krec* r, bool init_rec, pf_ctx& cx, pf_cnt& cnt,
                                               pf_cnt& cnt_stage) {
-  // this CTA's warp partials per task, double-buffered by level parity
-  __shared__ double wpart[2][PF_SETUP_MAXQ][PF_SETUP_THREADS / 32];
+  // this CTA's warp partials per task (double-double), double-buffered by level parity
+  __shared__ pf_dd wpart[2][PF_SETUP_MAXQ][PF_SETUP_THREADS / 32];
   __shared__ pf_task tk[16];
 #ifdef PF_SETUP_TRACE
   __shared__ long long trs[32];
@@ -121,9 +121,12 @@ __device__ __forceinline__ void pf_setup_core(const pf_args& a, int k, unsigned 
     while (t1 < nt && tk[t1].level == level) ++t1;
     const int nl = min(t1 - t0, PF_SETUP_MAXQ);  // (coarse, fine) task pairs of the level's nodes
     // every midpoint sum of the level first (this CTA's share of the points).
-    // The grid values are non-negative: plain-double pairwise trees are good
-    // to ~1.5e-15 relative over the 3n points (the reference's long double
-    // is not needed at the 1e-12 bar), at a tenth of double-double's cost.
+    // A thread adds its few points in plain double (a handful per task);
+    // every tree above that is double-double, so the sum is good to ~1e-17
+    // relative whatever the split into threads and CTAs -- its rounding to
+    // double is the correctly rounded sum, as the reference's long double
+    // sum rounded to double (pdf.hpp:163-175) nearly always is, and the same
+    // for the cluster, single-CTA (fused) and multi-block paths.
     double x[PF_SETUP_MAXQ];
 #pragma unroll
     for (int q = 0; q < PF_SETUP_MAXQ; ++q) x[q] = 0.0;
@@ -150,15 +153,18 @@ __device__ __forceinline__ void pf_setup_core(const pf_args& a, int k, unsigned 
       for (int qq = 0; qq < PF_SETUP_MAXQ; ++qq) x[qq] += qq == q ? v : 0.0;
     }
     PF_TRACE("points");
-    // warp trees of all the level's sums together
+    // warp trees of all the level's sums together (double-double)
+    pf_dd xd[PF_SETUP_MAXQ];
+#pragma unroll
+    for (int q = 0; q < PF_SETUP_MAXQ; ++q) xd[q] = pf_dd{x[q], 0.0};
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) {
 #pragma unroll
-      for (int q = 0; q < PF_SETUP_MAXQ; ++q) x[q] += __shfl_down_sync(0xffffffffu, x[q], d);
+      for (int q = 0; q < PF_SETUP_MAXQ; ++q) xd[q] = pf_dd_add(xd[q], pf_shfl_down_dd(xd[q], d));
     }
     if (lane == 0)
 #pragma unroll
-      for (int q = 0; q < PF_SETUP_MAXQ; ++q) wpart[level & 1][q][warp] = x[q];
+      for (int q = 0; q < PF_SETUP_MAXQ; ++q) wpart[level & 1][q][warp] = xd[q];
     PF_TRACE("wtree");
     // warp partials of every rank visible cluster-wide (double-buffered by
     // level parity: a rank cannot overwrite a buffer another rank may still
@@ -173,19 +179,20 @@ __device__ __forceinline__ void pf_setup_core(const pf_args& a, int k, unsigned 
     // a fixed tree, then a 16-lane tree; lane 0 finishes the node
     if (2 * warp < nl) {
       const int q = 2 * warp + (lane >> 4);
-      const double* src = &wpart[level & 1][q][lane & 15];
-      double v[CL];
+      const pf_dd* src = &wpart[level & 1][q][lane & 15];
+      pf_dd v[CL];
 #pragma unroll
-      for (int rk = 0; rk < CL; ++rk) v[rk] = CL > 1 ? pf_dsmem_load(src, (unsigned)rk) : *src;
+      for (int rk = 0; rk < CL; ++rk)
+        v[rk] = CL > 1 ? pf_dd{pf_dsmem_load(&src->hi, (unsigned)rk), pf_dsmem_load(&src->lo, (unsigned)rk)} : *src;
 #pragma unroll
       for (int w = 1; w < CL; w <<= 1)
 #pragma unroll
-        for (int rk = 0; rk + w < CL; rk += 2 * w) v[rk] += v[rk + w];
-      double y = v[0];
+        for (int rk = 0; rk + w < CL; rk += 2 * w) v[rk] = pf_dd_add(v[rk], v[rk + w]);
+      pf_dd y = v[0];
 #pragma unroll
-      for (int d = 8; d > 0; d >>= 1) y += __shfl_down_sync(0xffffffffu, y, d);
+      for (int d = 8; d > 0; d >>= 1) y = pf_dd_add(y, pf_shfl_down_dd(y, d));
       // midpoint_sum returns static_cast<double>(sum) * vol (pdf.hpp:173-175)
-      const double sum = __dmul_rn(y, tk[t0 + q].vol);
+      const double sum = __dmul_rn(pf_dd_to_double(y), tk[t0 + q].vol);
       const double fine = __shfl_down_sync(0xffffffffu, sum, 16);
       if (lane == 0) pf_finish_norm(S, r, tk[t0 + q].node, sum, fine);
     }
@@ -590,6 +597,62 @@ __device__ __forceinline__ pf_fk pf_fk_get(const pf_args& a, int k) {
   return pf_fk_load(a.P + (pf_u64)k * PF_NP, a.S + (pf_u64)k * PF_SS, a.C);
 }
 
+#ifdef PF_QFAST
+// Mixture fast path: AddPdf of two Exp/Gauss children of one observable,
+// the per-call proof K.qfast holding (codegen.cpp: every event's terms in
+// range, no floor, |d| <= 700, quadratic terms <= 4096).  With
+// u_i = log(coef_i raw_i) = a_i x^2 + b_i x + c_i and d = u0 - u1,
+//   -log v = -(max(u0, u1) + log(1 + e^-|d|)),  max(u0, u1) = (u0 + u1 + |d|) / 2,
+// so per event: d by two FMAs, e^-|d| = 2^(k/1024) e^r by a 1024-entry table
+// and a cubic (|r| <= ln2/2048: truncation r^4/24 < 6e-16), and the lane
+// sums x, x^2, |d| and two products of (1 + e^-|d|).  Sum (u0 + u1) over the
+// lane's events is one quadratic in (sum x^2, sum x, n) per sub-chunk; the
+// result is the log-form accumulator {sum L, product F} of the other paths.
+// 13 FP64 instructions per event.
+template <bool FULL>
+__device__ __forceinline__ pf_lacc pf_qfast_terms(const double* st, int lane, int n_valid, const pf_fk& K) {
+  const double qA = K.q[0], qB = K.q[1], qC = K.q[2];
+  double sx = 0.0, sxx = 0.0, sd = 0.0, p0 = 1.0, p1 = 1.0;
+  int n = 0;
+  const double2* s2 = reinterpret_cast<const double2*>(st);
+#pragma unroll
+  for (int j = 0; j < PF_EPT / 2; ++j) {
+    const int i = 32 * j + lane;  // this lane's events 2i and 2i + 1 of the stage
+    const double2 xv = s2[i];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const bool valid = FULL || 2 * i + h < n_valid;
+      const double x = valid ? (h ? xv.y : xv.x) : 0.0;
+      const double d = fma(fma(qA, x, qB), x, qC);
+      const double ad = valid ? fabs(d) : 0.0;
+      sx += x;
+      sxx = fma(x, x, sxx);
+      sd += ad;
+      const double kd = fma(-ad, PF_Q_INVLN2N, 0x1.8p52);
+      const int ki = __double2loint(kd);
+      const double k = kd - 0x1.8p52;
+      const double r = fma(k, -PF_Q_LN2N, -ad);
+      const double T = pf_exp2_1024[ki & 1023];
+      double pp = fma(r, 1.0 / 6.0, 0.5);
+      pp = fma(pp, r, 1.0);
+      const double sv = fma(T, r * pp, T);
+      double e = __hiloint2double(__double2hiint(sv) + (int)((unsigned)(ki >> 10) << 20), __double2loint(sv));
+      if (!FULL && !valid) e = 0.0;
+      if (h == 0)
+        p0 = fma(p0, e, p0);
+      else
+        p1 = fma(p1, e, p1);
+      n += valid ? 1 : 0;
+    }
+  }
+  pf_lacc out;
+  const double nn = FULL ? (double)PF_EPT : (double)n;
+  out.v[0] = 0.5 * (fma(K.q[3], sxx, fma(K.q[4], sx, nn * K.q[5])) + sd);
+  out.v[1] = p0 * p1;
+  return out;
+}
+#endif
+
 template <bool FULL>
 __device__ __forceinline__ pf_lacc pf_stage_terms(const pf_args& a, int k, pf_u64 base, int lane,
                                                 const double* st, int n_valid, const pf_fk& K,
@@ -600,6 +663,9 @@ __device__ __forceinline__ pf_lacc pf_stage_terms(const pf_args& a, int k, pf_u6
 #ifdef PF_LOG_FAST_SLOT
   // per-call fast path: interval bounds over the data box (pf_stage_post)
   // proved every event's terms in range, so no per-event test at all
+#ifdef PF_QFAST
+  if (K.qfast) return pf_qfast_terms<FULL>(st, lane, n_valid, K);
+#endif
   if (K.fast) {
 #pragma unroll pf_unroll
     for (int j = 0; j < PF_EPT; ++j) {

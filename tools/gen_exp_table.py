@@ -30,6 +30,15 @@ def main():
     inv = float(Decimal(128) / LN2)
     lines += [f"#define PF_EXP_INVLN2N {inv.hex()}", f"#define PF_EXP_LN2N_HI {hi.hex()}",
               f"#define PF_EXP_LN2N_LO {lo.hex()}"]
+    # the mixture fast path (pf_qfast_terms): 2^(j/1024) rounded to nearest,
+    # one double per entry (1.1e-16 relative), and ln2/1024 as one double
+    # (k * ln2/1024 by a single FMA: |k| < 2^17, error < 4e-20 |k|)
+    lines += ["// 2^(j/1024) = RN(2^(j/1024)) (pf_qfast_terms)", "__device__ const double pf_exp2_1024_g[1024] = {"]
+    for j in range(1024):
+        lines.append(f"  {float((LN2 * j / 1024).exp()).hex()},")
+    lines.append("};")
+    lines += [f"#define PF_Q_INVLN2N {float(Decimal(1024) / LN2).hex()}",
+              f"#define PF_Q_LN2N {float(LN2 / 1024).hex()}"]
     with open(OUT, "w") as fh:
         fh.write("\n".join(lines) + "\n")
     _ = struct
