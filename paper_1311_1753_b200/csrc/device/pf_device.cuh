@@ -100,7 +100,9 @@ struct pf_args {
   long long* big;       // K x PF_BIG_STRIDE: wide accumulator of chunk sums >= 2^62 (pf_big_add)
   pf_u32* ticket;       // fused pass: dynamic chunk counter (self-resetting)
   int fused;            // 1: this launch is the single fused kernel (setup in every CTA)
-  int pad1;
+  pf_u32 gmask;         // K = 1 inline: bit 0 = count this call's grid clamps
+  const pf_u32* hmask;  // host-mapped: bit k = parameter set k recomputes its norms
+                        // (the reference's fingerprint cache, pdf.hpp:111-123)
   double pin[PF_MAX_INLINE];
 };
 
@@ -129,6 +131,15 @@ __device__ __forceinline__ bool pf_finish_norm_s(double* S, int node, double coa
   S[PF_SUMS_BASE + 2 * node + 1] = fine;
 #endif
   return !(norm > 0.0) || !isfinite(norm);
+}
+
+// Does parameter set k count the clamps met on the normalisation grids?  The
+// reference recomputes norms only when the parameters' hash changed since the
+// last refresh (pdf.hpp:111-123, hash_params :40-51); this engine recomputes
+// every call, so it counts the grid clamps only when the reference would.
+__device__ __forceinline__ bool pf_grid_counts(const pf_args& a, int k) {
+  const pf_u32 m = a.npin ? a.gmask : __ldcv(a.hmask);
+  return (m >> k) & 1u;
 }
 
 __device__ __forceinline__ void pf_finish_norm_cx(double* S, pf_ctx& cx, int node, double coarse,

@@ -239,8 +239,10 @@ extern "C" __global__ void __launch_bounds__(PF_SETUP_THREADS) pf_setup_kernel(c
   pf_cnt_init(cnt_stage);
   pf_setup_core<PF_SETUP_CLUSTER>(a, k, rank, P, S, r, true, cx, cnt, cnt_stage);
   if (cx.err) atomicMin(&r->norm_error, cx.err);
-  pf_cnt_flush(cnt, a.clamp);
-  if (rank == 0) pf_cnt_flush(cnt_stage, a.clamp);
+  if (pf_grid_counts(a, k)) {
+    pf_cnt_flush(cnt, a.clamp);
+    if (rank == 0) pf_cnt_flush(cnt_stage, a.clamp);
+  }
   __syncthreads();
   if (rank == 0) {
     double* gS = a.S + (pf_u64)k * PF_SS;
@@ -271,7 +273,7 @@ extern "C" __global__ void __launch_bounds__(PF_THREADS) pf_pre_kernel(const __g
   pf_stage_pre(k, a.P + (pf_u64)k * PF_NP, a.S + (pf_u64)k * PF_SS, a.C, cx, cnt, threadIdx.x,
                blockDim.x);
   if (cx.err) atomicMin(&r->norm_error, cx.err);
-  pf_cnt_flush(cnt, a.clamp);
+  if (pf_grid_counts(a, k)) pf_cnt_flush(cnt, a.clamp);
 }
 
 // ---------------------------------------------------------------------------
@@ -314,7 +316,7 @@ extern "C" __global__ void __launch_bounds__(PF_THREADS) pf_norm_kernel(const __
     if (threadIdx.x == 0) part[blockIdx.x] = s;
   }
   if (cx.err) atomicMin(&a.rec[k].norm_error, cx.err);
-  pf_cnt_flush(cnt, a.clamp);
+  if (pf_grid_counts(a, k)) pf_cnt_flush(cnt, a.clamp);
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -342,7 +344,7 @@ extern "C" __global__ void __launch_bounds__(PF_THREADS) pf_norm_kernel(const __
   pf_cnt_init(cnt2);
   pf_stage_post(a.level, k, P, S, a.C, cx2, cnt2, threadIdx.x, blockDim.x);
   if (cx2.err) atomicMin(&a.rec[k].norm_error, cx2.err);
-  pf_cnt_flush(cnt2, a.clamp);
+  if (pf_grid_counts(a, k)) pf_cnt_flush(cnt2, a.clamp);
 }
 
 // ---------------------------------------------------------------------------
@@ -1143,6 +1145,9 @@ extern "C" __global__ void __launch_bounds__(PF_EV_THREADS, PF_EVENT_MIN_BLOCKS)
 
 extern "C" __global__ void __launch_bounds__(PF_FUSED_THREADS, 1) pf_fused_kernel(const __grid_constant__ pf_args a) {
   static_assert(PF_FUSED_THREADS == PF_SETUP_THREADS, "the setup core strides by PF_SETUP_THREADS");
+#ifdef PF_EVENT_TRACE
+  const unsigned long long t_in = pf_gtime();
+#endif
   extern __shared__ __align__(16) unsigned char pf_dyn[];
   __shared__ __align__(8) pf_u64 bars[PF_FUSED_WARPS * PF_NST];
   __shared__ long long bfx[PF_FUSED_WARPS][PF_FX_DIGITS];
@@ -1193,14 +1198,19 @@ extern "C" __global__ void __launch_bounds__(PF_FUSED_THREADS, 1) pf_fused_kerne
   pf_setup_core<1>(a, 0, 0u, P, S, r, false, cx, cnt_grid, cnt_stage);
   if (blockIdx.x == 0) {  // one CTA reports what every CTA found
     if (cx.err) atomicMin(&r->norm_error, cx.err);
-    pf_cnt_flush(cnt_grid, a.clamp);
-    pf_cnt_flush(cnt_stage, a.clamp);
+    if (pf_grid_counts(a, 0)) {
+      pf_cnt_flush(cnt_grid, a.clamp);
+      pf_cnt_flush(cnt_stage, a.clamp);
+    }
     double* gS = a.S;
     double* gP = (double*)a.P;
     for (int i = threadIdx.x; i < PF_SS; i += blockDim.x) gS[i] = S[i];
     for (int i = threadIdx.x; i < PF_NP; i += blockDim.x) gP[i] = P[i];
   }
   __syncthreads();  // P and S complete (the setup core ends with a barrier too)
+#ifdef PF_EVENT_TRACE
+  const unsigned long long t_setup = pf_gtime();
+#endif
   const pf_fk fk = pf_fk_load(P, S, a.C);
   pf_fxl F;
 #pragma unroll
@@ -1231,9 +1241,27 @@ extern "C" __global__ void __launch_bounds__(PF_FUSED_THREADS, 1) pf_fused_kerne
       c_cur = c_nxt;
       c_nxt = c_pend;
       c_pend = nch;
-      if (c_nxt < nch) c_pend = 2 * nw + (int)atomicAdd(a.ticket, 1u);
+      if (c_nxt < nch) {
+        c_pend = 2 * nw + (int)atomicAdd(a.ticket, 1u);
+#ifdef PF_L2_PREFETCH
+        // the chunk after this one into L2 now: its TMA copies later hit L2
+        const pf_u64 b = (pf_u64)c_nxt * (PF_SUB * PF_NSUB);
+#pragma unroll
+        for (int q = 0; q < PF_NLOAD; ++q)
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.data + (pf_u64)pf_load_col(q) * a.col_stride + b),
+                       "r"((unsigned)(PF_SUB * PF_NSUB * 8))
+                       : "memory");
+#endif
+      }
     }
   }
+#ifdef PF_EVENT_TRACE
+  const unsigned long long t_loop = pf_gtime();
+  __shared__ unsigned long long t_loop_max;
+  if (threadIdx.x == 0) t_loop_max = 0;
+  __syncthreads();
+  atomicMax(&t_loop_max, t_loop);
+#endif
   // block total (exact integer digits), ONE binned atomic set per CTA
   pf_fxl_warp_sum(F);
   if (lane == 0)
@@ -1254,13 +1282,30 @@ extern "C" __global__ void __launch_bounds__(PF_FUSED_THREADS, 1) pf_fused_kerne
     s_last = atomicAdd(a.done, 1u) == gridDim.x - 1;
   }
   __syncthreads();
+#ifdef PF_EVENT_TRACE
+  if (threadIdx.x == 0 && blockIdx.x < 4094) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    PF_ETRACE(0, t_in);
+    PF_ETRACE(1, t_setup);
+    PF_ETRACE(2, t_loop_max);
+    PF_ETRACE(3, pf_gtime());
+    PF_ETRACE(5, (unsigned long long)smid);
+  }
+#endif
   if (!s_last) return;
   __threadfence();
+#ifdef PF_EVENT_TRACE
+  if (threadIdx.x == 0) pf_trace_buf[4094 * 6 + 0] = pf_gtime();
+#endif
   if (threadIdx.x == 0) {
     *a.done = 0u;     // self-resetting (every CTA has arrived)
     *a.ticket = 0u;   // every ticket has been taken and consumed
   }
   if (warp == 0) pf_finalize_warp0(a, lane, S);
+#ifdef PF_EVENT_TRACE
+  if (threadIdx.x == 0) pf_trace_buf[4094 * 6 + 2] = pf_gtime();
+#endif
 }
 
 // ---------------------------------------------------------------------------

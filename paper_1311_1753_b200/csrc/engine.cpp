@@ -280,6 +280,9 @@ Model::Model(const pf_graph& g, const pf_data& d, uint32_t grid_points, const pf
   ck(cudaHostAlloc(reinterpret_cast<void**>(&h_params_), sizeof(double) * kMaxBatch * std::max(L_.np, 1),
                    cudaHostAllocMapped | cudaHostAllocPortable),
      "cudaHostAlloc params");
+  ck(cudaHostAlloc(reinterpret_cast<void**>(&h_mask_), sizeof(uint32_t) * 16, cudaHostAllocMapped | cudaHostAllocPortable),
+     "cudaHostAlloc mask");
+  std::memset(h_mask_, 0, sizeof(uint32_t) * 16);
 
   const int G = n_devices;
   const int groups = std::max(G, shard_count_);
@@ -405,6 +408,7 @@ Model::~Model() {
     cudaFree(sh.d_scratch);
   }
   cudaFreeHost(h_params_);
+  cudaFreeHost(h_mask_);
 }
 
 // Norm tasks: for every normalised node, midpoint sums at n and 2n points per
@@ -483,6 +487,8 @@ Args Model::base_args(Shard& sh, int K) {
   ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&a.hout), sh.h_out, 0), "mapped out");
   ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&a.hnorms), sh.h_norms, 0), "mapped norms");
   ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&a.hclamp), sh.h_clamp, 0), "mapped clamp");
+  ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(const_cast<uint32_t**>(&a.hmask)), h_mask_, 0),
+     "mapped mask");
   a.n_nodes = static_cast<int>(pg_.nodes.size());
   a.fuse_final = K == 1 ? 1 : 0;
   a.n_levels = static_cast<int>(L_.level_nodes.size());
@@ -662,8 +668,37 @@ void Model::run(const double* params, int K, std::vector<Raw>& out, bool partial
   wait_results(K, out, partial_only);
 }
 
+// hash_params (pdf.hpp:40-51): FNV-1a over the parameters' bytes
+static uint64_t hash_params(const double* p, int n) {
+  uint64_t h = 14695981039346656037ull;
+  for (int k = 0; k < n; ++k) {
+    uint64_t bits;
+    std::memcpy(&bits, p + k, sizeof bits);
+    for (int i = 0; i < 8; ++i) {
+      h ^= (bits >> (8 * i)) & 0xffu;
+      h *= 1099511628211ull;
+    }
+  }
+  return h;
+}
+
 void Model::launch_graphs(const double* params, int K) {
   if (L_.np > 0) std::memcpy(h_params_, params, sizeof(double) * K * L_.np);
+  // the reference recomputes norms (and so meets the grid's clamps) only
+  // when the parameters' hash differs from the last refresh's (pdf.hpp:111-123)
+  call_mask_ = 0;
+  call_hash_.assign(K, 0);
+  {
+    uint64_t cur = norm_hash_;
+    bool have = have_norm_hash_;
+    for (int k = 0; k < K; ++k) {
+      call_hash_[k] = hash_params(params + static_cast<size_t>(k) * L_.np, L_.np);
+      if (!have || call_hash_[k] != cur) call_mask_ |= 1u << k;
+      cur = call_hash_[k];
+      have = true;
+    }
+  }
+  *reinterpret_cast<volatile uint32_t*>(h_mask_) = call_mask_;
   for (Shard& sh : shards_) {
     cudaGraphExec_t g = graph_for(sh, K);
     ck(cudaSetDevice(sh.device), "cudaSetDevice");
@@ -677,6 +712,7 @@ void Model::launch_graphs(const double* params, int K) {
                                    : setup ? static_cast<unsigned>(setup_smem_bytes()) : 0u;
       Args inl = sh.first_args;
       inl.npin = L_.np;
+      inl.gmask = call_mask_;
       std::memcpy(inl.pin, params, sizeof(double) * L_.np);
       void* ptrs[] = {&inl};
       kp.kernelParams = ptrs;
@@ -726,6 +762,10 @@ void Model::wait_results(int K, std::vector<Raw>& out, bool partial_only) {
     if (norm_err != ~0u) {  // refresh_normalizations threw (engine.hpp:174-178)
       out[k].penalty = true;
       continue;
+    }
+    if (k < static_cast<int>(call_hash_.size())) {  // the fingerprint the reference now holds
+      norm_hash_ = call_hash_[k];
+      have_norm_hash_ = true;
     }
     // norms are replicated on every shard; keep the last successful set
     const double* hn = shards_[0].h_norms + static_cast<size_t>(k) * 3 * nn;

@@ -97,7 +97,8 @@ struct Args {
   int64_t* big;  // kMaxBatch x kBigStride wide accumulator (pf_big_add)
   uint32_t* ticket;  // fused pass: dynamic chunk counter
   int fused;
-  int pad1;
+  uint32_t gmask;          // K = 1 inline: count this call's grid clamps (bit 0)
+  const uint32_t* hmask;   // mapped: bit k = parameter set k recomputes its norms
   double pin[64];
 };
 
@@ -239,6 +240,11 @@ class Model {
   std::vector<int> level_first_task_, level_n_tasks_, level_blocks_;
   int max_norm_blocks_ = 0;
   double* h_params_ = nullptr;  // mapped, kMaxBatch x np
+  uint32_t* h_mask_ = nullptr;  // mapped: grid-clamp counting mask of the call (pf_grid_counts)
+  uint32_t call_mask_ = 0;      // the mask of the call in flight
+  std::vector<uint64_t> call_hash_;  // hash_params of each parameter set of the call in flight
+  uint64_t norm_hash_ = 0;      // hash_params of the last call whose norms were computed
+  bool have_norm_hash_ = false;
   uint64_t floor_total_ = 0;
   std::vector<uint64_t> clamp_total_;
   std::vector<double> norms_, errs_;
