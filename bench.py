@@ -440,6 +440,9 @@ def main():
                 handles = [None] * world
                 dist.all_gather_object(handles, bm.group_handle())
                 bm.group_join(world, rank, handles)
+                # every rank's receive buffer is reset by its own join: no
+                # record may be sent before every rank has joined
+                dist.barrier()
                 bm.eval_metric(params, metric)  # one grouped call: the peers' records must arrive
             except Exception as e:  # noqa: BLE001 - reported, then the fallback
                 print(f"rank {rank}: peer-memory group unavailable ({e}); using NCCL", file=sys.stderr)

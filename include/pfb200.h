@@ -123,15 +123,25 @@ typedef struct pf_data {
  *                  chunk range shard_index of shard_count (power of two);
  *                  pf_eval_partial returns its exact accumulator and
  *                  pf_combine_partials reproduces the global value.
- *                  shard_count = 1: whole data set. */
+ *                  shard_count = 1: whole data set.
+ *   oversubscribe: 1 lets n_devices exceed the visible devices: shard s
+ *                  runs on device (device + s) mod count.  The shards still
+ *                  combine on the host (no kernel waits on another), so this
+ *                  exercises the multi-device path on a one-GPU box; 0 (the
+ *                  default) rejects a count above the visible devices. */
 typedef struct pf_options {
   int32_t device;
   int32_t n_devices;
   int32_t shard_index;
   int32_t shard_count;
   int32_t verbose;
-  int32_t reserved[3];
+  int32_t oversubscribe;
+  int32_t reserved[2];
 } pf_options;
+
+/* number of CUDA devices visible to this process (cudaGetDeviceCount; 0
+ * when the driver reports none) */
+PF_API int32_t pf_device_count(void);
 
 typedef struct pf_status {
   int32_t code; /* 0 ok */

@@ -47,8 +47,8 @@ class pf_data(C.Structure):
 
 class pf_options(C.Structure):
     _fields_ = [("device", C.c_int32), ("n_devices", C.c_int32), ("shard_index", C.c_int32),
-                ("shard_count", C.c_int32), ("verbose", C.c_int32),
-                ("reserved", C.c_int32 * 3)]
+                ("shard_count", C.c_int32), ("verbose", C.c_int32), ("oversubscribe", C.c_int32),
+                ("reserved", C.c_int32 * 2)]
 
 
 class pf_status(C.Structure):
@@ -118,6 +118,7 @@ _SIGNATURES = {
                                C.POINTER(C.c_uint64)]),
     "pf_model_chunk": (C.c_uint64, [C.c_void_p]),
     "pf_abi_version": (C.c_int32, []),
+    "pf_device_count": (C.c_int32, []),
     "pf_kernel_launches": (C.c_uint64, []),
     "pf_debug_trace": (C.c_int64, [C.c_void_p, C.POINTER(C.c_uint64), C.c_int64]),
     "pf_generate_events": (C.c_int, [C.POINTER(pf_graph), C.POINTER(C.c_int32), C.c_int32, C.c_uint64,

@@ -47,21 +47,23 @@ def bench_rows(workload: str, gpu_counts: Sequence[int], repetitions: int,
     ds = _dataset(pf, W, obs, n_events, data_path)
     rows = []
     for n in gpu_counts:
-        bm = pf.BoundModel(pdf, ds, pf.GridSpec(W.grid), pf.Backend.gpus(n))
         times, last, metrics = [], None, set()
         for _ in range(repetitions):
-            for p in bm.registry().parameters():  # identical start every run
+            # one BoundModel per repetition, as the reference builds one per
+            # run (parfit_cli.cpp:147-152); identical start every run
+            bm = pf.BoundModel(pdf, ds, pf.GridSpec(W.grid), pf.Backend.gpus(n))
+            for p in bm.registry().parameters():
                 p.value = W.start[p.name]
             r = pf.fit(bm, pf.MetricKind(W.metric))
             times.append(r.wall_time_s)
             metrics.add(r.metric_value)
             last = r
+            del bm
         if len(metrics) != 1:
             raise pf.Error("determinism-violation", f"metric value differs across repetitions at {n} GPUs")
         times.sort()
         rows.append({"gpus": n, "median_s": times[len(times) // 2], "metric_value": last.metric_value,
                      "metric_calls": last.n_metric_calls})
-        del bm
     return rows
 
 
@@ -82,6 +84,15 @@ def cmd_bench(workload: str, gpu_counts: Sequence[int], repetitions: int, n_even
     counts = sorted(set(int(c) for c in gpu_counts))
     if len(counts) < 2 or 1 not in counts:
         raise Error("bad-arity", "bench needs >= 2 GPU counts including 1")
+    # the engine shards over powers of two (contiguous subtrees of the
+    # reduction tree) and never oversubscribes here: checked before any work
+    bad = [c for c in counts if c & (c - 1)]
+    if bad:
+        raise Error("bad-backend", f"GPU counts must be powers of two (got {bad})")
+    from .parfit import device_count
+    have = device_count()
+    if counts[-1] > have:
+        raise Error("bad-backend", f"bench asks for {counts[-1]} GPUs, {have} visible")
     rows = bench_rows(workload, counts, repetitions, n_events, data_path)
     if any(r["metric_value"] != rows[0]["metric_value"] for r in rows):
         raise Error("determinism-violation", "metric value differs across GPU counts: bench aborted")

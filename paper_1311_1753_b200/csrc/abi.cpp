@@ -1,6 +1,7 @@
 // abi.cpp — extern "C" entry points of include/pfb200.h.  Every C++
 // exception becomes a nonzero return plus the reference's "code: detail"
 // message (errors.hpp:9-16).
+#include <cuda_runtime.h>
 #include <algorithm>
 #include <cstring>
 #include <memory>
@@ -61,6 +62,14 @@ pfb::Config to_config(const pf_fit_config* c) {
 extern "C" {
 
 int32_t pf_abi_version(void) { return PF_ABI_VERSION; }
+int32_t pf_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
 uint64_t pf_kernel_launches(void) { return pfb::kernel_launch_count(); }
 
 int pf_graph_finalize(const pf_graph* graph, int32_t n_data_obs, const int32_t* data_obs,

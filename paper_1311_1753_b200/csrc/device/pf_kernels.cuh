@@ -808,8 +808,13 @@ __device__ __noinline__ void pf_group_exchange(const pf_args& a, int k, int lane
   // bit 0: an error or non-finite term, bit 1: wide (>= 2^62) chunk sums
   const int flag = __shfl_sync(0xffffffffu, (int)(nonfinite != ~0ull || evterr != ~0ull) | (gbig ? 2 : 0), 0);
   const unsigned long long seq = (unsigned long long)(a.done[1 + k] + 1u);
+  // slots double-buffered by call parity: a rank can run at most one call
+  // ahead of a peer (it needs every peer's record of call n to finish call
+  // n), so call n + 1's record can never overwrite call n's before the peer
+  // has read it
+  const pf_u64 slot_base = (pf_u64)(seq & 1ull) * PF_MAX_BATCH * PF_GROUP_MAX;
   if (lane < a.gworld) {  // send: lane q writes this rank's record into rank q's buffer
-    long long* dst = a.peers[lane] + ((pf_u64)k * PF_GROUP_MAX + a.grank) * 16;
+    long long* dst = a.peers[lane] + (slot_base + (pf_u64)k * PF_GROUP_MAX + a.grank) * 16;
 #pragma unroll
     for (int i = 0; i < PF_FX_DIGITS; ++i) dst[i] = g[i];
     dst[6] = (long long)nerr;
@@ -822,7 +827,7 @@ __device__ __noinline__ void pf_group_exchange(const pf_args& a, int k, int lane
   pf_u32 qerr = ~0u;
   int qflag = 0, timeout = 0;
   if (lane < a.gworld) {  // receive: lane q waits for rank q's record
-    const long long* src = a.peers[a.grank] + ((pf_u64)k * PF_GROUP_MAX + lane) * 16;
+    const long long* src = a.peers[a.grank] + (slot_base + (pf_u64)k * PF_GROUP_MAX + lane) * 16;
     unsigned long long t0, t, got;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     for (;;) {

@@ -286,10 +286,16 @@ Model::Model(const pf_graph& g, const pf_data& d, uint32_t grid_points, const pf
 
   const int G = n_devices;
   const int groups = std::max(G, shard_count_);
+  int visible = 0;
+  if (cudaGetDeviceCount(&visible) != cudaSuccess || visible < 1)
+    throw Error("cuda-error", "no CUDA device visible (there is no CPU fallback)");
+  if (!opt.oversubscribe && opt.device + G > visible)
+    throw Error("bad-backend", std::to_string(G) + " devices requested from device " + std::to_string(opt.device) +
+                                   ", " + std::to_string(visible) + " visible");
   shards_.resize(G);
   for (int s = 0; s < G; ++s) {
     Shard& sh = shards_[s];
-    sh.device = opt.device + s;
+    sh.device = opt.oversubscribe ? (opt.device + s) % visible : opt.device + s;
     int part = shard_count_ > 1 ? shard_index_ : s;
     // balanced contiguous chunk ranges; the exact accumulator makes the sum
     // independent of where the shards split
@@ -321,8 +327,8 @@ Model::Model(const pf_graph& g, const pf_data& d, uint32_t grid_points, const pf
     ck(cudaMalloc(&sh.d_partials, 16 * part_elems), "cudaMalloc partials");
     ck(cudaMalloc(&sh.d_done, sizeof(uint32_t) * (1 + kMaxBatch)), "cudaMalloc done");
     ck(cudaMemset(sh.d_done, 0, sizeof(uint32_t) * (1 + kMaxBatch)), "memset done");
-    ck(cudaMalloc(&sh.d_recv, sizeof(int64_t) * 16 * kMaxGroup * kMaxBatch), "cudaMalloc group receive");
-    ck(cudaMemset(sh.d_recv, 0, sizeof(int64_t) * 16 * kMaxGroup * kMaxBatch), "memset group receive");
+    ck(cudaMalloc(&sh.d_recv, sizeof(int64_t) * 2 * 16 * kMaxGroup * kMaxBatch), "cudaMalloc group receive");
+    ck(cudaMemset(sh.d_recv, 0, sizeof(int64_t) * 2 * 16 * kMaxGroup * kMaxBatch), "memset group receive");
     ck(cudaMalloc(&sh.d_part, sizeof(int64_t) * 8 * kMaxBatch), "cudaMalloc partial");
     ck(cudaMemset(sh.d_part, 0, sizeof(int64_t) * 8 * kMaxBatch), "memset partial");
     ck(cudaMalloc(&sh.d_big, sizeof(int64_t) * kBigStride * kMaxBatch), "cudaMalloc wide digits");
@@ -949,7 +955,7 @@ void Model::group_join(int world, int rank, const void* handles) {
   ck(cudaMemcpy(sh.d_peers, ptrs.data(), sizeof(int64_t*) * world, cudaMemcpyHostToDevice), "peers H2D");
   // every rank restarts its per-call sequence at 0 (callers barrier after
   // joining, before the first evaluation)
-  ck(cudaMemset(sh.d_recv, 0, sizeof(int64_t) * 16 * kMaxGroup * kMaxBatch), "memset group receive");
+  ck(cudaMemset(sh.d_recv, 0, sizeof(int64_t) * 2 * 16 * kMaxGroup * kMaxBatch), "memset group receive");
   ck(cudaMemset(sh.d_done, 0, sizeof(uint32_t) * (1 + kMaxBatch)), "memset done");
   for (int k = 0; k < kMaxBatch; ++k) sh.seq[k] = 0;
   std::memset(sh.h_out, 0, sizeof(Out) * kMaxBatch);

@@ -917,12 +917,13 @@ class Backend:
     compatibility and select nothing: evaluation always runs on the GPU.
     ``Backend.gpus(n)`` shards events over n devices of this process."""
 
-    def __init__(self, kind="gpu", threads=1, chunk_size=4096, devices=1, device=0):
+    def __init__(self, kind="gpu", threads=1, chunk_size=4096, devices=1, device=0, oversubscribe=False):
         self.kind = kind
         self.threads = threads
         self.chunk_size = chunk_size
         self.devices = devices
         self.device = device
+        self.oversubscribe = oversubscribe
 
     @staticmethod
     def serial():
@@ -935,8 +936,10 @@ class Backend:
         return Backend("threads", n, chunk)
 
     @staticmethod
-    def gpus(n=1, device=0):
-        return Backend("gpu", devices=n, device=device)
+    def gpus(n=1, device=0, oversubscribe=False):
+        """n devices from `device`; oversubscribe=True places shard s on
+        device (device + s) mod count (the multi-device path on fewer GPUs)"""
+        return Backend("gpu", devices=n, device=device, oversubscribe=oversubscribe)
 
 
 class BoundModel:
@@ -959,7 +962,8 @@ class BoundModel:
         self._data_idx = (C.c_int32 * max(len(obs), 1))(*[self._desc.var_index(o) for o in obs])
         cdata = _abi.pf_data(1 if self._binned else 0, len(obs), self._data_idx, self._n,
                              self._values.ctypes.data_as(C.POINTER(C.c_double)), self._total)
-        opt = _abi.pf_options(backend.device, max(1, backend.devices), shard_index, shard_count, 0)
+        opt = _abi.pf_options(backend.device, max(1, backend.devices), shard_index, shard_count, 0,
+                              1 if getattr(backend, "oversubscribe", False) else 0)
         st = _abi.pf_status()
         h = C.c_void_p()
         if lib.pf_model_create(C.byref(self._desc.c_graph), C.byref(cdata), grid.points, C.byref(opt),
@@ -1125,6 +1129,11 @@ def combine_partials(parts) -> float:
     """exact combine of shard accumulators [[d0..d5], ...] (pfb200.h)"""
     flat = (C.c_int64 * (_abi.PF_FX_DIGITS * len(parts)))(*[int(v) for fx in parts for v in fx])
     return lib.pf_combine_partials(flat, len(parts))
+
+
+def device_count() -> int:
+    """CUDA devices visible to this process (pf_device_count)"""
+    return int(lib.pf_device_count())
 
 
 def kernel_launches() -> int:

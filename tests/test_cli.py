@@ -63,6 +63,14 @@ def test_bench_full_command(tmp_path):
         lines = out.read_text().splitlines()
         assert lines[0] == "backend gpus time_s speedup metric_calls" and len(lines) == 3
         assert lines[1].split()[3] == "1"
-    else:  # one GPU: the second count has no device and the engine says so
-        with pytest.raises(pf.Error):
+    else:  # one GPU: refused up front, before any fit, with the visible count
+        with pytest.raises(pf.Error) as ei:
             cli.cmd_bench("C1", [1, 2], 3, n_events=20_000, out_path=str(out))
+        assert ei.value.args[0].startswith("bad-backend") and "1 visible" in str(ei.value)
+
+
+def test_bench_rejects_non_power_of_two_counts_up_front():
+    """the engine shards over powers of two; the CLI says so before any work"""
+    with pytest.raises(pf.Error) as ei:
+        cli.cmd_bench("C1", [1, 3], 3, n_events=1000)
+    assert ei.value.args[0].startswith("bad-backend") and "powers of two" in str(ei.value)

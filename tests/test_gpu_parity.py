@@ -517,3 +517,38 @@ def test_c4_wide_sums_on_the_partial_path_raise_metric_overflow():
             bm.eval_partial([2.5, 0.05, 0.2, 0.0001], pf.MetricKind.ChiSquared)
     parts2 = [bm.eval_partial(truth, pf.MetricKind.ChiSquared)[0] for bm in shards]
     assert [list(p) for p in parts2] == [list(p) for p in parts]
+
+
+@pytest.mark.parametrize("n_dev", [2, 4, 8])
+def test_multi_device_path_bitwise_on_oversubscribed_devices(n_dev):
+    """the in-process multi-device path (engine.cpp: one shard per device,
+    contiguous subtrees of the chunk range, host combine of the exact digits)
+    run with its shards placed round-robin on the visible devices: bitwise
+    the single-device value, for NLL, batched NLL and binned chi2 (no kernel
+    waits on another, so sharing one GPU is safe)"""
+    x, pdf = mixture()
+    rng = np.random.default_rng(21)
+    ds = pf.UnbinnedDataSet.from_columns([x], 10.0 * rng.random(1_000_003))
+    one = pf.BoundModel(pdf, ds)
+    many = pf.BoundModel(pdf, ds, pf.GridSpec(), pf.Backend.gpus(n_dev, oversubscribe=True))
+    p = one.registry().export_values()
+    assert many.eval_metric(p) == one.eval_metric(p)
+    assert many.log_floor_count() == one.log_floor_count()
+    pts = np.array([p, [0.3, -0.5, 4.9, 1.1], [0.5, -0.7, 5.2, 0.9]])
+    assert np.array_equal(many.eval_metric_batch(pts), one.eval_metric_batch(pts))
+    W = WORKLOADS["C4"]
+    obs, cpdf = W.build(pf)
+    b = W.data(pf, obs, 20_000, seed=3)
+    c1 = pf.BoundModel(cpdf, b, pf.GridSpec(W.grid))
+    cn = pf.BoundModel(cpdf, b, pf.GridSpec(W.grid), pf.Backend.gpus(n_dev, oversubscribe=True))
+    q = c1.registry().export_values()
+    assert cn.eval_metric(q, pf.MetricKind.ChiSquared) == c1.eval_metric(q, pf.MetricKind.ChiSquared)
+
+
+def test_more_devices_than_visible_is_refused():
+    import torch
+    x, pdf = mixture()
+    ds = pf.UnbinnedDataSet.from_columns([x], 10.0 * np.random.default_rng(1).random(1000))
+    with pytest.raises(pf.Error) as ei:
+        pf.BoundModel(pdf, ds, pf.GridSpec(), pf.Backend.gpus(torch.cuda.device_count() * 2))
+    assert ei.value.args[0].startswith("bad-backend")
