@@ -322,7 +322,7 @@ int pf_fit(pf_model* model, int32_t metric, const pf_fit_config* config, const d
 }  // extern "C"
 
 extern "C" PF_API int64_t pf_debug_trace(pf_model* model, uint64_t* out, int64_t n) {
-  if (!model || !out || n <= 0) return 0;
+  if (!model || !out || n == 0) return 0;  // n < 0: the per-warp trace buffer
   try {
     return model->impl->debug_trace(out, n);
   } catch (...) {

@@ -99,8 +99,10 @@ struct pf_args {
   int npin;             // K = 1: parameters passed inline (pin[0..npin))
   int s_smem;            // S staged in the event pass's shared memory (models with conv tables)
   long long* big;       // K x PF_BIG_STRIDE: wide accumulator of chunk sums >= 2^62 (pf_big_add)
-  pf_u32* ticket;       // fused pass: dynamic chunk counter (self-resetting)
+  pf_u32* ticket;       // (unused: reserved)
   int fused;            // 1: this launch is the single fused kernel (setup in every CTA)
+  int nwa;              // fused pass: active warps (static balanced schedule)
+  int kpw;              // fused pass: chunks per active warp (at most)
   pf_u32 gmask;         // K = 1 inline: bit 0 = count this call's grid clamps
   const pf_u32* hmask;  // host-mapped: bit k = parameter set k recomputes its norms
                         // (the reference's fingerprint cache, pdf.hpp:111-123)

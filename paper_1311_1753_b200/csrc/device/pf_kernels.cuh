@@ -27,6 +27,7 @@ __device__ __forceinline__ unsigned long long pf_gtime() {
 // per block: [in, prologue done, PDL wait done, main loop done, block done,
 // published]; setup: slot 0 of block 4095 (in), slot 1 (out)
 __device__ unsigned long long pf_trace_buf[4096 * 6];
+__device__ unsigned long long pf_trace_w[4096 * 2];
 #define PF_ETRACE(slot, v) (pf_trace_buf[(pf_u64)blockIdx.x * 6 + (slot)] = (v))
 #endif
 __device__ __forceinline__ void pf_pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
@@ -87,8 +88,9 @@ template <int CL>
 __device__ __forceinline__ void pf_setup_core(const pf_args& a, int k, unsigned rank, double* P, double* S,
                                               pf_krec* r, bool init_rec, pf_ctx& cx, pf_cnt& cnt,
                                               pf_cnt& cnt_stage) {
-  // this CTA's warp partials per task (double-double), double-buffered by level parity
-  __shared__ pf_dd wpart[2][PF_SETUP_MAXQ][PF_SETUP_THREADS / 32];
+  // this CTA's run partials per task (double-double), double-buffered by level parity
+  __shared__ pf_dd wpart[2][PF_SETUP_MAXQ][4];
+  __shared__ double red[PF_SETUP_MAXQ][PF_SETUP_THREADS];  // the threads' partials
   __shared__ pf_task tk[16];
 #ifdef PF_SETUP_TRACE
   __shared__ long long trs[32];
@@ -127,70 +129,71 @@ __device__ __forceinline__ void pf_setup_core(const pf_args& a, int k, unsigned 
     // double is the correctly rounded sum, as the reference's long double
     // sum rounded to double (pdf.hpp:163-175) nearly always is, and the same
     // for the cluster, single-CTA (fused) and multi-block paths.
+    // one loop per task (constant q: no per-point task search); the loops'
+    // few iterations are independent evaluations
     double x[PF_SETUP_MAXQ];
 #pragma unroll
-    for (int q = 0; q < PF_SETUP_MAXQ; ++q) x[q] = 0.0;
-    // the level's midpoints as one index space (task q owns [off[q], off[q+1])):
-    // a thread's few points are independent evaluations whose latencies
-    // overlap, instead of one short loop per task
-    pf_u64 off[PF_SETUP_MAXQ + 1];
-    off[0] = 0;
-#pragma unroll
-    for (int q = 0; q < PF_SETUP_MAXQ; ++q) off[q + 1] = off[q] + (q < nl ? tk[t0 + q].points : 0ull);
-#pragma unroll 2
-    for (pf_u64 g = rank * PF_SETUP_THREADS + threadIdx.x; g < off[PF_SETUP_MAXQ]; g += PF_SETUP_THREADS * CL) {
-      int q = 0;
-      pf_u64 first = 0;  // (constant indices only: off[] stays in registers)
-#pragma unroll
-      for (int qq = 1; qq < PF_SETUP_MAXQ; ++qq)
-        if (g >= off[qq]) {
-          q = qq;
-          first = off[qq];
-        }
-      const pf_task& T = tk[t0 + q];
-      const double v = pf_norm_point(T.node, g - first, T, P, S, a.C, cx, cnt);
-#pragma unroll
-      for (int qq = 0; qq < PF_SETUP_MAXQ; ++qq) x[qq] += qq == q ? v : 0.0;
+    for (int q = 0; q < PF_SETUP_MAXQ; ++q) {
+      x[q] = 0.0;
+      if (q < nl) {
+        const pf_task& T = tk[t0 + q];
+        const pf_u64 np = T.points;
+#pragma unroll 4
+        for (pf_u64 g = rank * PF_SETUP_THREADS + threadIdx.x; g < np; g += PF_SETUP_THREADS * CL)
+          x[q] += pf_norm_point(T.node, g, T, P, S, a.C, cx, cnt);
+      }
     }
     PF_TRACE("points");
-    // warp trees of all the level's sums together (double-double)
-    pf_dd xd[PF_SETUP_MAXQ];
+    // the threads' partials through shared memory; then warp w sums run
+    // (w % 4) of task (w / 4) -- 128 partials -- in double-double and 4 runs
+    // per task are added in double-double: every task's sum is good to
+    // ~1e-17 relative for a fraction of the cost of per-warp trees of all tasks
 #pragma unroll
-    for (int q = 0; q < PF_SETUP_MAXQ; ++q) xd[q] = pf_dd{x[q], 0.0};
+    for (int q = 0; q < PF_SETUP_MAXQ; ++q) red[q][threadIdx.x] = x[q];
+    __syncthreads();
+    static_assert(PF_SETUP_THREADS == 512, "16 warps: 4 runs of 128 partials for each of 4 tasks per pass");
+    for (int q0 = 0; q0 < nl; q0 += 4) {
+      const int q = q0 + warp / 4;
+      if (q < nl) {
+        const int base = (warp % 4) * 128;
+        pf_dd acc = pf_dd_zero();
 #pragma unroll
-    for (int d = 16; d > 0; d >>= 1) {
+        for (int i = 0; i < 4; ++i) acc = pf_dd_add_d(acc, red[q][base + 32 * i + lane]);
 #pragma unroll
-      for (int q = 0; q < PF_SETUP_MAXQ; ++q) xd[q] = pf_dd_add(xd[q], pf_shfl_down_dd(xd[q], d));
+        for (int d = 16; d > 0; d >>= 1) acc = pf_dd_add(acc, pf_shfl_down_dd(acc, d));
+        if (lane == 0) wpart[level & 1][q][warp % 4] = acc;
+      }
     }
-    if (lane == 0)
-#pragma unroll
-      for (int q = 0; q < PF_SETUP_MAXQ; ++q) wpart[level & 1][q][warp] = xd[q];
     PF_TRACE("wtree");
-    // warp partials of every rank visible cluster-wide (double-buffered by
-    // level parity: a rank cannot overwrite a buffer another rank may still
-    // read without first passing the next level's barrier)
+    // partials of every rank visible cluster-wide (double-buffered by level
+    // parity: a rank cannot overwrite a buffer another rank may still read
+    // without first passing the next level's barrier)
     if (CL > 1)
       pf_cluster_sync();
     else
       __syncthreads();
     PF_TRACE("csync");
     // one warp per node: lanes 0-15 its coarse sum, lanes 16-31 its fine sum;
-    // lane l holds warp partial (l & 15) of every rank, combined over ranks by
-    // a fixed tree, then a 16-lane tree; lane 0 finishes the node
+    // lane l < 4 of each half holds run l of every rank, combined over ranks
+    // by a fixed tree, then a 4-lane tree; lane 0 finishes the node
     if (2 * warp < nl) {
       const int q = 2 * warp + (lane >> 4);
-      const pf_dd* src = &wpart[level & 1][q][lane & 15];
-      pf_dd v[CL];
+      const int l = lane & 15;
+      pf_dd y = pf_dd_zero();
+      if (l < 4) {
+        const pf_dd* src = &wpart[level & 1][q][l];
+        pf_dd v[CL];
 #pragma unroll
-      for (int rk = 0; rk < CL; ++rk)
-        v[rk] = CL > 1 ? pf_dd{pf_dsmem_load(&src->hi, (unsigned)rk), pf_dsmem_load(&src->lo, (unsigned)rk)} : *src;
+        for (int rk = 0; rk < CL; ++rk)
+          v[rk] = CL > 1 ? pf_dd{pf_dsmem_load(&src->hi, (unsigned)rk), pf_dsmem_load(&src->lo, (unsigned)rk)} : *src;
 #pragma unroll
-      for (int w = 1; w < CL; w <<= 1)
+        for (int w = 1; w < CL; w <<= 1)
 #pragma unroll
-        for (int rk = 0; rk + w < CL; rk += 2 * w) v[rk] = pf_dd_add(v[rk], v[rk + w]);
-      pf_dd y = v[0];
+          for (int rk = 0; rk + w < CL; rk += 2 * w) v[rk] = pf_dd_add(v[rk], v[rk + w]);
+        y = v[0];
+      }
 #pragma unroll
-      for (int d = 8; d > 0; d >>= 1) y = pf_dd_add(y, pf_shfl_down_dd(y, d));
+      for (int d = 2; d > 0; d >>= 1) y = pf_dd_add(y, pf_shfl_down_dd(y, d));
       // midpoint_sum returns static_cast<double>(sum) * vol (pdf.hpp:173-175)
       const double sum = __dmul_rn(pf_dd_to_double(y), tk[t0 + q].vol);
       const double fine = __shfl_down_sync(0xffffffffu, sum, 16);
@@ -1139,10 +1142,11 @@ extern "C" __global__ void __launch_bounds__(PF_EV_THREADS, PF_EVENT_MIN_BLOCKS)
 // copies are in flight -- the setup work is a few thousand raw evaluations,
 // cheaper to repeat per SM than to hand over through a second grid -- and
 // then streams its chunks.  Chunks (fixed event ranges: the reduction unit,
-// so the result does not depend on the schedule) are taken dynamically from
-// a self-resetting ticket counter, two ahead, so every warp of every SM stays
-// busy to the end.  Lane accumulators live in registers; one exact block
-// total per CTA; the last CTA rounds and publishes (pf_finalize_warp0).
+// so the result does not depend on the schedule) go to a balanced set of
+// active warps, every chunk of a warp prefetched into L2 at entry so HBM
+// streams the whole pass while the setup runs.  Lane accumulators live in
+// registers; one exact block total per CTA; the last CTA rounds and
+// publishes (pf_finalize_warp0).
 #ifndef PF_FUSED_WARPS
 #define PF_FUSED_WARPS 16
 #endif
@@ -1164,35 +1168,47 @@ extern "C" __global__ void __launch_bounds__(PF_FUSED_THREADS, 1) pf_fused_kerne
   const int warp = threadIdx.x >> 5;
   double* my = stages + warp * PF_NST * PF_STAGE;
   pf_u64* mybar = bars + warp * PF_NST;
-  const int nw = gridDim.x * PF_FUSED_WARPS;
-  const int gw = blockIdx.x * PF_FUSED_WARPS + warp;
   const int nch = a.n_chunks;
-  // lane 0's chunk schedule: the current and next chunk, and the ticket for
-  // the one after (chunk ids >= nch mean "no more work")
-  int c_cur = gw, c_nxt = gw + nw, c_pend = nch;
+  // Static balanced schedule: nwa active warps (host: nwa = ceil(nch / kpw),
+  // kpw = ceil(nch / all warps)), spread evenly over the SMs (warp-major
+  // index), each taking chunks gw, gw + nwa, ... -- every active warp has kpw
+  // chunks (the last ones one fewer), so no warp runs a lone extra round.
+  const int nwa = a.nwa;
+  const int gw = warp * gridDim.x + blockIdx.x;
+  const bool active = gw < nwa;
+  int n_mine = active ? (nch - 1 - gw) / nwa + 1 : 0;
+  if (n_mine > a.kpw) n_mine = a.kpw;
   if (lane == 0) {
     for (int s = 0; s < PF_NST; ++s) pf_mbar_init(mybar + s, 1);
     pf_fence_mbar_init();
-    if (c_nxt < nch) c_pend = 2 * nw + (int)atomicAdd(a.ticket, 1u);
-  }
-  // sub-chunk v of this warp (v / PF_NSUB chunks after the current one, 0 or 1)
-  auto issue = [&](int v, int vbase) {
-    if (lane == 0) {
-      const int c = (v / PF_NSUB) == vbase ? c_cur : c_nxt;
-      if (c < nch) {
-        const int st = v % PF_NST;
-        const pf_u64 base = (pf_u64)c * (PF_SUB * PF_NSUB) + (pf_u64)(v % PF_NSUB) * PF_SUB;
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        pf_mbar_expect_tx(mybar + st, PF_STAGE * 8);
+#ifndef PF_NO_L2_PREFETCH
+    // every chunk of this warp into L2 now: HBM streams the whole pass while
+    // the setup below runs, and the TMA copies of the loop hit L2
+    for (int j = 0; j < n_mine; ++j) {
+      const pf_u64 b = (pf_u64)(gw + j * nwa) * (PF_SUB * PF_NSUB);
 #pragma unroll
-        for (int q = 0; q < PF_NLOAD; ++q)
-          pf_tma_load(my + st * PF_STAGE + q * PF_SUB, a.data + (pf_u64)pf_load_col(q) * a.col_stride + base,
-                      PF_SUB * 8, mybar + st);
-      }
+      for (int q = 0; q < PF_NLOAD; ++q)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.data + (pf_u64)pf_load_col(q) * a.col_stride + b),
+                     "r"((unsigned)(PF_SUB * PF_NSUB * 8))
+                     : "memory");
+    }
+#endif
+  }
+  // sub-chunk v of this warp: chunk gw + (v / PF_NSUB) nwa
+  auto issue = [&](int v) {
+    if (lane == 0 && v < n_mine * PF_NSUB) {
+      const int c = gw + (v / PF_NSUB) * nwa;
+      const int st = v % PF_NST;
+      const pf_u64 base = (pf_u64)c * (PF_SUB * PF_NSUB) + (pf_u64)(v % PF_NSUB) * PF_SUB;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      pf_mbar_expect_tx(mybar + st, PF_STAGE * 8);
+#pragma unroll
+      for (int q = 0; q < PF_NLOAD; ++q)
+        pf_tma_load(my + st * PF_STAGE + q * PF_SUB, a.data + (pf_u64)pf_load_col(q) * a.col_stride + base,
+                    PF_SUB * 8, mybar + st);
     }
   };
-  static_assert(PF_NST <= PF_NSUB, "the fused ring runs at most one chunk ahead");
-  for (int v = 0; v < PF_NST; ++v) issue(v, 0);
+  for (int v = 0; v < PF_NST; ++v) issue(v);
   // the setup, redundantly in every CTA, while the first stages stream in
   pf_krec* r = a.rec;
   pf_ctx cx;
@@ -1223,9 +1239,11 @@ extern "C" __global__ void __launch_bounds__(PF_FUSED_THREADS, 1) pf_fused_kerne
   long long* big = a.big;
   pf_lacc acc;
   int w = 0;  // sub-chunks consumed by this warp
-  while (__shfl_sync(0xffffffffu, c_cur, 0) < nch) {
-    const int c = __shfl_sync(0xffffffffu, c_cur, 0);
-    const int vb = w / PF_NSUB;
+#ifdef PF_EVENT_TRACE
+  const int n_done = n_mine;
+#endif
+  for (int jc = 0; jc < n_mine; ++jc) {
+    const int c = gw + jc * nwa;
     for (int j = 0; j < PF_NSUB; ++j, ++w) {
       const int st = w % PF_NST;
       pf_mbar_wait(mybar + st, (unsigned)((w / PF_NST) & 1));
@@ -1236,32 +1254,19 @@ extern "C" __global__ void __launch_bounds__(PF_FUSED_THREADS, 1) pf_fused_kerne
                              : pf_stage_terms<false>(a, 0, base, lane, my + st * PF_STAGE, n_valid, fk, P, S);
       acc = j == 0 ? t : pf_lacc_merge(acc, t);
       __syncwarp();
-      issue(w + PF_NST, vb);  // refills the stage just read
+      issue(w + PF_NST);  // refills the stage just read
     }
     // chunk done: its exact value into the lane's fixed-point accumulator
     const pf_dd tv = pf_lacc_terms(acc, P);
     pf_fxl_add_w(F, tv.hi, big);
     pf_fxl_add_w(F, tv.lo, big);
-    if (lane == 0) {  // next chunk; take the ticket after it
-      c_cur = c_nxt;
-      c_nxt = c_pend;
-      c_pend = nch;
-      if (c_nxt < nch) {
-        c_pend = 2 * nw + (int)atomicAdd(a.ticket, 1u);
-#ifdef PF_L2_PREFETCH
-        // the chunk after this one into L2 now: its TMA copies later hit L2
-        const pf_u64 b = (pf_u64)c_nxt * (PF_SUB * PF_NSUB);
-#pragma unroll
-        for (int q = 0; q < PF_NLOAD; ++q)
-          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.data + (pf_u64)pf_load_col(q) * a.col_stride + b),
-                       "r"((unsigned)(PF_SUB * PF_NSUB * 8))
-                       : "memory");
-#endif
-      }
-    }
   }
 #ifdef PF_EVENT_TRACE
   const unsigned long long t_loop = pf_gtime();
+  if (lane == 0 && gw < 4096) {  // per warp: chunks taken, loop end
+    pf_trace_w[2 * gw] = (unsigned long long)n_done;
+    pf_trace_w[2 * gw + 1] = t_loop;
+  }
   __shared__ unsigned long long t_loop_max;
   if (threadIdx.x == 0) t_loop_max = 0;
   __syncthreads();
@@ -1303,10 +1308,7 @@ extern "C" __global__ void __launch_bounds__(PF_FUSED_THREADS, 1) pf_fused_kerne
 #ifdef PF_EVENT_TRACE
   if (threadIdx.x == 0) pf_trace_buf[4094 * 6 + 0] = pf_gtime();
 #endif
-  if (threadIdx.x == 0) {
-    *a.done = 0u;     // self-resetting (every CTA has arrived)
-    *a.ticket = 0u;   // every ticket has been taken and consumed
-  }
+  if (threadIdx.x == 0) *a.done = 0u;  // self-resetting (every CTA has arrived)
   if (warp == 0) pf_finalize_warp0(a, lane, S);
 #ifdef PF_EVENT_TRACE
   if (threadIdx.x == 0) pf_trace_buf[4094 * 6 + 2] = pf_gtime();

@@ -117,10 +117,17 @@ const Module* load_module(const Layout& L, int device) {
   ck(cudaKernelSetAttributeForDevice(m->event, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(event_smem_max(L)), device),
      "event kernel smem attribute");
-  if (fused_smem(L) <= 200 * 1024)
-    ck(cudaKernelSetAttributeForDevice(m->fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(fused_smem(L)), device),
-       "fused kernel smem attribute");
+  {
+    cudaFuncAttributes fa{};
+    if (cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(m->fused)) == cudaSuccess)
+      m->fused_static_smem = fa.sharedSizeBytes;
+    else
+      m->fused_static_smem = 64 * 1024, cudaGetLastError();
+    if (fused_smem(L) + m->fused_static_smem <= kFusedSmemLimit)
+      ck(cudaKernelSetAttributeForDevice(m->fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(fused_smem(L)), device),
+         "fused kernel smem attribute");
+  }
   c.modules.emplace(key, m);
   return m;
 }
@@ -552,6 +559,12 @@ cudaGraphExec_t Model::graph_for(Shard& sh, int K) {
     Args f = a;
     f.clamp = sh.d_clamp;
     f.fused = 1;
+    {  // balanced static schedule: kpw chunks for each of nwa active warps
+      const int all = sm_count(sh.device) * kFusedWarps;
+      const int n = std::max(sh.n_chunks, 1);
+      f.kpw = (n + all - 1) / all;
+      f.nwa = (n + f.kpw - 1) / f.kpw;
+    }
     launch(sh.mod->fused, dim3(sm_count(sh.device)), dim3(32 * kFusedWarps), fused_smem(L_), sh.stream, f);
     ++kernels;
     sh.event_args = f;
@@ -621,8 +634,8 @@ cudaGraphExec_t Model::graph_for(Shard& sh, int K) {
 bool Model::fused_ok(const Shard& sh) const {
   if (const char* env = std::getenv("PFB200_FUSED"))
     if (std::atoi(env) == 0) return false;
-  return small_norms_ && sh.n_local > 0 && L_.nst <= L_.nsub && fused_smem(L_) <= 200 * 1024 &&
-         L_.setup_maxq <= 8;
+  return small_norms_ && sh.n_local > 0 && L_.nst <= L_.nsub &&
+         fused_smem(L_) + sh.mod->fused_static_smem <= kFusedSmemLimit && L_.setup_maxq <= 8;
 }
 
 void Model::check_call(size_t n, int metric) const {
@@ -991,7 +1004,10 @@ int64_t Model::debug_trace(uint64_t* out, int64_t n) {
   Shard& sh = shards_[0];
   void* ptr = nullptr;
   size_t bytes = 0;
-  if (cudaLibraryGetGlobal(&ptr, &bytes, sh.mod->lib, "pf_trace_buf") != cudaSuccess || !ptr) {
+  // n < 0: the per-warp buffer (pf_trace_w) instead of the per-block one
+  const char* name = n < 0 ? "pf_trace_w" : "pf_trace_buf";
+  if (n < 0) n = -n;
+  if (cudaLibraryGetGlobal(&ptr, &bytes, sh.mod->lib, name) != cudaSuccess || !ptr) {
     cudaGetLastError();
     return 0;
   }

@@ -95,8 +95,10 @@ struct Args {
   int npin;
   int s_smem;  // the event pass stages S in shared memory (event_s_staged)
   int64_t* big;  // kMaxBatch x kBigStride wide accumulator (pf_big_add)
-  uint32_t* ticket;  // fused pass: dynamic chunk counter
+  uint32_t* ticket;  // (unused: reserved)
   int fused;
+  int nwa;  // fused pass: active warps
+  int kpw;  // fused pass: chunks per active warp
   uint32_t gmask;          // K = 1 inline: count this call's grid clamps (bit 0)
   const uint32_t* hmask;   // mapped: bit k = parameter set k recomputes its norms
   double pin[64];
@@ -106,6 +108,7 @@ struct Module {
   cudaLibrary_t lib = nullptr;
   cudaKernel_t setup = nullptr, pre = nullptr, norm = nullptr, event = nullptr, final = nullptr,
                publish = nullptr, fused = nullptr;
+  size_t fused_static_smem = 0;  // static shared memory of pf_fused_kernel
   // generator modules only (PF_GEN, pf_generate.cuh)
   cudaKernel_t gen_max = nullptr, gen_mt = nullptr, gen_mt_jump = nullptr, gen_eval = nullptr,
                gen_scan = nullptr, gen_scatter = nullptr;
@@ -161,6 +164,7 @@ void subtree_range(uint64_t n, int shard_count, int index, uint64_t* lo, uint64_
 size_t event_smem(const Layout& L, int K);
 size_t fused_smem(const Layout& L);
 constexpr int kFusedWarps = 16;  // PF_FUSED_WARPS
+constexpr size_t kFusedSmemLimit = 227 * 1024;  // static + dynamic shared memory of one CTA
 bool event_s_staged(const Layout& L, int K);
 int sm_count(int device);
 

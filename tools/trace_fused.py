@@ -30,3 +30,14 @@ for name, col in zip(["enter", "setup done", "loop done", "block done"], range(4
     print("%-11s min %7.2f  median %7.2f  max %7.2f us" % (name, v.min(), np.median(v), v.max()))
 print("finalize: starts %.2f, ends %.2f us" % ((t[4094, 0] - t0) / 1000, (t[4094, 2] - t0) / 1000))
 print("CTAs traced:", len(blk))
+wb = (C.c_uint64 * (4096 * 2))()
+pf.lib.pf_debug_trace(bm._h, wb, -4096 * 2)
+w = np.frombuffer(wb, dtype=np.uint64).reshape(4096, 2).astype(np.float64)
+w = w[w[:, 1] > 0]
+cnt = w[:, 0]
+end = (w[:, 1] - t0) / 1000.0
+print("warps %d: chunks per warp min %d median %d max %d; loop end min %.2f median %.2f p90 %.2f max %.2f us"
+      % (len(w), cnt.min(), np.median(cnt), cnt.max(), end.min(), np.median(end), np.percentile(end, 90), end.max()))
+for c in sorted(set(cnt.astype(int))):
+    e = end[cnt == c]
+    print("  warps with %d chunks: %4d  end median %.2f max %.2f" % (c, len(e), np.median(e), e.max()))
