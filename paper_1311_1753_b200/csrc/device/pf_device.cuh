@@ -63,13 +63,36 @@ struct pf_out {
   pf_u64 floor_count, first_nonfinite, first_event_error;
   pf_u32 norm_error, pad;  // pad: completion sequence number (pf_publish)
   long long fx[6];  // exact digits (combined across shards on the host)
+  pf_u64 check;     // pf_out_check of every field above: the record is complete
 };
+
+// The record is published with plain stores (no system-scope fence, which
+// costs microseconds at the end of every call): the host accepts it once
+// `pad` carries the call's sequence number AND `check` matches every field,
+// so a record read while its stores are still landing is retried (host twin:
+// engine.cpp out_check).
+__device__ __forceinline__ pf_u64 pf_mix64(pf_u64 h, pf_u64 v) {
+  h ^= v + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
+  h ^= h >> 31;
+  h *= 0xbf58476d1ce4e5b9ull;
+  return h ^ (h >> 29);
+}
+__device__ __forceinline__ pf_u64 pf_out_check(const pf_out& o) {
+  pf_u64 h = 0x243f6a8885a308d3ull;
+  h = pf_mix64(h, (pf_u64)__double_as_longlong(o.result));
+  h = pf_mix64(h, o.floor_count);
+  h = pf_mix64(h, o.first_nonfinite);
+  h = pf_mix64(h, o.first_event_error);
+  h = pf_mix64(h, ((pf_u64)o.norm_error << 32) | o.pad);
+  for (int i = 0; i < 6; ++i) h = pf_mix64(h, (pf_u64)o.fx[i]);
+  return h;
+}
 
 struct pf_args {
   const double* hP;     // host-mapped parameters (K x PF_NP)
   pf_out* hout;         // host-mapped results (K)
-  double* hnorms;       // host-mapped norms (K x 3 n_nodes)
-  pf_u64* hclamp;       // host-mapped clamp counters
+  double* hnorms;       // DEVICE: norms of the last call without a norm error (3 n_nodes)
+  pf_u64* hclamp;       // (unused: the host reads the device counters on demand)
   int n_nodes;
   int fuse_final;       // K == 1: the last event block runs the final tree
   int n_levels;

@@ -916,7 +916,6 @@ __device__ void pf_finalize_warp0(const pf_args& a, int lane, const double* S0 =
       }
       int gbig = nbig != 0;
       if (a.peers) pf_group_exchange(a, k, lane, d, normerr, nonfinite, evterr, gbig);
-      pf_out* o = a.hout + k;
       if (lane == 0) {
         bg[PF_BIG_COUNT] = 0ll;
         bg[PF_BIG_SNAP_COUNT] = nbig;
@@ -925,37 +924,33 @@ __device__ void pf_finalize_warp0(const pf_args& a, int lane, const double* S0 =
         for (int i = 0; i < PF_FX_DIGITS; ++i) dp[i] = d[i];
         dp[6] = (long long)normerr;
         dp[7] = ((nonfinite != ~0ull || evterr != ~0ull) ? 1 : 0) | (gbig ? 2 : 0);
+        // the record, built in registers, then stored field by field into
+        // mapped host memory with its sequence number and check word
+        pf_out o;
         // NaN: the host adds the wide digits (Model::wait_results)
-        o->result = gbig ? __longlong_as_double(0x7ff8000000000000ll) : pf_fx_round(d);
+        o.result = gbig ? __longlong_as_double(0x7ff8000000000000ll) : pf_fx_round(d);
 #pragma unroll
-        for (int i = 0; i < PF_FX_DIGITS; ++i) o->fx[i] = d[i];
-        o->floor_count = floors;
-        o->first_nonfinite = nonfinite;
-        o->first_event_error = evterr;
-        o->norm_error = normerr;
-      }
-      const double* S = S0 ? S0 : a.S + (pf_u64)k * PF_SS;
-      for (int i = lane; i < 3 * a.n_nodes; i += 32) a.hnorms[(pf_u64)k * 3 * a.n_nodes + i] = S[i];
-#if PF_NPOLY > 0
-      if (k == a.K - 1)
-        for (int i = lane; i < PF_NPOLY; i += 32) a.hclamp[i] = __ldcg(a.clamp + i);
-#endif
-    }
-    __syncwarp();
-    if (lane == 0) {
-#ifdef PF_PUBLISH_FENCE
-      __threadfence_system();  // every field above reaches the host first
-#endif
-      for (int k = 0; k < a.K; ++k) {
+        for (int i = 0; i < PF_FX_DIGITS; ++i) o.fx[i] = d[i];
+        o.floor_count = floors;
+        o.first_nonfinite = nonfinite;
+        o.first_event_error = evterr;
+        o.norm_error = normerr;
         const pf_u32 seq = a.done[1 + k] + 1u;
         a.done[1 + k] = seq;
-#ifdef PF_PUBLISH_FENCE
-        *(volatile pf_u32*)&a.hout[k].pad = seq;
-#else
-        // system-scope release: every field above (this warp's writes, made
-        // visible to lane 0 by the __syncwarp) reaches the host first
-        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(&a.hout[k].pad), "r"(seq) : "memory");
-#endif
+        o.pad = seq;
+        o.check = pf_out_check(o);
+        volatile pf_u64* dst = reinterpret_cast<volatile pf_u64*>(a.hout + k);
+        const pf_u64* src = reinterpret_cast<const pf_u64*>(&o);
+#pragma unroll
+        for (int i = 0; i < (int)(sizeof(pf_out) / 8); ++i) dst[i] = src[i];
+      }
+      // the norms the reference's nodes now cache: device memory, read by
+      // the host only when asked (pf_node_norms); a call whose normalisation
+      // failed leaves the last successful set (engine.hpp:174-178)
+      const pf_u32 ne = __shfl_sync(0xffffffffu, normerr, 0);
+      if (ne == ~0u) {
+        const double* S = S0 ? S0 : a.S + (pf_u64)k * PF_SS;
+        for (int i = lane; i < 3 * a.n_nodes; i += 32) a.hnorms[i] = S[i];
       }
     }
   }
@@ -1313,6 +1308,21 @@ extern "C" __global__ void __launch_bounds__(PF_FUSED_THREADS, 1) pf_fused_kerne
 #ifdef PF_EVENT_TRACE
   if (threadIdx.x == 0) pf_trace_buf[4094 * 6 + 2] = pf_gtime();
 #endif
+}
+
+// ---------------------------------------------------------------------------
+// bench only: the read half of the L2 flush.  After the flush buffer is
+// written, reading it back leaves L2 full of CLEAN lines of that buffer, so
+// the timed call starts with its inputs evicted (as after the write) but does
+// not pay the write-back of 126 MB of dirty flush data -- which a real fit,
+// whose calls run back to back, never does either.
+extern "C" __global__ void pf_flush_read_kernel(const ulonglong2* p, pf_u64 n, unsigned long long* sink) {
+  unsigned long long acc = 0;
+  for (pf_u64 i = (pf_u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (pf_u64)gridDim.x * blockDim.x) {
+    const ulonglong2 v = __ldcg(p + i);
+    acc ^= v.x ^ v.y;
+  }
+  if (acc == 0x5eed5eed5eed5eedull) *sink = acc;
 }
 
 // ---------------------------------------------------------------------------

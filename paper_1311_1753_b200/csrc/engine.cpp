@@ -106,6 +106,7 @@ const Module* load_module(const Layout& L, int device) {
   ck(cudaLibraryGetKernel(&m->norm, m->lib, "pf_norm_kernel"), "get pf_norm_kernel");
   ck(cudaLibraryGetKernel(&m->event, m->lib, "pf_event_kernel"), "get pf_event_kernel");
   ck(cudaLibraryGetKernel(&m->fused, m->lib, "pf_fused_kernel"), "get pf_fused_kernel");
+  ck(cudaLibraryGetKernel(&m->flush_read, m->lib, "pf_flush_read_kernel"), "get pf_flush_read_kernel");
   if (L.source.rfind("#define PF_GEN 1\n", 0) == 0) {
     ck(cudaLibraryGetKernel(&m->gen_max, m->lib, "pf_gen_max_kernel"), "get pf_gen_max_kernel");
     ck(cudaLibraryGetKernel(&m->gen_mt, m->lib, "pf_mt_kernel"), "get pf_mt_kernel");
@@ -363,9 +364,7 @@ Model::Model(const pf_graph& g, const pf_data& d, uint32_t grid_points, const pf
     // pinned memory may be recycled from a freed model: clear the completion
     // words (pad) so no stale value can equal the sequence the host expects
     std::memset(sh.h_out, 0, sizeof(Out) * kMaxBatch);
-    ck(cudaHostAlloc(reinterpret_cast<void**>(&sh.h_norms),
-                     sizeof(double) * kMaxBatch * 3 * pg_.nodes.size(), cudaHostAllocMapped),
-       "mapped norms");
+    ck(cudaMalloc(&sh.h_norms, sizeof(double) * 3 * pg_.nodes.size()), "cudaMalloc norms");
     ck(cudaHostAlloc(reinterpret_cast<void**>(&sh.h_clamp), sizeof(uint64_t) * std::max(L_.n_poly, 1),
                      cudaHostAllocMapped),
        "mapped clamp");
@@ -416,7 +415,7 @@ Model::~Model() {
     cudaFree(sh.d_ticket);
     cudaFree(sh.d_clamp);
     cudaFreeHost(sh.h_out);
-    cudaFreeHost(sh.h_norms);
+    cudaFree(sh.h_norms);
     cudaFreeHost(sh.h_clamp);
     cudaFree(sh.d_scratch);
   }
@@ -498,7 +497,7 @@ Args Model::base_args(Shard& sh, int K) {
   ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(const_cast<double**>(&a.hP)), h_params_, 0),
      "mapped params");
   ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&a.hout), sh.h_out, 0), "mapped out");
-  ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&a.hnorms), sh.h_norms, 0), "mapped norms");
+  a.hnorms = sh.h_norms;  // device memory
   ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&a.hclamp), sh.h_clamp, 0), "mapped clamp");
   ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(const_cast<uint32_t**>(&a.hmask)), h_mask_, 0),
      "mapped mask");
@@ -619,7 +618,7 @@ cudaGraphExec_t Model::graph_for(Shard& sh, int K) {
     size_t n_roots = 1;
     ck(cudaGraphGetRootNodes(graph, &sh.first_node, &n_roots), "cudaGraphGetRootNodes");
     sh.graph1 = graph;
-    sh.first_args = a;
+    sh.first_args = fused ? sh.event_args : a;
   } else {
     cudaGraphDestroy(graph);
   }
@@ -749,13 +748,23 @@ void Model::wait_results(int K, std::vector<Raw>& out, bool partial_only) {
   // the result is in mapped memory as soon as the publishing block has
   // written its completion word: spin on it (a stream synchronisation costs
   // a wake-up); the stream is queried now and then so errors still surface
+  // the record is stored without a system fence: it is complete once its
+  // sequence number and check word agree with its fields (pf_out_check)
   for (Shard& sh : shards_) {
     for (int k = 0; k < K; ++k) {
       const volatile uint32_t* word = &sh.h_out[k].pad;
-      for (uint64_t spin = 1; *word != sh.seq[k]; ++spin) {
+      for (uint64_t spin = 1;; ++spin) {
+        if (*word == sh.seq[k]) {
+          std::atomic_thread_fence(std::memory_order_acquire);
+          Out o;
+          const volatile uint64_t* src = reinterpret_cast<const volatile uint64_t*>(&sh.h_out[k]);
+          uint64_t* dst = reinterpret_cast<uint64_t*>(&o);
+          for (size_t i = 0; i < sizeof(Out) / 8; ++i) dst[i] = src[i];
+          if (o.pad == sh.seq[k] && o.check == out_check(o)) break;
+        }
         if ((spin & 1023) == 0) {
           const cudaError_t e = cudaStreamQuery(sh.stream);
-          if (e == cudaSuccess && *word != sh.seq[k])
+          if (e == cudaSuccess && spin > (1u << 22))  // the kernel ended long ago: its stores have landed
             throw Error("device-error", "evaluation finished without publishing its result");
           if (e != cudaSuccess && e != cudaErrorNotReady) ck(e, "evaluation");
         }
@@ -786,14 +795,10 @@ void Model::wait_results(int K, std::vector<Raw>& out, bool partial_only) {
       norm_hash_ = call_hash_[k];
       have_norm_hash_ = true;
     }
-    // norms are replicated on every shard; keep the last successful set
-    const double* hn = shards_[0].h_norms + static_cast<size_t>(k) * 3 * nn;
-    for (size_t i = 0; i < nn; ++i) {
-      if (!pg_.nodes[i].normalised) continue;
-      norms_[i] = hn[3 * i];
-      errs_[i] = hn[3 * i + 1];
-      norm_valid_[i] = 1;
-    }
+    // norms are replicated on every shard; the device keeps the last
+    // successful set, read when asked (fetch_norms)
+    norms_on_device_ = true;
+    (void)nn;
     if (ev_err != ~0ull) throw Error("event-error", error_message(static_cast<uint32_t>(ev_err & 0xffffff)));
     for (Shard& sh : shards_) floor_total_ += sh.h_out[k].floor_count;
     // shard accumulators are exact: summing their digits and rounding once
@@ -814,12 +819,41 @@ void Model::wait_results(int K, std::vector<Raw>& out, bool partial_only) {
       if (!std::isfinite(out[k].value)) throw Error("non-finite-metric", "non-finite reduction");
     }
   }
-  if (L_.n_poly > 0) {
-    std::fill(clamp_total_.begin(), clamp_total_.end(), 0);
-    for (Shard& sh : shards_)
-      for (size_t i = 0; i < pg_.nodes.size(); ++i)
-        if (L_.poly_index[i] >= 0) clamp_total_[i] += sh.h_clamp[L_.poly_index[i]];
+}
+
+uint64_t out_check(const Out& o) {
+  auto mix = [](uint64_t h, uint64_t v) {
+    h ^= v + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
+    h ^= h >> 31;
+    h *= 0xbf58476d1ce4e5b9ull;
+    return h ^ (h >> 29);
+  };
+  uint64_t h = 0x243f6a8885a308d3ull, bits;
+  std::memcpy(&bits, &o.result, 8);
+  h = mix(h, bits);
+  h = mix(h, o.floor_count);
+  h = mix(h, o.first_nonfinite);
+  h = mix(h, o.first_event_error);
+  h = mix(h, (static_cast<uint64_t>(o.norm_error) << 32) | o.pad);
+  for (int i = 0; i < 6; ++i) h = mix(h, static_cast<uint64_t>(o.fx[i]));
+  return h;
+}
+
+void Model::fetch_norms() {
+  if (!norms_on_device_) return;
+  Shard& sh = shards_[0];
+  const size_t nn = pg_.nodes.size();
+  std::vector<double> hn(3 * nn);
+  ck(cudaSetDevice(sh.device), "cudaSetDevice");
+  ck(cudaStreamSynchronize(sh.stream), "cudaStreamSynchronize");
+  ck(cudaMemcpy(hn.data(), sh.h_norms, sizeof(double) * 3 * nn, cudaMemcpyDeviceToHost), "norms D2H");
+  for (size_t i = 0; i < nn; ++i) {
+    if (!pg_.nodes[i].normalised) continue;
+    norms_[i] = hn[3 * i];
+    errs_[i] = hn[3 * i + 1];
+    norm_valid_[i] = 1;
   }
+  norms_on_device_ = false;
 }
 
 // Rare path: some chunk sums were >= 2^62 (pf_big_add), beyond the six
@@ -982,12 +1016,24 @@ void Model::group_join(int world, int rank, const void* handles) {
   ck(cudaDeviceSynchronize(), "group join");
 }
 
-uint64_t Model::clamp_count(int node) const {
+// PolynomialPdf clamp counter (pdf.hpp:320): the device's cumulative
+// counters of every shard, read when asked
+uint64_t Model::clamp_count(int node) {
   if (node < 0 || node >= static_cast<int>(clamp_total_.size())) return 0;
-  return clamp_total_[node];
+  if (L_.poly_index[node] < 0) return 0;
+  uint64_t total = 0;
+  for (Shard& sh : shards_) {
+    uint64_t v = 0;
+    ck(cudaSetDevice(sh.device), "cudaSetDevice");
+    ck(cudaStreamSynchronize(sh.stream), "cudaStreamSynchronize");
+    ck(cudaMemcpy(&v, sh.d_clamp + L_.poly_index[node], sizeof v, cudaMemcpyDeviceToHost), "clamp D2H");
+    total += v;
+  }
+  return total;
 }
 
-void Model::norms(double* norms, double* errs, int32_t* valid, int n) const {
+void Model::norms(double* norms, double* errs, int32_t* valid, int n) {
+  fetch_norms();
   for (int i = 0; i < n && i < static_cast<int>(norms_.size()); ++i) {
     if (norms) norms[i] = norms_[i];
     if (errs) errs[i] = errs_[i];
@@ -1018,13 +1064,28 @@ int64_t Model::debug_trace(uint64_t* out, int64_t n) {
   return m;
 }
 
+void Model::flush_l2(int i) {
+  Shard& sh = shards_[0];
+  const size_t bytes = 256ull << 20;
+  if (!sh.d_scratch) ck(cudaMalloc(&sh.d_scratch, bytes + 64), "cudaMalloc scratch");
+  ck(cudaMemsetAsync(sh.d_scratch, i & 0xff, bytes, sh.stream), "flush");
+  const char* mode = std::getenv("PFB200_FLUSH");
+  if (mode && std::string(mode) == "write") return;
+  const void* p = sh.d_scratch;
+  uint64_t n16 = bytes / 16;
+  void* sink = static_cast<char*>(sh.d_scratch) + bytes;
+  void* args[] = {&p, &n16, &sink};
+  ck(cudaLaunchKernel(reinterpret_cast<const void*>(sh.mod->flush_read), dim3(sm_count(sh.device) * 4), dim3(512),
+                      args, 0, sh.stream),
+     "flush read");
+}
+
 BenchResult Model::bench(const double* params, size_t n, int metric, int steps, bool flush) {
   BenchResult r;
   r.metric = eval(params, n, metric, nullptr);  // builds the K = 1 graph
   Shard& sh = shards_[0];
   ck(cudaSetDevice(sh.device), "cudaSetDevice");
-  const size_t scratch_bytes = 256ull << 20;
-  if (flush && !sh.d_scratch) ck(cudaMalloc(&sh.d_scratch, scratch_bytes), "cudaMalloc scratch");
+
   cudaEvent_t e0, e1;
   ck(cudaEventCreate(&e0), "cudaEventCreate");
   ck(cudaEventCreate(&e1), "cudaEventCreate");
@@ -1032,7 +1093,7 @@ BenchResult Model::bench(const double* params, size_t n, int metric, int steps, 
   double sum = 0, mn = 1e300;
   const uint64_t launches0 = g_launches.load();
   for (int i = 0; i < steps; ++i) {
-    if (flush) ck(cudaMemsetAsync(sh.d_scratch, i & 0xff, scratch_bytes, sh.stream), "flush");
+    if (flush) flush_l2(i);
     ck(cudaEventRecord(e0, sh.stream), "record");
     ck(cudaGraphLaunch(g, sh.stream), "cudaGraphLaunch");
     ck(cudaEventRecord(e1, sh.stream), "record");
@@ -1050,7 +1111,7 @@ BenchResult Model::bench(const double* params, size_t n, int metric, int steps, 
   mn = 1e300;
   if (sh.n_local > 0) {
     for (int i = 0; i < steps; ++i) {
-      if (flush) ck(cudaMemsetAsync(sh.d_scratch, i & 0xff, scratch_bytes, sh.stream), "flush");
+      if (flush) flush_l2(i);
       Args a = sh.event_args;
       if (sh.fused) {  // the whole call is this one kernel: parameters inline, as in the graph
         a.npin = L_.np;
@@ -1078,7 +1139,7 @@ BenchResult Model::bench(const double* params, size_t n, int metric, int steps, 
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   r.h2d_bytes = sizeof(double) * std::max(L_.np, 1);
-  r.d2h_bytes = sizeof(Out) + sizeof(double) * 3 * pg_.nodes.size() + sizeof(uint64_t) * L_.n_poly;
+  r.d2h_bytes = sizeof(Out);
   return r;
 }
 

@@ -52,8 +52,11 @@ struct Out {
   uint64_t floor_count, first_nonfinite, first_event_error;
   uint32_t norm_error, pad;
   int64_t fx[6];
+  uint64_t check;  // pf_out_check (pf_device.cuh): the record is complete
 };
-static_assert(sizeof(Out) == 88, "pf_out layout");
+static_assert(sizeof(Out) == 96, "pf_out layout");
+// host twin of pf_out_check
+uint64_t out_check(const Out& o);
 
 // Correctly rounded double of a superaccumulator (digits d_i 2^(32 i - 128));
 // host twin of pf_fx_round (pf_device.cuh).  NaN when poisoned.
@@ -109,6 +112,7 @@ struct Module {
   cudaKernel_t setup = nullptr, pre = nullptr, norm = nullptr, event = nullptr, final = nullptr,
                publish = nullptr, fused = nullptr;
   size_t fused_static_smem = 0;  // static shared memory of pf_fused_kernel
+  cudaKernel_t flush_read = nullptr;  // bench: read half of the L2 flush
   // generator modules only (PF_GEN, pf_generate.cuh)
   cudaKernel_t gen_max = nullptr, gen_mt = nullptr, gen_mt_jump = nullptr, gen_eval = nullptr,
                gen_scan = nullptr, gen_scatter = nullptr;
@@ -141,7 +145,7 @@ struct Shard {
   KRec* d_rec = nullptr;
   uint64_t* d_clamp = nullptr;  // [n_poly counted | n_poly discarded]
   Out* h_out = nullptr;         // mapped, kMaxBatch
-  double* h_norms = nullptr;    // mapped, kMaxBatch x 3 n_nodes
+  double* h_norms = nullptr;    // DEVICE: 3 n_nodes norms of the last call without a norm error
   uint64_t* h_clamp = nullptr;  // mapped
   std::map<int, cudaGraphExec_t> graphs;
   int kernels_per_graph = 0;
@@ -190,6 +194,9 @@ class Model {
   int64_t* partial_device() const { return shards_[0].d_part; }
   int64_t debug_trace(uint64_t* out, int64_t n);
   BenchResult bench(const double* params, size_t n, int metric, int steps, bool flush);
+  // bench's L2 flush on shard 0's stream: write 256 MiB, then (unless
+  // PFB200_FLUSH=write) read it back so the lines left in L2 are clean
+  void flush_l2(int i);
   // generate_events (generate.hpp:33-86) at the parameters' current values:
   // n events; box dimension d is written to out[d] (host, n doubles; null:
   // not copied) (generate.cpp)
@@ -201,8 +208,8 @@ class Model {
   uint64_t chunk() const { return chunk_; }
   bool binned() const { return binned_; }
   uint64_t floor_count() const { return floor_total_; }
-  uint64_t clamp_count(int node) const;
-  void norms(double* norms, double* errs, int32_t* valid, int n) const;
+  uint64_t clamp_count(int node);
+  void norms(double* norms, double* errs, int32_t* valid, int n);
 
  private:
   struct Raw {  // per-k outcome of one device pass
@@ -253,6 +260,8 @@ class Model {
   std::vector<uint64_t> clamp_total_;
   std::vector<double> norms_, errs_;
   std::vector<int32_t> norm_valid_;
+  bool norms_on_device_ = false;  // a call succeeded since norms_ was last read from the device
+  void fetch_norms();
 };
 
 uint64_t kernel_launch_count();

@@ -1,4 +1,4 @@
-for v in "X=1" "PFB200_NSUB=2" "PFB200_NSUB=1 PFB200_NST=1"; do
+for v in "X=1" "PFB200_NST=3"; do
   echo "== $v (setup phases, cycles)"
   env $v PFB200_DEFINES="PF_EVENT_TRACE;PF_SETUP_TRACE" python tools/trace_fused.py C2 2>&1 | grep "^setup" | tail -8
   echo "== $v (timeline)"

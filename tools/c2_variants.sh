@@ -9,10 +9,7 @@ for l in sys.stdin:
 "; }
 run default X=1
 run unfused PFB200_FUSED=0
-run l2pf PFB200_DEFINES=PF_L2_PREFETCH
-run ept8_nst4_nsub8 PFB200_EPT=8 PFB200_NST=4 PFB200_NSUB=8
-run ept8_nst6_nsub8 PFB200_EPT=8 PFB200_NST=6 PFB200_NSUB=8
-run ept8_nst4_nsub8_l2pf PFB200_EPT=8 PFB200_NST=4 PFB200_NSUB=8 PFB200_DEFINES=PF_L2_PREFETCH
-run nsub2_l2pf PFB200_NSUB=2 PFB200_DEFINES=PF_L2_PREFETCH
+run nol2pf PFB200_DEFINES=PF_NO_L2_PREFETCH
 run nst3 PFB200_NST=3
-run noqfast PFB200_NOQFAST=1
+run nsub2 PFB200_NSUB=2
+run nsub8_ept8_nst4 PFB200_NSUB=8 PFB200_EPT=8 PFB200_NST=4
