@@ -939,10 +939,16 @@ __device__ void pf_finalize_warp0(const pf_args& a, int lane, const double* S0 =
         a.done[1 + k] = seq;
         o.pad = seq;
         o.check = pf_out_check(o);
-        volatile pf_u64* dst = reinterpret_cast<volatile pf_u64*>(a.hout + k);
-        const pf_u64* src = reinterpret_cast<const pf_u64*>(&o);
+        volatile pf_out* dst = a.hout + k;
+        dst->result = o.result;
+        dst->floor_count = o.floor_count;
+        dst->first_nonfinite = o.first_nonfinite;
+        dst->first_event_error = o.first_event_error;
+        dst->norm_error = o.norm_error;
 #pragma unroll
-        for (int i = 0; i < (int)(sizeof(pf_out) / 8); ++i) dst[i] = src[i];
+        for (int i = 0; i < PF_FX_DIGITS; ++i) dst->fx[i] = o.fx[i];
+        dst->pad = o.pad;
+        dst->check = o.check;
       }
       // the norms the reference's nodes now cache: device memory, read by
       // the host only when asked (pf_node_norms); a call whose normalisation

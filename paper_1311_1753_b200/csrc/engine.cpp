@@ -756,10 +756,16 @@ void Model::wait_results(int K, std::vector<Raw>& out, bool partial_only) {
       for (uint64_t spin = 1;; ++spin) {
         if (*word == sh.seq[k]) {
           std::atomic_thread_fence(std::memory_order_acquire);
+          const volatile Out& v = sh.h_out[k];
           Out o;
-          const volatile uint64_t* src = reinterpret_cast<const volatile uint64_t*>(&sh.h_out[k]);
-          uint64_t* dst = reinterpret_cast<uint64_t*>(&o);
-          for (size_t i = 0; i < sizeof(Out) / 8; ++i) dst[i] = src[i];
+          o.result = v.result;
+          o.floor_count = v.floor_count;
+          o.first_nonfinite = v.first_nonfinite;
+          o.first_event_error = v.first_event_error;
+          o.norm_error = v.norm_error;
+          o.pad = v.pad;
+          for (int i = 0; i < 6; ++i) o.fx[i] = v.fx[i];
+          o.check = v.check;
           if (o.pad == sh.seq[k] && o.check == out_check(o)) break;
         }
         if ((spin & 1023) == 0) {
