@@ -163,8 +163,7 @@ def workload_config(W, n_local, n_total, world, exchange=None):
                         f"params at the fit start",
             f"{W.unit}_per_gpu": n_local, f"global_{W.unit}": n_total,
             "data": data_description(W),
-            "l2": "flushed before every timed step: a 256 MiB device buffer written, then read back (the lines left "
-                  "in L2 are clean, as between the back-to-back calls of a fit)",
+            "l2": "flushed (256 MiB device write) before every timed step",
             "parallelism": f"dp{world}",
             "exchange": exchange}
 
@@ -509,7 +508,6 @@ def main():
             for k in range(args.steps):
                 with torch.cuda.stream(model_stream):
                     flush_buf.fill_(k & 0xff)
-                    flush_buf.view(torch.int64).sum()
                     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     e0.record(model_stream)
                 value = step_value(params)
@@ -532,7 +530,6 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
     for k in range(min(args.steps, 50)):
         flush.fill_(k & 0xff)
-        flush.view(torch.int64).sum()  # read back: clean lines in L2 (as pf_bench's flush)
         torch.cuda.synchronize()
         t = time.perf_counter()
         step_value(params)

@@ -947,8 +947,11 @@ __device__ void pf_finalize_warp0(const pf_args& a, int lane, const double* S0 =
         dst->norm_error = o.norm_error;
 #pragma unroll
         for (int i = 0; i < PF_FX_DIGITS; ++i) dst->fx[i] = o.fx[i];
-        dst->pad = o.pad;
         dst->check = o.check;
+        // system-scope release of the sequence word: every field above
+        // reaches the host first, and the host sees the record right away
+        // rather than when the grid drains (measured: e2e 58 -> 48 us, C2)
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(&a.hout[k].pad), "r"(o.pad) : "memory");
       }
       // the norms the reference's nodes now cache: device memory, read by
       // the host only when asked (pf_node_norms); a call whose normalisation
@@ -1144,8 +1147,8 @@ extern "C" __global__ void __launch_bounds__(PF_EV_THREADS, PF_EVENT_MIN_BLOCKS)
 // cheaper to repeat per SM than to hand over through a second grid -- and
 // then streams its chunks.  Chunks (fixed event ranges: the reduction unit,
 // so the result does not depend on the schedule) go to a balanced set of
-// active warps, every chunk of a warp prefetched into L2 at entry so HBM
-// streams the whole pass while the setup runs.  Lane accumulators live in
+// active warps (every active warp the same number of chunks: no lone last
+// round).  Lane accumulators live in
 // registers; one exact block total per CTA; the last CTA rounds and
 // publishes (pf_finalize_warp0).
 #ifndef PF_FUSED_WARPS
@@ -1182,9 +1185,9 @@ extern "C" __global__ void __launch_bounds__(PF_FUSED_THREADS, 1) pf_fused_kerne
   if (lane == 0) {
     for (int s = 0; s < PF_NST; ++s) pf_mbar_init(mybar + s, 1);
     pf_fence_mbar_init();
-#ifndef PF_NO_L2_PREFETCH
-    // every chunk of this warp into L2 now: HBM streams the whole pass while
-    // the setup below runs, and the TMA copies of the loop hit L2
+#ifdef PF_L2_PREFETCH_ALL
+    // every chunk of this warp into L2 now (measured slower: 45 vs 40 us
+    // for C2 -- the prefetch storm delays the setup's own loads)
     for (int j = 0; j < n_mine; ++j) {
       const pf_u64 b = (pf_u64)(gw + j * nwa) * (PF_SUB * PF_NSUB);
 #pragma unroll
@@ -1317,11 +1320,8 @@ extern "C" __global__ void __launch_bounds__(PF_FUSED_THREADS, 1) pf_fused_kerne
 }
 
 // ---------------------------------------------------------------------------
-// bench only: the read half of the L2 flush.  After the flush buffer is
-// written, reading it back leaves L2 full of CLEAN lines of that buffer, so
-// the timed call starts with its inputs evicted (as after the write) but does
-// not pay the write-back of 126 MB of dirty flush data -- which a real fit,
-// whose calls run back to back, never does either.
+// bench only (PFB200_FLUSH=writeread): the optional read half of the L2
+// flush, leaving clean lines of the flush buffer in L2.
 extern "C" __global__ void pf_flush_read_kernel(const ulonglong2* p, pf_u64 n, unsigned long long* sink) {
   unsigned long long acc = 0;
   for (pf_u64 i = (pf_u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (pf_u64)gridDim.x * blockDim.x) {

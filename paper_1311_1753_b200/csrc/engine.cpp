@@ -1075,8 +1075,10 @@ void Model::flush_l2(int i) {
   const size_t bytes = 256ull << 20;
   if (!sh.d_scratch) ck(cudaMalloc(&sh.d_scratch, bytes + 64), "cudaMalloc scratch");
   ck(cudaMemsetAsync(sh.d_scratch, i & 0xff, bytes, sh.stream), "flush");
+  // write only (the protocol's flush); PFB200_FLUSH=writeread also reads the
+  // buffer back (clean lines in L2): measured the same C2 step (45.0 vs 45.4 us)
   const char* mode = std::getenv("PFB200_FLUSH");
-  if (mode && std::string(mode) == "write") return;
+  if (!mode || std::string(mode) != "writeread") return;
   const void* p = sh.d_scratch;
   uint64_t n16 = bytes / 16;
   void* sink = static_cast<char*>(sh.d_scratch) + bytes;

@@ -42,7 +42,7 @@ int main() {
       cudaMemsetAsync(flush, i, 256 << 20, s);
       cudaEventRecord(a, s);
       if (ge) cudaGraphLaunch(ge, s);
-      else if (c.smem == 0 && c.name[0] == 'e') k_empty<<<c.grid, c.block, 0, s>>>(nullptr);
+      else if (c.smem == 0) k_empty<<<c.grid, c.block, 0, s>>>(nullptr);
       else k_smem<<<c.grid, c.block, c.smem, s>>>(nullptr);
       cudaEventRecord(b, s);
       cudaEventSynchronize(b);
