@@ -31,7 +31,7 @@ struct Layout {
   bool binned = false;
   int ept = 8;                // events per lane per sub-chunk (32 * ept events)
   int nsub = 2;               // sub-chunks per chunk (chunk = nsub * 32 * ept events)
-  int setup_cluster = 1;      // CTAs of the setup kernel's thread-block cluster (1: the split of the fused pass, so batched == sequential bitwise)
+  int setup_cluster = 1;      // CTAs of a setup cluster: the setup kernel's and the fused pass's (same split: batched == sequential bitwise; 4 measured 41 -> 64 us for C2: 4-CTA clusters of 1-CTA/SM kernels do not all fit at once)
   int nst = 3;                // TMA stages per event warp (PF_NST)
   int setup_maxq = 8;         // most midpoint sums in one level (PF_SETUP_MAXQ)
   int lacc_n = 2;             // doubles of the per-lane chunk accumulator (PF_LACC_N)

@@ -1220,13 +1220,22 @@ extern "C" __global__ void __launch_bounds__(PF_FUSED_THREADS, 1) pf_fused_kerne
   pf_cnt cnt_grid, cnt_stage;
   pf_cnt_init(cnt_grid);
   pf_cnt_init(cnt_stage);
-  pf_setup_core<1>(a, 0, 0u, P, S, r, false, cx, cnt_grid, cnt_stage);
-  if (blockIdx.x == 0) {  // one CTA reports what every CTA found
-    if (cx.err) atomicMin(&r->norm_error, cx.err);
+  // the setup's grid points split over a cluster of PF_SETUP_CLUSTER CTAs
+  // (DSMEM exchange), exactly as the setup kernel of the batched path splits
+  // them: batched and single calls stay bitwise equal
+  const unsigned rank = PF_SETUP_CLUSTER > 1 ? pf_cluster_rank() : 0u;
+  pf_setup_core<PF_SETUP_CLUSTER>(a, 0, rank, P, S, r, false, cx, cnt_grid, cnt_stage);
+  // no CTA may leave while a cluster peer could still read its setup
+  // partials: arrive now, wait just before exit
+  if (PF_SETUP_CLUSTER > 1) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  if (blockIdx.x < PF_SETUP_CLUSTER) {  // one cluster reports what every cluster found
+    if (cx.err && rank == 0) atomicMin(&r->norm_error, cx.err);
     if (pf_grid_counts(a, 0)) {
       pf_cnt_flush(cnt_grid, a.clamp);
-      pf_cnt_flush(cnt_stage, a.clamp);
+      if (rank == 0) pf_cnt_flush(cnt_stage, a.clamp);
     }
+  }
+  if (blockIdx.x == 0) {
     double* gS = a.S;
     double* gP = (double*)a.P;
     for (int i = threadIdx.x; i < PF_SS; i += blockDim.x) gS[i] = S[i];
@@ -1296,6 +1305,7 @@ extern "C" __global__ void __launch_bounds__(PF_FUSED_THREADS, 1) pf_fused_kerne
     s_last = atomicAdd(a.done, 1u) == gridDim.x - 1;
   }
   __syncthreads();
+  if (PF_SETUP_CLUSTER > 1) asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 #ifdef PF_EVENT_TRACE
   if (threadIdx.x == 0 && blockIdx.x < 4094) {
     unsigned smid;

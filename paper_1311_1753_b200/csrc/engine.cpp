@@ -559,15 +559,16 @@ cudaGraphExec_t Model::graph_for(Shard& sh, int K) {
     f.clamp = sh.d_clamp;
     f.fused = 1;
     {  // balanced static schedule: kpw chunks for each of nwa active warps
-      const int all = sm_count(sh.device) * kFusedWarps;
+      const int all = fused_grid(sh) * kFusedWarps;
       const int n = std::max(sh.n_chunks, 1);
       f.kpw = (n + all - 1) / all;
       f.nwa = (n + f.kpw - 1) / f.kpw;
     }
-    launch(sh.mod->fused, dim3(sm_count(sh.device)), dim3(32 * kFusedWarps), fused_smem(L_), sh.stream, f);
+    launch(sh.mod->fused, dim3(fused_grid(sh)), dim3(32 * kFusedWarps), fused_smem(L_), sh.stream, f, false,
+           L_.setup_cluster);
     ++kernels;
     sh.event_args = f;
-    sh.event_grid = sm_count(sh.device);
+    sh.event_grid = fused_grid(sh);
     sh.fused = true;
   } else if (small_norms_) {
     launch(sh.mod->setup, dim3(K * L_.setup_cluster), dim3(512), setup_smem_bytes(), sh.stream, a, false,
@@ -630,6 +631,12 @@ cudaGraphExec_t Model::graph_for(Shard& sh, int K) {
 // The single-kernel path: small normalisation grids (the setup runs in every
 // CTA), a ring that runs at most one chunk ahead, shared memory that fits,
 // and events on this shard.  PFB200_FUSED=0 selects the two-kernel graph.
+// one CTA per SM, rounded down to whole setup clusters
+int Model::fused_grid(const Shard& sh) const {
+  const int c = std::max(1, L_.setup_cluster);
+  return std::max(c, sm_count(sh.device) / c * c);
+}
+
 bool Model::fused_ok(const Shard& sh) const {
   if (const char* env = std::getenv("PFB200_FUSED"))
     if (std::atoi(env) == 0) return false;
@@ -724,7 +731,7 @@ void Model::launch_graphs(const double* params, int K) {
       cudaKernelNodeParams kp = {};
       const bool setup = small_norms_;
       kp.func = reinterpret_cast<void*>(sh.fused ? sh.mod->fused : setup ? sh.mod->setup : sh.mod->pre);
-      kp.gridDim = dim3(sh.fused ? sm_count(sh.device) : setup ? L_.setup_cluster : 1);
+      kp.gridDim = dim3(sh.fused ? fused_grid(sh) : setup ? L_.setup_cluster : 1);
       kp.blockDim = dim3(sh.fused ? 32 * kFusedWarps : setup ? 512 : 256);
       kp.sharedMemBytes = sh.fused ? static_cast<unsigned>(fused_smem(L_))
                                    : setup ? static_cast<unsigned>(setup_smem_bytes()) : 0u;
@@ -1127,7 +1134,8 @@ BenchResult Model::bench(const double* params, size_t n, int metric, int steps, 
       }
       ck(cudaEventRecord(e0, sh.stream), "record");
       if (sh.fused)
-        launch(sh.mod->fused, dim3(sh.event_grid), dim3(32 * kFusedWarps), fused_smem(L_), sh.stream, a, false);
+        launch(sh.mod->fused, dim3(sh.event_grid), dim3(32 * kFusedWarps), fused_smem(L_), sh.stream, a, false,
+               L_.setup_cluster);
       else
         launch(sh.mod->event, dim3(sh.event_grid), dim3(32 * kEventWarps), event_smem(L_, 1), sh.stream,
                a, false);

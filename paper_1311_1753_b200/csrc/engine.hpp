@@ -233,6 +233,7 @@ class Model {
   }
   [[noreturn]] void throw_device_error(uint32_t code_node) const;
   bool fused_ok(const Shard& sh) const;
+  int fused_grid(const Shard& sh) const;
   size_t setup_smem_bytes() const {
     return sizeof(double) * (std::max(L_.np, 1) + std::max(L_.ss, 1));
   }

@@ -1,4 +1,6 @@
-for v in "X=1" "PFB200_DEFINES=PF_NO_L2_PREFETCH"; do
+for v in "X=1" "PFB200_NSUB=2"; do
+  echo "== $v (setup phases, cycles)"
+  env $v PFB200_DEFINES="PF_EVENT_TRACE;PF_SETUP_TRACE" python tools/trace_fused.py C2 2>&1 | grep "^setup" | tail -8
   echo "== $v (timeline)"
-  env $v python -c "import os; os.environ['PFB200_DEFINES']=(os.environ.get('PFB200_DEFINES','')+';PF_EVENT_TRACE').strip(';'); import runpy, sys; sys.argv=['t','C2']; runpy.run_path('tools/trace_fused.py', run_name='__main__')" 2>&1 | tail -14
+  env $v PFB200_DEFINES="PF_EVENT_TRACE" python tools/trace_fused.py C2 2>&1 | tail -14
 done

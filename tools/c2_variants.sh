@@ -8,9 +8,7 @@ for l in sys.stdin:
     elif 'Error' in l or 'error' in l: print(l)
 "; }
 run default X=1
-run writeflush PFB200_FLUSH=write
-run unfused PFB200_FUSED=0
-run nol2pf PFB200_DEFINES=PF_NO_L2_PREFETCH
-run nol2pf_writeflush PFB200_DEFINES=PF_NO_L2_PREFETCH PFB200_FLUSH=write
-run nst3 PFB200_NST=3
-run nst3_nol2pf PFB200_NST=3 PFB200_DEFINES=PF_NO_L2_PREFETCH
+run cluster1 PFB200_SETUP_CLUSTER=1
+run cluster2 PFB200_SETUP_CLUSTER=2
+run nsub2 PFB200_NSUB=2
+run ept8_nsub4 PFB200_EPT=8
