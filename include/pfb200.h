@@ -40,7 +40,14 @@ extern "C" {
  * DalitzPlotPdf, which the reference lacks (BASELINE configs 3 and 5; see
  * DESIGN.md).  DalitzPlotPdf: obs = {m^2_12, m^2_13}; params = per resonance
  * {mass, width, Re c, Im c}; reals = {M, m1, m2, m3, R, then per resonance
- * channel (12, 13 or 23) and spin (0 or 1)}. */
+ * channel (12, 13 or 23) and spin (0 or 1)}.
+ * TddpPdf (time-dependent Dalitz, BASELINE config 5): obs = {m^2_12, m^2_13,
+ * t}; params = the DalitzPlotPdf resonance params, then {tau, x, y}; reals =
+ * the DalitzPlotPdf reals (m1 == m2: daughters 1 and 2 CP conjugates).
+ * Density |A g+(t) + Abar g-(t)|^2 =
+ *   e^-(t/tau) [ (|A|^2 + |Abar|^2)/2 cosh(y t/tau) + (|A|^2 - |Abar|^2)/2 cos(x t/tau)
+ *                - Re(A* Abar) sinh(y t/tau) - Im(A* Abar) sin(x t/tau) ],
+ * Abar(s12, s13) = A(s12, s23) (the CP-mirrored point). */
 enum pf_kind {
   PF_EXPONENTIAL = 0,
   PF_GAUSSIAN = 1,
@@ -52,7 +59,8 @@ enum pf_kind {
   PF_MAPPED = 7,
   PF_CONVOLUTION = 8,
   PF_ARGUS = 9,
-  PF_DALITZ = 10
+  PF_DALITZ = 10,
+  PF_TDDP = 11
 };
 
 /* MetricKind, engine.hpp:48 */

@@ -191,19 +191,13 @@ static int po_dalitz_inside(double s12, double s13, double M, double m1, double 
   return s13 >= lo && s13 <= hi;
 }
 
-static double po_dalitz(const onode* o, const double* evt, const double* p) {
+/* the isobar amplitude sum at (s12, s13, s23), the kinematic boundary aside */
+static void po_dalitz_amp(const onode* o, int nres, double s12, double s13, double s23, const double* p,
+                          double* are_out, double* aim_out) {
   const double M = o->reals[0], m1 = o->reals[1], m2 = o->reals[2], m3 = o->reals[3], R = o->reals[4];
   const double R2 = R * R;
   const double ms[4] = {M, m1, m2, m3};
-  const double s12 = evt[o->ocol[0]], s13 = evt[o->ocol[1]];
-  if (!po_dalitz_inside(s12, s13, M, m1, m2, m3)) return 0.0;
-  double msum = M * M;
-  msum = msum + m1 * m1;
-  msum = msum + m2 * m2;
-  msum = msum + m3 * m3;
-  const double s23 = (msum - s12) - s13;
   double are = 0.0, aim = 0.0;
-  const int nres = o->np / 4;
   for (int r = 0; r < nres; ++r) {
     const int ch = (int)o->reals[5 + 2 * r], spin = (int)o->reals[6 + 2 * r];
     const int i = ch / 10, j = ch % 10, k = 6 - i - j;
@@ -225,9 +219,47 @@ static double po_dalitz(const onode* o, const double* evt, const double* p) {
     are = are + (cre * bre - cim * bim);
     aim = aim + (cre * bim + cim * bre);
   }
+  *are_out = are;
+  *aim_out = aim;
+}
+
+static double po_dalitz_s23(const onode* o, double s12, double s13) {
+  const double M = o->reals[0], m1 = o->reals[1], m2 = o->reals[2], m3 = o->reals[3];
+  double msum = M * M;
+  msum = msum + m1 * m1;
+  msum = msum + m2 * m2;
+  msum = msum + m3 * m3;
+  return (msum - s12) - s13;
+}
+
+static double po_dalitz(const onode* o, const double* evt, const double* p) {
+  const double s12 = evt[o->ocol[0]], s13 = evt[o->ocol[1]];
+  if (!po_dalitz_inside(s12, s13, o->reals[0], o->reals[1], o->reals[2], o->reals[3])) return 0.0;
+  double are, aim;
+  po_dalitz_amp(o, o->np / 4, s12, s13, po_dalitz_s23(o, s12, s13), p, &are, &aim);
   return are * are + aim * aim;
 }
 
+/* TddpPdf (no reference kernel; GooFit's TDDP of PAPER.md:299-309 restated):
+   |A g+(t) + Abar g-(t)|^2 with Abar(s12, s13) = A(s12, s23), T = t / tau:
+   e^-T [(|A|^2+|Abar|^2)/2 cosh(yT) + (|A|^2-|Abar|^2)/2 cos(xT)
+         - Re(A* Abar) sinh(yT) - Im(A* Abar) sin(xT)] */
+static double po_tddp(const onode* o, const double* evt, const double* p) {
+  const int nres = (o->np - 3) / 4;
+  const double s12 = evt[o->ocol[0]], s13 = evt[o->ocol[1]], t = evt[o->ocol[2]];
+  if (!po_dalitz_inside(s12, s13, o->reals[0], o->reals[1], o->reals[2], o->reals[3])) return 0.0;
+  const double s23 = po_dalitz_s23(o, s12, s13);
+  double are, aim, bre, bim;
+  po_dalitz_amp(o, nres, s12, s13, s23, p, &are, &aim);
+  po_dalitz_amp(o, nres, s12, s23, s13, p, &bre, &bim);
+  const double tau = p[o->p[4 * nres]], x = p[o->p[4 * nres + 1]], y = p[o->p[4 * nres + 2]];
+  const double T = t / tau;
+  const double a2 = are * are + aim * aim, b2 = bre * bre + bim * bim;
+  const double cre = are * bre + aim * bim, cim = are * bim - aim * bre;
+  const double v = ((0.5 * (a2 + b2)) * cosh(y * T) + (0.5 * (a2 - b2)) * cos(x * T)) - cre * sinh(y * T) -
+                   cim * sin(x * T);
+  return exp(-T) * v;
+}
 
 static double density(omodel* m, int id, double* evt, const double* p) { /* pdf.hpp:83-91 */
   onode* o = &m->nodes[id];
@@ -278,6 +310,21 @@ static double raw(omodel* m, int id, double* evt, const double* p) {
           return 0.0;
         }
       return po_dalitz(o, evt, p);
+    }
+    case PF_TDDP: {
+      const int nres = (o->np - 3) / 4;
+      for (int r = 0; r < nres; ++r)
+        if (!(p[o->p[4 * r + 1]] > 0.0)) {
+          char buf[300];
+          snprintf(buf, sizeof buf, "%s: width must be > 0", o->name);
+          fail(m, "nonpositive-width", buf);
+          return 0.0;
+        }
+      if (!(p[o->p[4 * nres]] > 0.0)) {
+        fail(m, "nonpositive-lifetime", o->name);
+        return 0.0;
+      }
+      return po_tddp(o, evt, p);
     }
     case PF_ARGUS: { /* GooFit ArgusPdf, upper threshold; no reference kernel */
       double x = evt[o->ocol[0]];
@@ -368,8 +415,67 @@ static uint64_t hash_params(const double* p, int n) { /* pdf.hpp:40-51 */
   return h;
 }
 
+/* TddpPdf: the 3-D midpoint sum over (s12, s13, t) evaluated by its
+   separability, sum_ij sum_l D(s12_i, s13_j) . T(t_l) = sum_c D_c T_c (the
+   four Dalitz bilinears times the four time functions, po_tddp), in long
+   double like midpoint_sum.  Mathematically the same sum as the brute-force
+   walk over n^3 points (checked against it at small n, tests/test_oracle.py),
+   which at n = 1024 would take 10^10 evaluations. */
+static double tddp_midpoint_sum(omodel* m, int id, const double* p, uint64_t n) {
+  onode* o = &m->nodes[id];
+  const int nres = (o->np - 3) / 4;
+  int b12 = -1, b13 = -1, bt = -1;
+  for (int d = 0; d < o->nbox; ++d) {
+    if (o->bcol[d] == o->ocol[0]) b12 = d;
+    if (o->bcol[d] == o->ocol[1]) b13 = d;
+    if (o->bcol[d] == o->ocol[2]) bt = d;
+  }
+  const pf_variable *v12 = &m->vars[o->bvar[b12]], *v13 = &m->vars[o->bvar[b13]], *vt = &m->vars[o->bvar[bt]];
+  const double h12 = (v12->upper - v12->lower) / (double)n, h13 = (v13->upper - v13->lower) / (double)n;
+  const double ht = (vt->upper - vt->lower) / (double)n;
+  for (int r = 0; r < nres; ++r)
+    if (!(p[o->p[4 * r + 1]] > 0.0)) {
+      fail(m, "nonpositive-width", o->name);
+      return 0.0;
+    }
+  const double tau = p[o->p[4 * nres]], x = p[o->p[4 * nres + 1]], y = p[o->p[4 * nres + 2]];
+  if (!(tau > 0.0)) {
+    fail(m, "nonpositive-lifetime", o->name);
+    return 0.0;
+  }
+  long double D[4] = {0.0L, 0.0L, 0.0L, 0.0L}, T[4] = {0.0L, 0.0L, 0.0L, 0.0L};
+  for (uint64_t i = 0; i < n; ++i) {
+    const double s12 = v12->lower + ((double)i + 0.5) * h12;
+    for (uint64_t j = 0; j < n; ++j) {
+      const double s13 = v13->lower + ((double)j + 0.5) * h13;
+      if (!po_dalitz_inside(s12, s13, o->reals[0], o->reals[1], o->reals[2], o->reals[3])) continue;
+      const double s23 = po_dalitz_s23(o, s12, s13);
+      double are, aim, bre, bim;
+      po_dalitz_amp(o, nres, s12, s13, s23, p, &are, &aim);
+      po_dalitz_amp(o, nres, s12, s23, s13, p, &bre, &bim);
+      const double a2 = are * are + aim * aim, b2 = bre * bre + bim * bim;
+      D[0] += 0.5 * (a2 + b2);
+      D[1] += 0.5 * (a2 - b2);
+      D[2] += are * bre + aim * bim;
+      D[3] += are * bim - aim * bre;
+    }
+  }
+  for (uint64_t l = 0; l < n; ++l) {
+    const double t = vt->lower + ((double)l + 0.5) * ht;
+    const double Tt = t / tau, e = exp(-Tt);
+    T[0] += e * cosh(y * Tt);
+    T[1] += e * cos(x * Tt);
+    T[2] -= e * sinh(y * Tt);
+    T[3] -= e * sin(x * Tt);
+  }
+  long double sum = 0.0L;
+  for (int c = 0; c < 4; ++c) sum += D[c] * T[c];
+  return (double)sum * ((h12 * h13) * ht);
+}
+
 static double midpoint_sum(omodel* m, int id, const double* p, uint64_t n) {
   onode* o = &m->nodes[id];
+  if (o->kind == PF_TDDP && !getenv("PO_TDDP_BRUTE")) return tddp_midpoint_sum(m, id, p, n);
   int dims = o->nbox;
   double lo[8], h[8];
   uint64_t total = 1;

@@ -14,6 +14,7 @@ LIB_PATH = os.path.join(_HERE, "libpfb200.so")
 PF_EXPONENTIAL, PF_GAUSSIAN, PF_BREIT_WIGNER, PF_POLYNOMIAL = 0, 1, 2, 3
 PF_PRODUCT, PF_SUM, PF_COMPOSITE, PF_MAPPED, PF_CONVOLUTION, PF_ARGUS = 4, 5, 6, 7, 8, 9
 PF_DALITZ = 10
+PF_TDDP = 11
 PF_NLL, PF_CHISQ = 0, 1
 PF_FX_DIGITS = 6
 PF_OBSERVABLE, PF_PARAMETER = 0, 1

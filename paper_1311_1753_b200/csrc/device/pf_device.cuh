@@ -29,6 +29,7 @@ typedef unsigned int pf_u32;
 #define PF_E_ZERO_INTEGRAL 4  // pdf.hpp:186-187
 #define PF_E_NONPOS_ENDPOINT 5 // ArgusPdf m0 <= 0
 #define PF_E_GROUP_TIMEOUT 6   // a peer's record never arrived (exchange group)
+#define PF_E_NONPOS_LIFETIME 7 // TddpPdf tau <= 0
 #define PF_GROUP_MAX 16        // ranks of a peer-memory exchange group (engine.hpp kMaxGroup)
 #define PF_MAX_BATCH 16        // parameter sets per launch (engine.hpp kMaxBatch)
 
@@ -49,7 +50,7 @@ struct pf_krec {
 
 struct pf_task {  // one midpoint sum: node, n points per box dimension
   int node, n, dims, first_block;
-  int n_blocks, partial_offset, fine, level;
+  int n_blocks, comp, fine, level;  // comp: component of a TddpPdf grid (-1: a plain midpoint sum)
   pf_u64 points, per_block;
   double lo[PF_MAX_BOX];
   double h[PF_MAX_BOX];

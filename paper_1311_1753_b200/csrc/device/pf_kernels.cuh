@@ -54,6 +54,16 @@ __device__ __forceinline__ void pf_finish_norm(double* S, pf_krec* r, int node, 
     atomicMin(&r->norm_error, ((pf_u32)node << 8) | PF_E_ZERO_INTEGRAL);
 }
 
+// a finished (coarse, fine) task pair: a node's norm, or one component sum of
+// a TddpPdf's separable grid (combined by pf_stage_post)
+__device__ __forceinline__ void pf_finish_task(double* S, pf_krec* r, const pf_task& T, double coarse,
+                                               double fine) {
+  if (T.comp >= 0)
+    pf_store_comp(S, T.node, T.comp, coarse, fine);
+  else
+    pf_finish_norm(S, r, T.node, coarse, fine);
+}
+
 // ---------------------------------------------------------------------------
 #define PF_SETUP_THREADS 512  // 128 registers: the level's 8 reductions interleave unspilled
 #ifndef PF_SETUP_CLUSTER
@@ -197,7 +207,7 @@ __device__ __forceinline__ void pf_setup_core(const pf_args& a, int k, unsigned 
       // midpoint_sum returns static_cast<double>(sum) * vol (pdf.hpp:173-175)
       const double sum = __dmul_rn(pf_dd_to_double(y), tk[t0 + q].vol);
       const double fine = __shfl_down_sync(0xffffffffu, sum, 16);
-      if (lane == 0) pf_finish_norm(S, r, tk[t0 + q].node, sum, fine);
+      if (lane == 0) pf_finish_task(S, r, tk[t0 + q], sum, fine);
     }
     __syncthreads();
     PF_TRACE("finish");
@@ -339,7 +349,7 @@ extern "C" __global__ void __launch_bounds__(PF_THREADS) pf_norm_kernel(const __
   __syncthreads();
   if (threadIdx.x == 0)
     for (int tt = 0; tt + 1 < a.n_tasks; tt += 2)
-      pf_finish_norm(S, a.rec + k, a.tasks[tt].node, sums[tt], sums[tt + 1]);
+      pf_finish_task(S, a.rec + k, a.tasks[tt], sums[tt], sums[tt + 1]);
   __syncthreads();
   pf_ctx cx2;
   cx2.err = 0;

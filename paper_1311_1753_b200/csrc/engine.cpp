@@ -438,6 +438,10 @@ void Model::build_tasks(uint32_t grid_points) {
     for (int node : L_.level_nodes[lvl]) {
       const Node& nd = pg_.nodes[node];
       const int dims = static_cast<int>(nd.box.size());
+      if (nd.kind == PF_TDDP) {
+        add_tddp_tasks(node, grid_points, static_cast<int>(lvl), &blocks);
+        continue;
+      }
       if (dims > 8) throw Error("bad-graph", nd.name + ": more than 8 box dimensions");
       // a convolution's grid runs over (point, tau_j) pairs (codegen.cpp
       // emit_norm_point): Q elements per point, each one resolution call
@@ -480,7 +484,7 @@ void Model::build_tasks(uint32_t grid_points) {
         t.n_blocks = static_cast<int>(nb);
         t.level = static_cast<int>(lvl);
         t.first_block = blocks;
-        t.partial_offset = blocks;
+        t.comp = -1;
         blocks += t.n_blocks;
         tasks_.push_back(t);
       }
@@ -488,6 +492,59 @@ void Model::build_tasks(uint32_t grid_points) {
     level_n_tasks_[lvl] = static_cast<int>(tasks_.size()) - level_first_task_[lvl];
     level_blocks_[lvl] = blocks;
     max_norm_blocks_ = std::max(max_norm_blocks_, blocks);
+  }
+}
+
+// TddpPdf: its 3-D midpoint sums (pdf.hpp:148-176 over (s12, s13, t)) are
+// separable, sum_c D_c T_c: four Dalitz-grid component sums D_c and four
+// time-grid sums T_c, each at n and 2n points per dimension (codegen.cpp
+// emit_tddp_components; pf_stage_post combines them)
+void Model::add_tddp_tasks(int node, uint32_t grid_points, int lvl, int* blocks) {
+  const Node& nd = pg_.nodes[node];
+  auto box_of = [&](int col) -> const BoxDim& {
+    for (const BoxDim& b : nd.box)
+      if (b.column == col) return b;
+    throw Error("bad-graph", nd.name + ": observable outside the box");
+  };
+  const BoxDim* dims[3] = {&box_of(nd.obs_cols[0]), &box_of(nd.obs_cols[1]), &box_of(nd.obs_cols[2])};
+  const double cost = subtree_cost(pg_, node);
+  for (int comp = 0; comp < 8; ++comp) {
+    const bool time = comp >= 4;
+    for (int fine = 0; fine < 2; ++fine) {
+      Task t;
+      std::memset(&t, 0, sizeof t);
+      const uint64_t n = static_cast<uint64_t>(grid_points) * (fine ? 2 : 1);
+      t.node = node;
+      t.comp = comp;
+      t.n = static_cast<int>(n);
+      t.dims = time ? 1 : 2;
+      t.fine = fine;
+      double vol = 1.0;
+      uint64_t total = 1;
+      for (int d = 0; d < t.dims; ++d) {
+        const Var& v = pg_.vars[dims[time ? 2 : d]->var];
+        t.lo[d] = v.lower;
+        t.h[d] = (v.upper - v.lower) / static_cast<double>(n);
+        vol *= t.h[d];
+        total *= n;
+      }
+      t.vol = vol;
+      t.points = total;
+      uint64_t per = static_cast<uint64_t>(std::max(1.0, std::floor(4096.0 / (time ? 8.0 : cost))));
+      if (!time) per = std::max<uint64_t>(per, 256ull * 32ull);
+      uint64_t nb = (total + per - 1) / per;
+      if (nb > 4096) {
+        nb = 4096;
+        per = (total + nb - 1) / nb;
+        nb = (total + per - 1) / per;
+      }
+      t.per_block = per;
+      t.n_blocks = static_cast<int>(nb);
+      t.level = lvl;
+      t.first_block = *blocks;
+      *blocks += t.n_blocks;
+      tasks_.push_back(t);
+    }
   }
 }
 
@@ -678,6 +735,7 @@ std::string Model::error_message(uint32_t code_node) const {
     case 3: return "out-of-domain: " + name + ": x outside mapped range";
     case 4: return "zero-integral: degenerate PDF '" + name + "'";
     case 5: return "nonpositive-endpoint: " + name;
+    case 7: return "nonpositive-lifetime: " + name;
   }
   return "device-error: code " + std::to_string(code);
 }

@@ -39,7 +39,7 @@ static_assert(sizeof(KRec) == 136, "pf_krec layout");
 
 struct Task {
   int node, n, dims, first_block;
-  int n_blocks, partial_offset, fine, level;
+  int n_blocks, comp, fine, level;  // comp: component of a TddpPdf grid (-1: a plain midpoint sum)
   uint64_t points, per_block;
   double lo[8];
   double h[8];
@@ -227,6 +227,7 @@ class Model {
   cudaGraphExec_t graph_for(Shard& s, int K);
   Args base_args(Shard& s, int K);
   void build_tasks(uint32_t grid_points);
+  void add_tddp_tasks(int node, uint32_t grid_points, int lvl, int* blocks);
   std::string error_message(uint32_t code_node) const;
   bool conv_windowed(int node) const {
     return std::find(L_.conv_windowed.begin(), L_.conv_windowed.end(), node) != L_.conv_windowed.end();

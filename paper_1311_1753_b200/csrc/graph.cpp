@@ -22,6 +22,7 @@ const char* kind_name(int kind) {
     case PF_CONVOLUTION: return "ConvolutionPdf";
     case PF_ARGUS: return "ArgusPdf";
     case PF_DALITZ: return "DalitzPlotPdf";
+    case PF_TDDP: return "TddpPdf";
   }
   return "unknown";
 }
@@ -115,14 +116,24 @@ void validate_node(const pf_graph& g, int idx) {
       require(g.variables[n.params[0]].lower > 0, "nonpositive-endpoint",
               name + ": m0 limits must exclude 0");
       break;
-    case PF_DALITZ: {  // DalitzPlotPdf(m12^2, m13^2; resonances), new
-      require(n.n_obs == 2 && is_obs(n.obs[0]) && is_obs(n.obs[1]), "wrong-role",
-              name + ": m12^2 and m13^2 must be observables");
-      const int nres = n.n_params / 4;
-      require(nres >= 1 && n.n_params == 4 * nres, "bad-arity",
-              name + ": need (mass, width, Re c, Im c) per resonance");
+    case PF_DALITZ:    // DalitzPlotPdf(m12^2, m13^2; resonances), new
+    case PF_TDDP: {    // TddpPdf(m12^2, m13^2, t; resonances, tau, x, y), new
+      const bool td = n.kind == PF_TDDP;
+      require(n.n_obs == (td ? 3 : 2) && is_obs(n.obs[0]) && is_obs(n.obs[1]) && (!td || is_obs(n.obs[2])),
+              "wrong-role", name + (td ? ": m12^2, m13^2 and t must be observables" : ": m12^2 and m13^2 must be observables"));
+      const int nres = (n.n_params - (td ? 3 : 0)) / 4;
+      require(nres >= 1 && n.n_params == 4 * nres + (td ? 3 : 0), "bad-arity",
+              name + (td ? ": need (mass, width, Re c, Im c) per resonance, then tau, x, y"
+                         : ": need (mass, width, Re c, Im c) per resonance"));
+      if (td) {
+        require(is_par(n.params[4 * nres]) && is_par(n.params[4 * nres + 1]) && is_par(n.params[4 * nres + 2]),
+                "wrong-role", name + ": tau, x, y must be parameters");
+        require(g.variables[n.params[4 * nres]].lower > 0, "nonpositive-lifetime", name + ": tau limits must exclude 0");
+        require(n.n_reals >= 5 && n.reals[1] == n.reals[2], "bad-kinematics",
+                name + ": daughters 1 and 2 must be CP conjugates (m1 == m2)");
+      }
       require(n.n_reals == 5 + 2 * nres, "bad-arity", name + ": need M, m1, m2, m3, R and (channel, spin) per resonance");
-      for (int i = 0; i < n.n_params; ++i)
+      for (int i = 0; i < 4 * nres; ++i)
         require(is_par(n.params[i]), "wrong-role", name + ": resonance constants must be parameters");
       for (int r = 0; r < nres; ++r) {
         const double ch = n.reals[5 + 2 * r], sp = n.reals[6 + 2 * r];
@@ -390,6 +401,7 @@ double subtree_cost(const Program& pg, int node) {
   const Node& n = pg.nodes[node];
   double c = 1.0;
   if (n.kind == PF_DALITZ) return 8.0 * static_cast<double>(n.params.size() / 4);  // per resonance
+  if (n.kind == PF_TDDP) return 16.0 * static_cast<double>(n.params.size() / 4) + 8.0;  // two amplitudes + time
   if (n.kind == PF_CONVOLUTION) {
     // model values are hoisted per call; the resolution runs Q times
     return 1.0 + static_cast<double>(n.q) * subtree_cost(pg, n.children[1]);

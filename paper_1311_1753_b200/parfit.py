@@ -629,6 +629,33 @@ class DalitzPlotPdf(PdfNode):
         self._reals = reals
 
 
+class TddpPdf(DalitzPlotPdf):
+    """Time-dependent Dalitz-plot PDF of D0 -> 1 2 3 with mixing (BASELINE
+    config 5; GooFit's TddpPdf of PAPER.md:299-309, restated -- not in the
+    reference).  Observables m12^2, m13^2, t; the DalitzPlotPdf resonances,
+    then lifetime tau and mixing parameters x, y.  With A the isobar
+    amplitude and Abar(s12, s13) = A(s12, s23) its CP mirror (daughters 1 and
+    2 conjugate, m1 == m2), the density is |A g+(t) + Abar g-(t)|^2:
+      e^-(t/tau) [(|A|^2+|Abar|^2)/2 cosh(y t/tau) + (|A|^2-|Abar|^2)/2 cos(x t/tau)
+                  - Re(A* Abar) sinh(y t/tau) - Im(A* Abar) sin(x t/tau)]
+    inside the kinematic boundary, 0 outside (pfb200.h, pf_oracle.c)."""
+
+    kind = _abi.PF_TDDP
+
+    def __init__(self, name, m12sq, m13sq, t, resonances, masses, tau, x, y, radius=1.5):
+        super().__init__(name, m12sq, m13sq, resonances, masses, radius)
+        _need_obs(name, t, "t")
+        for v, w in ((tau, "tau"), (x, "x"), (y, "y")):
+            _need_par(name, v, w)
+        if not (tau.lower > 0):
+            raise Error("nonpositive-lifetime", f"{name}: tau limits must exclude 0")
+        M, m1, m2, m3 = (float(v) for v in masses)
+        if m1 != m2:
+            raise Error("bad-kinematics", f"{name}: daughters 1 and 2 must be CP conjugates (m1 == m2)")
+        self._obs = [m12sq, m13sq, t]
+        self._params = self._params + [tau, x, y]
+
+
 class ProdPdf(PdfNode):
     kind = _abi.PF_PRODUCT
 
@@ -723,6 +750,11 @@ def polynomial_pdf(name, x, coeffs):
 def dalitz_pdf(name, m12sq, m13sq, resonances, masses, radius=1.5):
     """resonances: [(mass, width, Re c, Im c, channel, spin), ...]"""
     return DalitzPlotPdf(name, m12sq, m13sq, resonances, masses, radius)
+
+
+def tddp_pdf(name, m12sq, m13sq, t, resonances, masses, tau, x, y, radius=1.5):
+    """resonances as dalitz_pdf; tau, x, y: lifetime and mixing parameters"""
+    return TddpPdf(name, m12sq, m13sq, t, resonances, masses, tau, x, y, radius)
 
 
 def argus_pdf(name, x, m0, c, p):

@@ -221,6 +221,70 @@ class C4(Workload):
         return 24.0  # EventTable row: bin centre, content, volume (dataset.hpp:161-182)
 
 
+def dalitz_inside(s12, s13, M, ms):
+    """the kinematic boundary of M -> 1 2 3 in the 12 rest frame"""
+    m1, m2, m3 = ms
+    r12 = np.sqrt(np.clip(s12, 1e-300, None))
+    e1 = (s12 - m2 * m2 + m1 * m1) / (2 * r12)
+    e3 = (M * M - s12 - m3 * m3) / (2 * r12)
+    p1 = np.sqrt(np.clip(e1 * e1 - m1 * m1, 0, None))
+    p3 = np.sqrt(np.clip(e3 * e3 - m3 * m3, 0, None))
+    lo = (e1 + e3) ** 2 - (p1 + p3) ** 2
+    hi = (e1 + e3) ** 2 - (p1 - p3) ** 2
+    return (s12 >= (m1 + m2) ** 2) & (s12 <= (M - m3) ** 2) & (s13 >= lo) & (s13 <= hi)
+
+
+def dalitz_amplitude(s12, s13, s23, M, ms, R, res):
+    """numpy complex isobar amplitude at (s12, s13, s23), boundary aside (an
+    independent copy of the formulas in pf_device.cuh / pf_oracle.c)"""
+    m1, m2, m3 = ms
+    mm = {1: m1, 2: m2, 3: m3}
+
+    def q2(s, a, b):
+        return np.clip((s - (a + b) ** 2) * (s - (a - b) ** 2) / (4 * s), 0, None)
+
+    A = np.zeros_like(np.asarray(s12, dtype=np.float64), dtype=np.complex128)
+    for mass, width, cre, cim, ch, spin in res:
+        i, j = ch // 10, ch % 10
+        k = 6 - i - j
+        sv = {12: s12, 13: s13, 23: s23}
+        sij = sv[ch]
+        sik = sv[int(f"{min(i, k)}{max(i, k)}")]
+        sjk = sv[int(f"{min(j, k)}{max(j, k)}")]
+        qq = q2(sij, mm[i], mm[j])
+        q0 = q2(mass * mass, mm[i], mm[j])
+        x = np.sqrt(qq) / np.sqrt(q0)
+        if spin == 1:
+            bf2 = (1 + R * R * q0) / (1 + R * R * qq)
+            ratio = x ** 3
+            Z = sjk - sik + (M * M - mm[k] ** 2) * (mm[i] ** 2 - mm[j] ** 2) / sij
+        else:
+            bf2, ratio, Z = 1.0, x, 1.0
+        g = width * ratio * mass / np.sqrt(sij) * bf2
+        A += complex(cre, cim) * Z * np.sqrt(bf2) / (mass * mass - sij - 1j * mass * g)
+    return A
+
+
+def tddp_density(s12, s13, t, M, ms, R, res, tau, x, y):
+    """numpy TddpPdf density (pfb200.h): |A g+ + Abar g-|^2 with
+    Abar(s12, s13) = A(s12, s23), computed from its complex form"""
+    m1, m2, m3 = ms
+    s12 = np.asarray(s12, dtype=np.float64)
+    s13 = np.asarray(s13, dtype=np.float64)
+    s23 = M * M + m1 * m1 + m2 * m2 + m3 * m3 - s12 - s13
+    A = dalitz_amplitude(s12, s13, s23, M, ms, R, res)
+    Ab = dalitz_amplitude(s12, s23, s13, M, ms, R, res)
+    T = np.asarray(t, dtype=np.float64) / tau
+    # g+- = (e^{-i l1 t} +- e^{-i l2 t}) / 2 with l12 = (1 +- x)/tau... in units of 1/tau:
+    # |g+|^2 = e^-T (cosh yT + cos xT)/2, |g-|^2 = e^-T (cosh yT - cos xT)/2,
+    # g+* g- = e^-T (-sinh yT + i sin xT)/2 -- the convention of pfb200.h
+    gp2 = np.exp(-T) * (np.cosh(y * T) + np.cos(x * T)) / 2
+    gm2 = np.exp(-T) * (np.cosh(y * T) - np.cos(x * T)) / 2
+    gpgm = np.exp(-T) * (-np.sinh(y * T) + 1j * np.sin(x * T)) / 2
+    v = np.abs(A) ** 2 * gp2 + np.abs(Ab) ** 2 * gm2 + 2 * np.real(np.conj(A) * Ab * gpgm)
+    return np.where(dalitz_inside(s12, s13, M, ms), v, 0.0)
+
+
 def dalitz_amplitude2(s12, s13, M, ms, R, res):
     """numpy |A|^2 of the isobar model (the generator's copy of the kernels in
     pf_device.cuh / pf_oracle.c; used only to draw toy events)"""
@@ -264,8 +328,8 @@ def dalitz_amplitude2(s12, s13, M, ms, R, res):
     return np.where(inside, np.abs(A) ** 2, 0.0)
 
 
-class C5(Workload):
-    name = "C5"
+class C5TI(Workload):
+    name = "C5TI"
     description = ("DalitzPlotPdf D0 -> pi+ pi- pi0 (rho+, rho-, rho0, f0(980) isobars), time-integrated, "
                    "m12^2 x m13^2 grid 1024")
     default_n = 10_000_000
@@ -347,4 +411,89 @@ class C5(Workload):
         return 16.0
 
 
-WORKLOADS = {w.name: w for w in (C1(), C2(), C3(), C4(), C5())}
+class C5(C5TI):
+    """BASELINE config 5: the time-dependent Dalitz-plot fit (TddpPdf) of
+    D0 -> pi+ pi- pi0 with the C5TI isobars, decay time t in [0, 10 tau]
+    and mixing parameters x, y (pfb200.h), 1e7 events."""
+    name = "C5"
+    description = ("TddpPdf D0 -> pi+ pi- pi0 (rho+, rho-, rho0, f0(980) isobars) with mixing, "
+                   "(m12^2, m13^2, t) grid 1024")
+    tau, x_mix, y_mix = 0.4101, 0.0039, 0.0065  # ps; D0 lifetime and mixing (PDG-like)
+    tmax = 10 * 0.4101
+    truth = dict(C5TI.truth, tau=tau, x=x_mix, y=y_mix)
+    start = dict(C5TI.start, tau=0.41, x=0.004, y=0.006)
+
+    def build(self, pf):
+        (a12, b12), (a13, b13) = self.box()
+        s12 = pf.new_observable("m12sq", a12, b12)
+        s13 = pf.new_observable("m13sq", a13, b13)
+        t = pf.new_observable("t", 0.0, self.tmax)
+        resonances = []
+        for nm, ch, sp, m, w, re, im in self.res:
+            mv = pf.new_parameter(f"{nm}_m", self.start[f"{nm}_m"], 0.001, m - 0.05, m + 0.05)
+            wv = pf.new_parameter(f"{nm}_w", self.start[f"{nm}_w"], 0.001, 0.01, 0.5)
+            cr = pf.new_parameter(f"{nm}_re", self.start[f"{nm}_re"], 0.01, -5.0, 5.0)
+            ci = pf.new_parameter(f"{nm}_im", self.start[f"{nm}_im"], 0.01, -5.0, 5.0)
+            mv.fixed = wv.fixed = True
+            if nm == "rhop":
+                cr.fixed = ci.fixed = True
+            resonances.append((mv, wv, cr, ci, ch, sp))
+        tau = pf.new_parameter("tau", self.start["tau"], 0.001, 0.2, 0.8)
+        x = pf.new_parameter("x", self.start["x"], 0.001, -0.2, 0.2)
+        y = pf.new_parameter("y", self.start["y"], 0.001, -0.2, 0.2)
+        return [s12, s13, t], pf.tddp_pdf("d0tddp", s12, s13, t, resonances, (self.M,) + self.ms, tau, x, y, self.R)
+
+    @classmethod
+    def columns(cls, n, seed=11):
+        """accept-reject under (|A|^2 + |Abar|^2) e^-((1 - |y|) t / tau), which
+        bounds |A g+ + Abar g-|^2 (Cauchy-Schwarz; e^-T cosh yT <= e^-(1-|y|)T):
+        cell envelope of (|A|^2 + |Abar|^2) as C5TI's, t from the truncated
+        exponential of lifetime tau / (1 - |y|)"""
+        rng = np.random.default_rng(seed)
+        (a12, b12), (a13, b13) = cls.box()
+        res = [(m, w, re, im, ch, sp) for _, ch, sp, m, w, re, im in cls.res]
+        M, ms = cls.M, cls.ms
+        msum = M * M + sum(v * v for v in ms)
+
+        def both(c12, c13):
+            c23 = msum - c12 - c13
+            A = dalitz_amplitude(c12, c13, c23, M, ms, cls.R, res)
+            Ab = dalitz_amplitude(c12, c23, c13, M, ms, cls.R, res)
+            return np.where(dalitz_inside(c12, c13, M, ms), np.abs(A) ** 2 + np.abs(Ab) ** 2, 0.0)
+
+        nc, sub = 64, 16
+        h12, h13 = (b12 - a12) / nc, (b13 - a13) / nc
+        u = (np.arange(sub) + 0.5) / sub
+        f12 = (a12 + (np.arange(nc)[:, None] + u[None, :]) * h12).ravel()
+        f13 = (a13 + (np.arange(nc)[:, None] + u[None, :]) * h13).ravel()
+        g12, g13 = np.meshgrid(f12, f13, indexing="ij")
+        with np.errstate(all="ignore"):
+            v = both(g12.ravel(), g13.ravel())
+        env = 1.5 * v.reshape(nc, sub, nc, sub).max(axis=(1, 3)).ravel()
+        env[env <= 0] = 0.0
+        p = env / env.sum()
+        rate = (1.0 - abs(cls.y_mix)) / cls.tau
+        cut = 1.0 - np.exp(-rate * cls.tmax)
+        out = np.empty((3, n))
+        filled = 0
+        while filled < n:
+            k = min(2 * (n - filled) + 4096, 1 << 21)
+            cell = rng.choice(nc * nc, size=k, p=p)
+            c12 = a12 + (cell // nc + rng.random(k)) * h12
+            c13 = a13 + (cell % nc + rng.random(k)) * h13
+            ct = -np.log1p(-rng.random(k) * cut) / rate
+            with np.errstate(all="ignore"):
+                f = tddp_density(c12, c13, ct, M, ms, cls.R, res, cls.tau, cls.x_mix, cls.y_mix)
+            keep = rng.random(k) * env[cell] * np.exp(-rate * ct) < f
+            take = min(int(keep.sum()), n - filled)
+            out[0, filled:filled + take] = c12[keep][:take]
+            out[1, filled:filled + take] = c13[keep][:take]
+            out[2, filled:filled + take] = ct[keep][:take]
+            filled += take
+        return out
+
+    def bytes_per_unit(self):
+        return 24.0
+
+
+WORKLOADS = {w.name: w for w in (C1(), C2(), C3(), C4(), C5(), C5TI())}

@@ -115,7 +115,7 @@ def test_argus_sample_vs_restatement():
 
 def test_dalitz_sample_vs_restatement():
     from paper_1311_1753_b200.workloads import WORKLOADS
-    W = WORKLOADS["C5"]
+    W = WORKLOADS["C5TI"]
     obs, pdf = W.build(pf)
     got = pf.generate_events(pdf, obs, 2000, 23, pf.GridSpec(256)).columns()
     want = restated_generate(pf, pdf, obs, 2000, 23, 256)

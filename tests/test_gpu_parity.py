@@ -347,7 +347,7 @@ def test_c5_dalitz_vs_oracle():
     """C5 shape: DalitzPlotPdf, 4 isobars, 2-D normalisation grid (128 here so
     the oracle's walk stays short).  No reference code: parity against the C
     restatement, itself checked against numpy in test_oracle.py."""
-    W = WORKLOADS["C5"]
+    W = WORKLOADS["C5TI"]
     obs, pdf = W.build(pf)
     ds = pf.UnbinnedDataSet.from_columns(obs, W.columns(20_011, seed=4))
     bm = pf.BoundModel(pdf, ds, pf.GridSpec(128))
@@ -423,7 +423,7 @@ def test_c5_boundary_decisions_match_oracle():
     both s12 edges): the fast boundary test (pf_dalitz_inside_fast) decides
     every one like the oracle's exactly rounded sequence — a single flip would
     move the NLL by ~690 (floor) and the floor count."""
-    W = WORKLOADS["C5"]
+    W = WORKLOADS["C5TI"]
     obs, pdf = W.build(pf)
     M, (m1, m2, m3) = W.M, W.ms
     rng = np.random.default_rng(8)
@@ -552,3 +552,34 @@ def test_more_devices_than_visible_is_refused():
     with pytest.raises(pf.Error) as ei:
         pf.BoundModel(pdf, ds, pf.GridSpec(), pf.Backend.gpus(torch.cuda.device_count() * 2))
     assert ei.value.args[0].startswith("bad-backend")
+
+
+@pytest.mark.parametrize("mix", [(0.4101, 0.0039, 0.0065), (0.41, 0.15, -0.12)])
+def test_c5_tddp_vs_oracle(mix):
+    """C5 (BASELINE config 5): TddpPdf over (m12^2, m13^2, t), separable 3-D
+    normalisation on the GPU (8 Dalitz-grid + 8 time-grid component sums)
+    against the C restatement (its separable sum pinned to the brute-force
+    3-D walk in test_oracle.py, its density to numpy).  Parity unpinned by
+    nature (no reference code)."""
+    W = WORKLOADS["C5"]
+    obs, pdf = W.build(pf)
+    ds = pf.UnbinnedDataSet.from_columns(obs, W.columns(20011, seed=4))
+    grid = 64
+    bm = pf.BoundModel(pdf, ds, pf.GridSpec(grid))
+    o = oracle.Oracle(pdf, ds, grid)
+    names = [v.name for v in bm.registry().parameters()]
+    assert names == o.param_names()
+    p = [W.truth[n] for n in names]
+    p[names.index("tau")], p[names.index("x")], p[names.index("y")] = mix
+    got, want = bm.eval_metric(p), o.eval(p)
+    assert close(got, want), (got, want, abs(got - want) / abs(want))
+    assert close(pdf.cached_norm(), o.norms()[0][0])
+    q = list(p)
+    q[names.index("rhom_re")] *= 1.1
+    assert close(bm.eval_metric(q), o.eval(q))
+    # batched == sequential
+    assert np.array_equal(bm.eval_metric_batch(np.array([p, q])), [bm.eval_metric(p), bm.eval_metric(q)])
+    # tau <= 0: the normalisation fails -> the reference's penalty (engine.hpp:174-178)
+    r = list(p)
+    r[names.index("tau")] = -0.1
+    assert bm.eval_metric(r) == o.eval(r) == pf.kPenaltyValue

@@ -191,7 +191,7 @@ def test_argus_evaluator_compiles():
 
 def test_dalitz_evaluator_compiles_and_validates():
     from paper_1311_1753_b200.workloads import WORKLOADS
-    W = WORKLOADS["C5"]
+    W = WORKLOADS["C5TI"]
     obs, pdf = W.build(pf)
     g = pf.GraphDesc(pdf, obs)
     o = (C.c_int32 * 2)(g.var_index(obs[0]), g.var_index(obs[1]))

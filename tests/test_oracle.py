@@ -122,7 +122,7 @@ def test_dalitz_restatement_vs_numpy():
     constant 1/norm at every point of the plot, and 0 outside."""
     import numpy as np
     from paper_1311_1753_b200.workloads import WORKLOADS, dalitz_amplitude2
-    W = WORKLOADS["C5"]
+    W = WORKLOADS["C5TI"]
     obs, pdf = W.build(pf)
     pts = W.columns(2000, seed=3)
     ds = pf.UnbinnedDataSet.from_columns(obs, pts)
@@ -154,3 +154,54 @@ def test_generate_restatement_matches_reference_samples():
         pdf, obs, n, seed, grid = CASES[name](pf)
         cols = restated_generate(pf, pdf, obs, n, seed, grid)
         assert hashlib.sha256(np.ascontiguousarray(cols).tobytes()).hexdigest() == golden[name]["sha256"], name
+
+
+def _tddp_case(n=2000, seed=3):
+    from paper_1311_1753_b200.workloads import WORKLOADS
+    W = WORKLOADS["C5"]
+    obs, pdf = W.build(pf)
+    pts = W.columns(n, seed=seed)
+    return W, obs, pdf, pts
+
+
+def test_tddp_restatement_vs_numpy():
+    """TddpPdf has no reference code (parity unpinned): the C oracle's
+    expanded density is checked against an independent numpy evaluation of
+    the complex form |A g+ + Abar g-|^2 (workloads.tddp_density): density /
+    numpy must be the constant 1/norm, for physical and exaggerated mixing"""
+    import numpy as np
+    from paper_1311_1753_b200.workloads import tddp_density
+    W, obs, pdf, pts = _tddp_case()
+    ds = pf.UnbinnedDataSet.from_columns(obs, pts)
+    o = oracle.Oracle(pdf, ds, 16)
+    names = o.param_names()
+    res = [(m, w, re, im, ch, sp) for _, ch, sp, m, w, re, im in W.res]
+    for tau, x, y in ((W.tau, W.x_mix, W.y_mix), (0.41, 0.15, -0.12), (0.35, -0.08, 0.19)):
+        p = [W.truth[nm] for nm in names]
+        p[names.index("tau")], p[names.index("x")], p[names.index("y")] = tau, x, y
+        dens = o.density(p, pts)
+        ref = tddp_density(pts[0], pts[1], pts[2], W.M, W.ms, W.R, res, tau, x, y)
+        assert np.all(ref > 0)
+        ratio = dens / ref
+        assert np.max(np.abs(ratio / ratio[0] - 1.0)) < 1e-12, (tau, x, y)
+
+
+def test_tddp_separable_norm_is_the_3d_midpoint_sum():
+    """the oracle (and the GPU) normalise a TddpPdf by the separable form of
+    the 3-D midpoint sum; at a small grid it equals the brute-force walk over
+    all n^3 (s12, s13, t) points (midpoint_sum, pdf.hpp:148-176) to rounding"""
+    W, obs, pdf, pts = _tddp_case(500)
+    ds = pf.UnbinnedDataSet.from_columns(obs, pts)
+    names = oracle.Oracle(pdf, ds, 12).param_names()
+    p = [W.truth[nm] for nm in names]
+    p[names.index("x")], p[names.index("y")] = 0.15, -0.12
+    sep = oracle.Oracle(pdf, ds, 12)
+    a = sep.eval(p)
+    os.environ["PO_TDDP_BRUTE"] = "1"
+    try:
+        brute = oracle.Oracle(pdf, ds, 12)
+        b = brute.eval(p)
+    finally:
+        del os.environ["PO_TDDP_BRUTE"]
+    assert abs(a - b) <= 1e-13 * abs(b)
+    assert abs(sep.norms()[0][0] - brute.norms()[0][0]) <= 1e-13 * abs(brute.norms()[0][0])
