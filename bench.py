@@ -116,7 +116,32 @@ def peaks():
         return 6650.0, "fallback"
 
 
-NCU_TAGS = ("r1m", "r1l", "r1j", "r1i", "r1h", "r1g", "r1f", "r1e")  # newest first
+NCU_TAGS = ("r2", "r1n", "r1m", "r1l", "r1j", "r1i", "r1h", "r1g", "r1f", "r1e")  # newest first
+FP64_BOUND = ("C4", "C5", "C5TI")  # FP64-pipe-bound configs (ncu: FP64 pipe 42-61 %, HBM < 11 %)
+
+
+def fp64_peak():
+    """the builder-measured FP64 peak (profiles/fp64_peak.json: a DFMA
+    microkernel, tools/fp64_peak.cu) -- MEASURED_PEAKS.json has none"""
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp64_peak.json")) as fh:
+            return float(json.load(fh)["fp64_tflops"]), "builder-measured (profiles/fp64_peak.json, DFMA microkernel)"
+    except Exception:
+        return 37.0, "nominal (148 SM x 64 DFMA/clk x 2 x 1.965 GHz)"
+
+
+def fp64_ops(config):
+    """algorithmic FP64 flops per unit of the config's dominant kernel, from
+    the newest committed SASS op-count capture (tools/fp64_count.sh ->
+    profiles/<tag>_fp64_ops.json; DADD, DMUL 1 flop, DFMA 2)"""
+    for tag in NCU_TAGS:
+        p = os.path.join(ROOT, "profiles", f"{tag}_fp64_ops.json")
+        if os.path.exists(p):
+            with open(p) as fh:
+                d = json.load(fh)
+            if config in d:
+                return d[config], os.path.relpath(p, ROOT)
+    return None, None
 
 
 def ncu_summary_path(config):
@@ -562,20 +587,39 @@ def main():
     if ev_ms:
         algo_bytes = W.bytes_per_unit() * n_local  # EventTable columns read per call
         achieved = algo_bytes / (ev_ms * 1e-3) / 1e9
-        line["roofline"] = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                            "frac": achieved / hbm_peak,
-                            "traffic": ncu_traffic(W.name),
-                            "traffic_source": os.path.relpath(ncu_summary_path(W.name), ROOT) +
-                                              " (ncu --set full, 1 launch)",
-                            "kernel": "pf_event_kernel", "kernel_ms": ev_ms,
-                            "algorithmic_bytes_per_launch": algo_bytes,
-                            "kernel_share_of_step": ev_ms / ms_step, "peak_kind": peak_kind}
+        kernel = res_kernel_name(bm)
+        hbm = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+               "frac": achieved / hbm_peak,
+               "traffic": ncu_traffic(W.name),
+               "traffic_source": os.path.relpath(ncu_summary_path(W.name), ROOT) + " (ncu --set full, 1 launch)",
+               "kernel": kernel, "kernel_ms": ev_ms,
+               "algorithmic_bytes_per_launch": algo_bytes,
+               "kernel_share_of_step": ev_ms / ms_step, "peak_kind": peak_kind}
+        ops, ops_src = fp64_ops(W.name)
+        fp64 = None
+        if ops:
+            pk, pk_kind = fp64_peak()
+            flops = ops["flops_per_unit"] * n_local
+            fa = flops / (ev_ms * 1e-3) / 1e12
+            fp64 = {"bound": "fp64", "achieved": fa, "peak": pk, "unit": "TFLOP/s", "frac": fa / pk,
+                    "traffic": hbm["traffic"], "kernel": kernel, "kernel_ms": ev_ms,
+                    "algorithmic_flops_per_launch": flops, "flops_per_unit": ops["flops_per_unit"],
+                    "flops_source": ops_src + " (DADD, DMUL = 1 flop, DFMA = 2; per unit, ncu SASS op counters)",
+                    "kernel_share_of_step": ev_ms / ms_step, "peak_kind": pk_kind}
+        if W.name in FP64_BOUND and fp64:
+            line["roofline"] = fp64
+            line["roofline"]["hbm_view"] = {k: hbm[k] for k in ("achieved", "peak", "unit", "frac")}
+        else:
+            line["roofline"] = hbm
+            if fp64:
+                line["roofline"]["fp64_view"] = {k: fp64[k] for k in ("achieved", "peak", "unit", "frac",
+                                                                      "flops_per_unit")}
         # the event pass is issue/FP64-pipe limited rather than HBM limited:
         # the ncu-measured pipe utilisation of the same capture beside it
-        fp64, _ = ncu_metric(W.name, "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active")
+        fp64p, _ = ncu_metric(W.name, "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active")
         issue, _ = ncu_metric(W.name, "smsp__issue_active.avg.pct_of_peak_sustained_active")
-        if fp64 is not None:
-            line["roofline"]["fp64_pipe_active_frac_ncu"] = fp64 / 100.0
+        if fp64p is not None:
+            line["roofline"]["fp64_pipe_active_frac_ncu"] = fp64p / 100.0
         if issue is not None:
             line["roofline"]["issue_active_frac_ncu"] = issue / 100.0
     if world == 1 and not args.no_fit and W.has_reference:  # otherwise no reference fit to compare with
@@ -592,6 +636,17 @@ def main():
     print(json.dumps(line))
     if dist is not None:
         dist.destroy_process_group()
+
+
+def res_kernel_name(bm):
+    """the kernel the bench's event timing measures: the single fused kernel
+    (setup + event pass, K = 1 small-grid models) or the event pass"""
+    import ctypes as C
+    from paper_1311_1753_b200 import parfit as pf
+    try:
+        return "pf_fused_kernel" if pf.lib.pf_model_fused(C.c_void_p(bm._h)) else "pf_event_kernel"
+    except AttributeError:
+        return "pf_event_kernel"
 
 
 class _Null:

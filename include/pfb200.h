@@ -307,6 +307,10 @@ PF_API void pf_shard_events(uint64_t n_events, uint64_t chunk, int32_t shard_cou
 /* Events per reduction chunk of a bound model (warp sub-chunks x 32 lanes x
  * events per lane); shard boundaries fall on whole chunks. */
 PF_API uint64_t pf_model_chunk(const pf_model* model);
+/* 1 when this model's single-parameter-set call is the one fused kernel
+ * (pf_fused_kernel: setup in every CTA + event pass), 0 for the setup/norm
+ * kernels + event pass graph; known once a call has run */
+PF_API int32_t pf_model_fused(const pf_model* model);
 
 /* ---- fit-manager --------------------------------------------------------- */
 

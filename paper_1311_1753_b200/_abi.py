@@ -118,6 +118,7 @@ _SIGNATURES = {
     "pf_shard_events": (None, [C.c_uint64, C.c_uint64, C.c_int32, C.c_int32, C.POINTER(C.c_uint64),
                                C.POINTER(C.c_uint64)]),
     "pf_model_chunk": (C.c_uint64, [C.c_void_p]),
+    "pf_model_fused": (C.c_int32, [C.c_void_p]),
     "pf_abi_version": (C.c_int32, []),
     "pf_device_count": (C.c_int32, []),
     "pf_kernel_launches": (C.c_uint64, []),

@@ -281,6 +281,7 @@ void pf_shard_events(uint64_t n_events, uint64_t chunk, int32_t shard_count, int
 }
 
 uint64_t pf_model_chunk(const pf_model* m) { return m ? m->impl->chunk() : 0; }
+int32_t pf_model_fused(const pf_model* m) { return m && m->impl->fused_path() ? 1 : 0; }
 
 uint64_t pf_log_floor_count(const pf_model* m) { return m ? m->impl->floor_count() : 0; }
 uint64_t pf_clamp_count(const pf_model* m, int32_t node) { return m ? m->impl->clamp_count(node) : 0; }

@@ -206,6 +206,7 @@ class Model {
   const Layout& layout() const { return L_; }
   uint64_t n_events() const { return n_events_; }
   uint64_t chunk() const { return chunk_; }
+  bool fused_path() const { return !shards_.empty() && shards_[0].fused; }
   bool binned() const { return binned_; }
   uint64_t floor_count() const { return floor_total_; }
   uint64_t clamp_count(int node);
