@@ -644,7 +644,7 @@ def res_kernel_name(bm):
     import ctypes as C
     from paper_1311_1753_b200 import parfit as pf
     try:
-        return "pf_fused_kernel" if pf.lib.pf_model_fused(C.c_void_p(bm._h)) else "pf_event_kernel"
+        return "pf_fused_kernel" if pf.lib.pf_model_fused(bm._h) else "pf_event_kernel"
     except AttributeError:
         return "pf_event_kernel"
 
