@@ -613,45 +613,48 @@ __device__ __forceinline__ pf_fk pf_fk_get(const pf_args& a, int k) {
 }
 
 #ifdef PF_QFAST
-// Mixture fast path: AddPdf of two Exp/Gauss children of one observable,
-// the per-call proof K.qfast holding (codegen.cpp: every event's terms in
-// range, no floor, |d| <= 700, quadratic terms <= 4096).  With
-// u_i = log(coef_i raw_i) = a_i x^2 + b_i x + c_i and d = u0 - u1,
-//   -log v = -(max(u0, u1) + log(1 + e^-|d|)),  max(u0, u1) = (u0 + u1 + |d|) / 2,
-// so per event: d by two FMAs, e^-|d| = 2^(k/1024) e^r by a 1024-entry table
-// and a quartic (|r| <= ln2/2048: truncation r^5/120 < 4e-20), and the lane
-// sums x, x^2, |d| and two products of (1 + e^-|d|).  Sum (u0 + u1) over the
-// lane's events is one quadratic in (sum x^2, sum x, n) per sub-chunk; the
-// result is the log-form accumulator {sum L, product F} of the other paths.
-// 14 FP64 instructions per event.
+// Mixture fast path: AddPdf of two Exp/Gauss children of one observable, the
+// per-call proof K.qfast holding (codegen.cpp: every event's terms in range,
+// no floor, |d| <= 700, d's quadratic terms <= 256).  Centred at m (a
+// Gaussian child's mean), t = x - m; u_i = log(coef_i raw_i) are quadratics
+// in t; base child b, d = u_o - u_b:
+//   -log v = -(max(u_o, u_b) + log(1 + e^-|d|)),  max = u_b + (d + |d|) / 2,
+// so per event: t, d by two FMAs, u_b by one (ExpPdf base), the lane sums
+// of u_b and d + |d| (exact), and e^-|d| = 2^(k/1024) e^r by a 1024-entry
+// table and a quartic (|r| <= ln2/2048: truncation r^5/120 < 4e-20: smooth
+// at the ulp level in the parameters, which the reference minimiser's
+// finite differences need) multiplied into two products of (1 + e^-|d|).
+// The result is the log-form accumulator {sum L, product F} of the other
+// paths.  16 FP64 instructions per event (the general fast path: 19).
 template <bool FULL>
 __device__ __forceinline__ pf_lacc pf_qfast_terms(const double* st, int lane, int n_valid, const pf_fk& K) {
-  const double qA = K.q[0], qB = K.q[1], qC = K.q[2];
-  double sx = 0.0, sxx = 0.0, sd = 0.0, p0 = 1.0, p1 = 1.0;
-  int n = 0;
-  const double2* s2 = reinterpret_cast<const double2*>(st);
+  const double zm = K.q[0], qA = K.q[1], qB = K.q[2], qC = K.q[3];
+  const double ba = K.q[4], bb = K.q[5], bc = K.q[6];
+  double s1 = 0.0, s2 = 0.0, p0 = 1.0, p1 = 1.0;
+  const double2* s2v = reinterpret_cast<const double2*>(st);
 #pragma unroll
   for (int j = 0; j < PF_EPT / 2; ++j) {
     const int i = 32 * j + lane;  // this lane's events 2i and 2i + 1 of the stage
-    const double2 xv = s2[i];
+    const double2 xv = s2v[i];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const bool valid = FULL || 2 * i + h < n_valid;
-      const double x = valid ? (h ? xv.y : xv.x) : 0.0;
-      const double d = fma(fma(qA, x, qB), x, qC);
-      const double ad = valid ? fabs(d) : 0.0;
-      sx += x;
-      sxx = fma(x, x, sxx);
-      sd += ad;
+      const double t = (h ? xv.y : xv.x) - zm;
+      const double d = fma(fma(qA, t, qB), t, qC);
+#ifdef PF_QFAST_LINEAR_BASE
+      const double ub = fma(bb, t, bc);
+      (void)ba;
+#else
+      const double ub = fma(fma(ba, t, bb), t, bc);
+#endif
+      const double ad = fabs(d);
+      s1 += valid ? ub : 0.0;
+      s2 += valid ? d + ad : 0.0;
       const double kd = fma(-ad, PF_Q_INVLN2N, 0x1.8p52);
       const int ki = __double2loint(kd);
       const double k = kd - 0x1.8p52;
       const double r = fma(k, -PF_Q_LN2N, -ad);
       const double T = pf_exp2_1024[ki & 1023];
-      // e^r - 1 = r (1 + r/2 + r^2/6 + r^3/24): truncation r^5/120 < 4e-20,
-      // so e^-|d| is smooth at the ulp level in the parameters (the cubic's
-      // 5.5e-16 ripple with period ln2/1024 in d made the reference
-      // minimiser's finite-difference gradients noisy)
       double pp = fma(r, 1.0 / 24.0, 1.0 / 6.0);
       pp = fma(pp, r, 0.5);
       pp = fma(pp, r, 1.0);
@@ -662,12 +665,10 @@ __device__ __forceinline__ pf_lacc pf_qfast_terms(const double* st, int lane, in
         p0 = fma(p0, e, p0);
       else
         p1 = fma(p1, e, p1);
-      n += valid ? 1 : 0;
     }
   }
   pf_lacc out;
-  const double nn = FULL ? (double)PF_EPT : (double)n;
-  out.v[0] = 0.5 * (fma(K.q[3], sxx, fma(K.q[4], sx, nn * K.q[5])) + sd);
+  out.v[0] = fma(0.5, s2, s1);
   out.v[1] = p0 * p1;
   return out;
 }
