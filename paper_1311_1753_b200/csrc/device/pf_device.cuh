@@ -14,6 +14,24 @@ typedef unsigned long long pf_u64;
 typedef long long pf_i64;
 typedef unsigned int pf_u32;
 
+// PF_CHECKS (PFB200_DEFINES=PF_CHECKS): device-side bounds checks on every
+// TMA copy, shared-memory stage, task and record index -- the substitute for
+// compute-sanitizer, which this GPU pool does not allow; a failed check traps
+// (the call then fails with a CUDA error instead of reading out of bounds)
+#ifdef PF_CHECKS
+#define PF_CHECK(cond)                                                                       \
+  do {                                                                                      \
+    if (!(cond)) {                                                                          \
+      printf("PF_CHECK failed: %s (block %d thread %d)\n", #cond, blockIdx.x, threadIdx.x); \
+      __trap();                                                                             \
+    }                                                                                       \
+  } while (0)
+#else
+#define PF_CHECK(cond) \
+  do {                 \
+  } while (0)
+#endif
+
 #define PF_THREADS 256
 #define PF_FINAL_THREADS 1024
 #define PF_LOG_FLOOR 1e-300   // engine.hpp:50 kLogFloor

@@ -146,6 +146,7 @@ __device__ __forceinline__ void pf_setup_core(const pf_args& a, int k, unsigned 
     for (int q = 0; q < PF_SETUP_MAXQ; ++q) {
       x[q] = 0.0;
       if (q < nl) {
+        PF_CHECK(t0 + q < nt && t0 + q < 16);
         const pf_task& T = tk[t0 + q];
         const pf_u64 np = T.points;
 #pragma unroll 4
@@ -308,6 +309,7 @@ extern "C" __global__ void __launch_bounds__(PF_THREADS) pf_norm_kernel(const __
   int t = 0;
   while (t + 1 < a.n_tasks && (int)blockIdx.x >= a.tasks[t + 1].first_block) ++t;
   const pf_task& T = a.tasks[t];
+  PF_CHECK(t < a.n_tasks && (int)blockIdx.x >= T.first_block && (int)blockIdx.x < T.first_block + T.n_blocks);
   const pf_u64 b = (pf_u64)((int)blockIdx.x - T.first_block);
   const pf_u64 lo = b * T.per_block;
   const pf_u64 hi = min(lo + T.per_block, T.points);
@@ -894,6 +896,7 @@ __device__ void pf_finalize_warp0(const pf_args& a, int lane, const double* S0 =
   static_assert(PF_FX_BINS == 32, "one bin per lane of warp 0");
   {
     for (int k = 0; k < a.K; ++k) {
+      PF_CHECK(k < PF_MAX_BATCH && lane < PF_FX_BINS);
       const pf_krec* r = a.rec + k;
       long long* bin = a.fxbins + ((pf_u64)k * PF_FX_BINS + lane) * PF_FX_BIN_STRIDE;
       long long d[PF_FX_DIGITS];
@@ -1016,6 +1019,7 @@ extern "C" __global__ void __launch_bounds__(PF_EV_THREADS, PF_EVENT_MIN_BLOCKS)
       const pf_u64 c = (pf_u64)gw + (pf_u64)(w / PF_NSUB) * (pf_u64)nw;
       const pf_u64 base = c * (PF_SUB * PF_NSUB) + (pf_u64)(w % PF_NSUB) * PF_SUB;
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      PF_CHECK(c < (pf_u64)a.n_chunks && base + PF_SUB <= a.col_stride && s < PF_NST);
       pf_mbar_expect_tx(mybar + s, PF_STAGE * 8);
 #pragma unroll
       for (int q = 0; q < PF_NLOAD; ++q)
@@ -1221,6 +1225,7 @@ extern "C" __global__ void __launch_bounds__(PF_FUSED_THREADS, 1) pf_fused_kerne
       const int st = v % PF_NST;
       const pf_u64 base = (pf_u64)c * (PF_SUB * PF_NSUB) + (pf_u64)(v % PF_NSUB) * PF_SUB;
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      PF_CHECK(c < nch && base + PF_SUB <= a.col_stride && st < PF_NST && gw < nwa);
       pf_mbar_expect_tx(mybar + st, PF_STAGE * 8);
 #pragma unroll
       for (int q = 0; q < PF_NLOAD; ++q)
@@ -1277,6 +1282,7 @@ extern "C" __global__ void __launch_bounds__(PF_FUSED_THREADS, 1) pf_fused_kerne
       const int st = w % PF_NST;
       pf_mbar_wait(mybar + st, (unsigned)((w / PF_NST) & 1));
       const pf_u64 base = (pf_u64)c * (PF_SUB * PF_NSUB) + (pf_u64)j * PF_SUB;
+      PF_CHECK(c < nch && base < a.col_stride && st < PF_NST);
       const bool full = base + PF_SUB <= a.n_local;
       const int n_valid = full ? PF_SUB : (int)(a.n_local > base ? a.n_local - base : 0);
       const pf_lacc t = full ? pf_stage_terms<true>(a, 0, base, lane, my + st * PF_STAGE, n_valid, fk, P, S)
