@@ -94,10 +94,16 @@ __device__ __forceinline__ double pf_dsmem_load(const double* p, unsigned rank) 
 // of CL CTAs splitting the grid points) and the fused kernel (every CTA
 // computes all of it, CL = 1): P and S in shared memory on return, identical
 // in every CTA.  Grid-point clamps go to `cnt`, stage clamps to `cnt_stage`.
-template <int CL>
+struct pf_no_hook {
+  __device__ void operator()() const {}
+};
+
+// after_init runs once the setup's own global loads (parameters, tasks,
+// tables) have landed: the fused pass starts its L2 prefetch there
+template <int CL, class Hook = pf_no_hook>
 __device__ __forceinline__ void pf_setup_core(const pf_args& a, int k, unsigned rank, double* P, double* S,
                                               pf_krec* r, bool init_rec, pf_ctx& cx, pf_cnt& cnt,
-                                              pf_cnt& cnt_stage) {
+                                              pf_cnt& cnt_stage, const Hook& after_init = Hook()) {
   // this CTA's run partials per task (double-double), double-buffered by level parity
   __shared__ pf_dd wpart[2][PF_SETUP_MAXQ][4];
   __shared__ double red[PF_SETUP_MAXQ][PF_SETUP_THREADS];  // the threads' partials
@@ -121,6 +127,7 @@ __device__ __forceinline__ void pf_setup_core(const pf_args& a, int k, unsigned 
     reinterpret_cast<pf_u64*>(tk)[i] = reinterpret_cast<const pf_u64*>(a.tasks)[i];
   if (init_rec && threadIdx.x == 0 && rank == 0) pf_rec_init(r);
   pf_math_init();  // includes __syncthreads
+  after_init();
   // the record is initialised before any CTA of the cluster reports into it
   if (CL > 1) pf_cluster_sync();
   PF_TRACE("init");
@@ -1245,7 +1252,30 @@ extern "C" __global__ void __launch_bounds__(PF_FUSED_THREADS, 1) pf_fused_kerne
   // (DSMEM exchange), exactly as the setup kernel of the batched path splits
   // them: batched and single calls stay bitwise equal
   const unsigned rank = PF_SETUP_CLUSTER > 1 ? pf_cluster_rank() : 0u;
+#ifdef PF_L2_PREFETCH_FIRST
+  // the sub-chunks beyond the ring of this warp's first PF_L2_PREFETCH_FIRST
+  // chunks into L2 while the setup computes: HBM keeps streaming, and the
+  // loop's first TMA copies hit L2
+  auto hook = [&]() {
+    if (lane == 0 && n_mine > 0) {
+      const pf_u64 b0 = (pf_u64)gw * (PF_SUB * PF_NSUB) + (pf_u64)PF_NST * PF_SUB;
+      const int m = n_mine < PF_L2_PREFETCH_FIRST ? n_mine : PF_L2_PREFETCH_FIRST;
+      for (int j = 0; j < m; ++j) {
+        const pf_u64 b = j == 0 ? b0 : (pf_u64)(gw + j * nwa) * (PF_SUB * PF_NSUB);
+        const unsigned bytes = (unsigned)((j == 0 ? PF_SUB * (PF_NSUB - PF_NST) : PF_SUB * PF_NSUB) * 8);
+#pragma unroll
+        for (int q = 0; q < PF_NLOAD; ++q)
+          if (bytes)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.data + (pf_u64)pf_load_col(q) * a.col_stride + b),
+                         "r"(bytes)
+                         : "memory");
+      }
+    }
+  };
+  pf_setup_core<PF_SETUP_CLUSTER>(a, 0, rank, P, S, r, false, cx, cnt_grid, cnt_stage, hook);
+#else
   pf_setup_core<PF_SETUP_CLUSTER>(a, 0, rank, P, S, r, false, cx, cnt_grid, cnt_stage);
+#endif
   // no CTA may leave while a cluster peer could still read its setup
   // partials: arrive now, wait just before exit
   if (PF_SETUP_CLUSTER > 1) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");

@@ -8,7 +8,7 @@ for l in sys.stdin:
     elif 'Error' in l or 'error' in l: print(l)
 "; }
 run default X=1
-run cluster1 PFB200_SETUP_CLUSTER=1
-run cluster2 PFB200_SETUP_CLUSTER=2
-run nsub2 PFB200_NSUB=2
-run ept8_nsub4 PFB200_EPT=8
+run pf1 PFB200_DEFINES=PF_L2_PREFETCH_FIRST=1
+run pf2 PFB200_DEFINES=PF_L2_PREFETCH_FIRST=2
+run pf3 PFB200_DEFINES=PF_L2_PREFETCH_FIRST=3
+run default_again X=1
