@@ -48,6 +48,7 @@ typedef unsigned int pf_u32;
 #define PF_E_NONPOS_ENDPOINT 5 // ArgusPdf m0 <= 0
 #define PF_E_GROUP_TIMEOUT 6   // a peer's record never arrived (exchange group)
 #define PF_E_NONPOS_LIFETIME 7 // TddpPdf tau <= 0
+#define PF_COMP_ALL4 8         // pf_task.comp: a TddpPdf Dalitz task returning its four components
 #define PF_GROUP_MAX 16        // ranks of a peer-memory exchange group (engine.hpp kMaxGroup)
 #define PF_MAX_BATCH 16        // parameter sets per launch (engine.hpp kMaxBatch)
 

@@ -305,14 +305,16 @@ extern "C" __global__ void __launch_bounds__(PF_THREADS) pf_pre_kernel(const __g
 extern "C" __global__ void __launch_bounds__(PF_THREADS) pf_norm_kernel(const __grid_constant__ pf_args a) {
   __shared__ pf_dd sm[PF_THREADS];
   __shared__ int s_last;
-  __shared__ double sums[64];
+  __shared__ double sums[64][4];
   if (a.level == a.n_levels - 1) pf_pdl_trigger();
   pf_math_init();
   const int k = blockIdx.y;
   const double* P = a.P + (pf_u64)k * PF_NP;
   double* S = a.S + (pf_u64)k * PF_SS;
-  // one partial per block: task t owns [first_block, first_block + n_blocks)
-  pf_dd* part = a.partials + (pf_u64)k * gridDim.x;
+  // per block and value one partial: task t owns blocks [first_block,
+  // first_block + n_blocks); value c (a TddpPdf's four Dalitz components,
+  // comp 8) at part[c * gridDim.x + block]
+  pf_dd* part = a.partials + (pf_u64)k * gridDim.x * 4;
   int t = 0;
   while (t + 1 < a.n_tasks && (int)blockIdx.x >= a.tasks[t + 1].first_block) ++t;
   const pf_task& T = a.tasks[t];
@@ -324,18 +326,29 @@ extern "C" __global__ void __launch_bounds__(PF_THREADS) pf_norm_kernel(const __
   cx.err = 0;
   pf_cnt cnt;
   pf_cnt_init(cnt);
-  pf_dd acc = pf_dd_zero();
-  if (T.dims >= 2 && T.per_block >= (pf_u64)PF_THREADS * PF_NORM_RUN) {
+  const bool multi = T.comp == PF_COMP_ALL4;
+  pf_dd acc[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) acc[c] = pf_dd_zero();
+  if (multi) {
+    // all four components from ONE evaluation of both amplitudes per point
+    for (pf_u64 i = lo + threadIdx.x; i < hi; i += PF_THREADS) {
+      double v4[4];
+      pf_norm_point4(T.node, i, T, P, S, a.C, v4);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[c] = pf_dd_add_d(acc[c], v4[c]);
+    }
+  } else if (T.dims >= 2 && T.per_block >= (pf_u64)PF_THREADS * PF_NORM_RUN) {
     // runs of PF_NORM_RUN consecutive points per thread, walked row by row
     for (pf_u64 i = lo + (pf_u64)threadIdx.x * PF_NORM_RUN; i < hi; i += (pf_u64)PF_THREADS * PF_NORM_RUN)
-      acc = pf_dd_add_d(acc, pf_norm_run(T.node, i, (int)min((pf_u64)PF_NORM_RUN, hi - i), T, P, S, a.C, cx, cnt));
+      acc[0] = pf_dd_add_d(acc[0], pf_norm_run(T.node, i, (int)min((pf_u64)PF_NORM_RUN, hi - i), T, P, S, a.C, cx, cnt));
   } else {
     for (pf_u64 i = lo + threadIdx.x; i < hi; i += PF_THREADS)
-      acc = pf_dd_add_d(acc, pf_norm_point(T.node, i, T, P, S, a.C, cx, cnt));
+      acc[0] = pf_dd_add_d(acc[0], pf_norm_point(T.node, i, T, P, S, a.C, cx, cnt));
   }
-  {
-    pf_dd s = pf_block_reduce(acc, sm);
-    if (threadIdx.x == 0) part[blockIdx.x] = s;
+  for (int c = 0; c < (multi ? 4 : 1); ++c) {
+    pf_dd s = pf_block_reduce(acc[c], sm);
+    if (threadIdx.x == 0) part[(pf_u64)c * gridDim.x + blockIdx.x] = s;
   }
   if (cx.err) atomicMin(&a.rec[k].norm_error, cx.err);
   if (pf_grid_counts(a, k)) pf_cnt_flush(cnt, a.clamp);
@@ -350,15 +363,23 @@ extern "C" __global__ void __launch_bounds__(PF_THREADS) pf_norm_kernel(const __
   __threadfence();
   for (int tt = 0; tt < a.n_tasks; ++tt) {
     const pf_task& U = a.tasks[tt];
+    const int nv = U.comp == PF_COMP_ALL4 ? 4 : 1;
     if (threadIdx.x < 32) {
-      pf_dd s = pf_warp_reduce_runs(part + U.first_block, U.n_blocks);
-      if (threadIdx.x == 0) sums[tt] = __dmul_rn(pf_dd_to_double(s), U.vol);
+      for (int c = 0; c < nv; ++c) {
+        pf_dd s = pf_warp_reduce_runs(part + (pf_u64)c * gridDim.x + U.first_block, U.n_blocks);
+        if (threadIdx.x == 0) sums[tt][c] = __dmul_rn(pf_dd_to_double(s), U.vol);
+      }
     }
   }
   __syncthreads();
   if (threadIdx.x == 0)
-    for (int tt = 0; tt + 1 < a.n_tasks; tt += 2)
-      pf_finish_task(S, a.rec + k, a.tasks[tt], sums[tt], sums[tt + 1]);
+    for (int tt = 0; tt + 1 < a.n_tasks; tt += 2) {
+      if (a.tasks[tt].comp == PF_COMP_ALL4) {
+        for (int c = 0; c < 4; ++c) pf_store_comp(S, a.tasks[tt].node, c, sums[tt][c], sums[tt + 1][c]);
+      } else {
+        pf_finish_task(S, a.rec + k, a.tasks[tt], sums[tt][0], sums[tt + 1][0]);
+      }
+    }
   __syncthreads();
   pf_ctx cx2;
   cx2.err = 0;

@@ -279,8 +279,10 @@ Model::Model(const pf_graph& g, const pf_data& d, uint32_t grid_points, const pf
   }
   int most_in_level = 0;
   for (int n : level_n_tasks_) most_in_level = std::max(most_in_level, n);
+  bool multi = false;
+  for (const Task& t : tasks_) multi |= t.comp == kCompAll4;  // four values per task: the norm kernel only
   small_norms_ = norm_work <= kSmallNormWork && setup_smem_bytes() <= 48 * 1024 && tasks_.size() <= 16 &&
-                 most_in_level <= L_.setup_maxq;
+                 most_in_level <= L_.setup_maxq && !multi;
 
   ck(cudaSetDevice(opt.device), "cudaSetDevice");
   // parameters and results live in mapped (zero-copy) pinned memory: the
@@ -332,7 +334,7 @@ Model::Model(const pf_graph& g, const pf_data& d, uint32_t grid_points, const pf
          "upload tasks");
     size_t part_elems = static_cast<size_t>(kMaxBatch) *
                         std::max<size_t>(std::max<size_t>(sh.n_chunks, max_norm_blocks_), 1);
-    ck(cudaMalloc(&sh.d_partials, 16 * part_elems), "cudaMalloc partials");
+    ck(cudaMalloc(&sh.d_partials, 16 * 4 * part_elems), "cudaMalloc partials");  // 4 values per block (kCompAll4)
     ck(cudaMalloc(&sh.d_done, sizeof(uint32_t) * (1 + kMaxBatch)), "cudaMalloc done");
     ck(cudaMemset(sh.d_done, 0, sizeof(uint32_t) * (1 + kMaxBatch)), "memset done");
     ck(cudaMalloc(&sh.d_recv, sizeof(int64_t) * 2 * 16 * kMaxGroup * kMaxBatch), "cudaMalloc group receive");
@@ -508,8 +510,11 @@ void Model::add_tddp_tasks(int node, uint32_t grid_points, int lvl, int* blocks)
   };
   const BoxDim* dims[3] = {&box_of(nd.obs_cols[0]), &box_of(nd.obs_cols[1]), &box_of(nd.obs_cols[2])};
   const double cost = subtree_cost(pg_, node);
-  for (int comp = 0; comp < 8; ++comp) {
-    const bool time = comp >= 4;
+  // the Dalitz grid: ONE task pair whose points yield all four components
+  // (kCompAll4: both amplitudes evaluated once per point); the time grid:
+  // one pair per component (cheap)
+  for (int comp : {kCompAll4, 4, 5, 6, 7}) {
+    const bool time = comp != kCompAll4;
     for (int fine = 0; fine < 2; ++fine) {
       Task t;
       std::memset(&t, 0, sizeof t);
@@ -531,7 +536,7 @@ void Model::add_tddp_tasks(int node, uint32_t grid_points, int lvl, int* blocks)
       t.vol = vol;
       t.points = total;
       uint64_t per = static_cast<uint64_t>(std::max(1.0, std::floor(4096.0 / (time ? 8.0 : cost))));
-      if (!time) per = std::max<uint64_t>(per, 256ull * 32ull);
+      if (!time) per = std::max<uint64_t>(per, 256ull * 4ull);
       uint64_t nb = (total + per - 1) / per;
       if (nb > 4096) {
         nb = 4096;
