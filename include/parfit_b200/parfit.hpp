@@ -302,7 +302,7 @@ inline EventTable to_event_table(const BinnedDataSet& ds) {
 
 // ---- pdf.hpp ----------------------------------------------------------------
 enum class PdfKind { Exponential, Gaussian, BreitWigner, Polynomial, Product, Sum, Composite, Mapped,
-                     Convolution, Argus, Dalitz };
+                     Convolution, Argus, Dalitz, Tddp };
 
 struct GridSpec {
   std::size_t points = 1024;
@@ -471,6 +471,30 @@ class DalitzPlotPdf final : public PdfNode {
   }
 };
 
+// Time-dependent Dalitz-plot PDF with mixing (not in the reference; BASELINE
+// config 5, GooFit's TDDP): |A g+(t) + Abar g-(t)|^2 with Abar(s12, s13) =
+// A(s12, s23), observables m12^2, m13^2, t; the DalitzPlotPdf resonances, then
+// tau, x, y (pfb200.h PF_TDDP).  Daughters 1 and 2 are CP conjugates (m1 == m2).
+class TddpPdf final : public PdfNode {
+ public:
+  TddpPdf(std::string name, VariablePtr m12sq, VariablePtr m13sq, VariablePtr t,
+          const std::vector<DalitzResonance>& res, double M, double m1, double m2, double m3, VariablePtr tau,
+          VariablePtr x, VariablePtr y, double radius = 1.5)
+      : PdfNode(std::move(name), PdfKind::Tddp) {
+    DalitzPlotPdf amp(name_, m12sq, m13sq, res, M, m1, m2, m3, radius);  // the same checks
+    need_obs(name_, t, "t");
+    need_par(name_, tau, "tau");
+    need_par(name_, x, "x");
+    need_par(name_, y, "y");
+    if (!(tau->lower > 0)) throw Error("nonpositive-lifetime", name_ + ": tau limits must exclude 0");
+    if (m1 != m2) throw Error("bad-kinematics", name_ + ": daughters 1 and 2 must be CP conjugates (m1 == m2)");
+    reals_ = amp.reals();
+    params_ = amp.declared_parameters();
+    params_.insert(params_.end(), {std::move(tau), std::move(x), std::move(y)});
+    obs_ = {std::move(m12sq), std::move(m13sq), std::move(t)};
+  }
+};
+
 class ProdPdf final : public PdfNode {
  public:
   ProdPdf(std::string name, std::vector<PdfPtr> children) : PdfNode(std::move(name), PdfKind::Product) {
@@ -549,6 +573,12 @@ inline PdfPtr dalitz_pdf(std::string n, VariablePtr m12sq, VariablePtr m13sq, co
                          double M, double m1, double m2, double m3, double radius = 1.5) {
   return std::make_shared<DalitzPlotPdf>(std::move(n), std::move(m12sq), std::move(m13sq), res, M, m1, m2, m3,
                                          radius);
+}
+inline PdfPtr tddp_pdf(std::string n, VariablePtr m12sq, VariablePtr m13sq, VariablePtr t,
+                       const std::vector<DalitzResonance>& res, double M, double m1, double m2, double m3,
+                       VariablePtr tau, VariablePtr x, VariablePtr y, double radius = 1.5) {
+  return std::make_shared<TddpPdf>(std::move(n), std::move(m12sq), std::move(m13sq), std::move(t), res, M, m1, m2,
+                                   m3, std::move(tau), std::move(x), std::move(y), radius);
 }
 inline PdfPtr prod_pdf(std::string n, std::vector<PdfPtr> ch) {
   return std::make_shared<ProdPdf>(std::move(n), std::move(ch));
