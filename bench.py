@@ -420,6 +420,9 @@ def main():
     if multi:
         import torch
         import torch.distributed as dist
+        # communicator logging on (NCCL's "comm ... nRanks" lines show every rank joined)
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
