@@ -74,6 +74,7 @@ struct pf_task {  // one midpoint sum: node, n points per box dimension
   double lo[PF_MAX_BOX];
   double h[PF_MAX_BOX];
   double vol;
+  double pad;  // 192 B: a whole number of 16-byte units (TMA bulk copies)
 };
 
 // Per-call result record, written by the device straight into mapped
@@ -474,7 +475,7 @@ __device__ __forceinline__ double pf_fx_round(const long long* acc) {
 
 __shared__ double2 pf_exp_tab[128];
 #ifdef PF_QFAST
-__shared__ double pf_exp2_1024[1024];  // 2^(j/1024) (pf_qfast_terms)
+__shared__ __align__(16) double pf_exp2_1024[1024];  // 2^(j/1024) (pf_qfast_terms)
 #endif
 
 // every kernel calls this before the first pf_exp (includes __syncthreads)

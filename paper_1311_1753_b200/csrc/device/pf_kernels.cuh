@@ -98,16 +98,43 @@ struct pf_no_hook {
   __device__ void operator()() const {}
 };
 
+// the setup's task table (shared memory; filled by the setup core, or by a
+// TMA bulk copy at kernel entry, pf_setup_prefetch)
+__shared__ __align__(16) pf_task pf_tk[16];
+
+// The setup's inputs, global -> shared by TMA bulk copies issued by one
+// thread at kernel entry and completing on `bar`: the task table and the exp
+// tables.  Their latency (cold after the L2 flush) then overlaps the
+// parameter copy and the TMA issue of the event stages instead of stalling
+// the setup (fused pass; measured 1.5 of its 7 us before).
+__device__ __forceinline__ void pf_setup_prefetch(const pf_args& a, pf_u64* bar) {
+  const unsigned tb = (unsigned)(min(a.n_tasks, 16) * (int)sizeof(pf_task));
+  unsigned total = tb + 2048u;
+#ifdef PF_QFAST
+  total += 8192u;
+#endif
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  pf_mbar_expect_tx(bar, total);
+  if (tb) pf_tma_load(pf_tk, a.tasks, tb, bar);
+  pf_tma_load(pf_exp_tab, pf_exp_tab_g, 2048u, bar);
+#ifdef PF_QFAST
+  pf_tma_load(pf_exp2_1024, pf_exp2_1024_g, 8192u, bar);
+#endif
+}
+
 // after_init runs once the setup's own global loads (parameters, tasks,
 // tables) have landed: the fused pass starts its L2 prefetch there
+// preloaded: the task and exp tables arrive by pf_setup_prefetch on this
+// mbarrier (phase 0) instead of being copied here
 template <int CL, class Hook = pf_no_hook>
 __device__ __forceinline__ void pf_setup_core(const pf_args& a, int k, unsigned rank, double* P, double* S,
                                               pf_krec* r, bool init_rec, pf_ctx& cx, pf_cnt& cnt,
-                                              pf_cnt& cnt_stage, const Hook& after_init = Hook()) {
+                                              pf_cnt& cnt_stage, const Hook& after_init = Hook(),
+                                              pf_u64* preloaded = nullptr) {
   // this CTA's run partials per task (double-double), double-buffered by level parity
   __shared__ pf_dd wpart[2][PF_SETUP_MAXQ][4];
   __shared__ double red[PF_SETUP_MAXQ][PF_SETUP_THREADS];  // the threads' partials
-  __shared__ pf_task tk[16];
+  pf_task* tk = pf_tk;
 #ifdef PF_SETUP_TRACE
   __shared__ long long trs[32];
   __shared__ const char* trn[32];
@@ -123,10 +150,17 @@ __device__ __forceinline__ void pf_setup_core(const pf_args& a, int k, unsigned 
     P[i] = a.npin ? a.pin[i] : a.hP[(pf_u64)k * PF_NP + i];
   for (int i = threadIdx.x; i < PF_SS; i += blockDim.x) S[i] = 0.0;
   const int nt = min(a.n_tasks, 16);
-  for (int i = threadIdx.x; i < nt * (int)(sizeof(pf_task) / 8); i += blockDim.x)
-    reinterpret_cast<pf_u64*>(tk)[i] = reinterpret_cast<const pf_u64*>(a.tasks)[i];
+  if (!preloaded)
+    for (int i = threadIdx.x; i < nt * (int)(sizeof(pf_task) / 8); i += blockDim.x)
+      reinterpret_cast<pf_u64*>(tk)[i] = reinterpret_cast<const pf_u64*>(a.tasks)[i];
   if (init_rec && threadIdx.x == 0 && rank == 0) pf_rec_init(r);
-  pf_math_init();  // includes __syncthreads
+  PF_TRACE("copy");
+  if (preloaded) {
+    pf_mbar_wait(preloaded, 0u);
+    __syncthreads();
+  } else {
+    pf_math_init();  // includes __syncthreads
+  }
   after_init();
   // the record is initialised before any CTA of the cluster reports into it
   if (CL > 1) pf_cluster_sync();
@@ -1211,6 +1245,7 @@ extern "C" __global__ void __launch_bounds__(PF_FUSED_THREADS, 1) pf_fused_kerne
 #endif
   extern __shared__ __align__(16) unsigned char pf_dyn[];
   __shared__ __align__(8) pf_u64 bars[PF_FUSED_WARPS * PF_NST];
+  __shared__ __align__(8) pf_u64 tbar;  // the setup's tables (pf_setup_prefetch)
   __shared__ long long bfx[PF_FUSED_WARPS][PF_FX_DIGITS];
   __shared__ int s_last;
   double* stages = reinterpret_cast<double*>(pf_dyn);
@@ -1230,6 +1265,11 @@ extern "C" __global__ void __launch_bounds__(PF_FUSED_THREADS, 1) pf_fused_kerne
   const bool active = gw < nwa;
   int n_mine = active ? (nch - 1 - gw) / nwa + 1 : 0;
   if (n_mine > a.kpw) n_mine = a.kpw;
+  if (threadIdx.x == 0) {
+    pf_mbar_init(&tbar, 1);
+    pf_fence_mbar_init();
+    pf_setup_prefetch(a, &tbar);
+  }
   if (lane == 0) {
     for (int s = 0; s < PF_NST; ++s) pf_mbar_init(mybar + s, 1);
     pf_fence_mbar_init();
@@ -1293,9 +1333,9 @@ extern "C" __global__ void __launch_bounds__(PF_FUSED_THREADS, 1) pf_fused_kerne
       }
     }
   };
-  pf_setup_core<PF_SETUP_CLUSTER>(a, 0, rank, P, S, r, false, cx, cnt_grid, cnt_stage, hook);
+  pf_setup_core<PF_SETUP_CLUSTER>(a, 0, rank, P, S, r, false, cx, cnt_grid, cnt_stage, hook, &tbar);
 #else
-  pf_setup_core<PF_SETUP_CLUSTER>(a, 0, rank, P, S, r, false, cx, cnt_grid, cnt_stage);
+  pf_setup_core<PF_SETUP_CLUSTER>(a, 0, rank, P, S, r, false, cx, cnt_grid, cnt_stage, pf_no_hook(), &tbar);
 #endif
   // no CTA may leave while a cluster peer could still read its setup
   // partials: arrive now, wait just before exit

@@ -45,8 +45,9 @@ struct Task {
   double lo[8];
   double h[8];
   double vol;
+  double pad;
 };
-static_assert(sizeof(Task) == 184, "pf_task layout");
+static_assert(sizeof(Task) == 192, "pf_task layout");
 
 struct Out {
   double result;

@@ -16,7 +16,7 @@ OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "paper_1311
 def main():
     lines = ["// 2^(j/128) = hi + lo (hi = RN(2^(j/128)), lo = RN(residual)); generated with",
              "// Python decimal at 60 digits (tools/gen_exp_table.py)",
-             "__device__ const double pf_exp_tab_g[256] = {"]
+             "__device__ const __align__(16) double pf_exp_tab_g[256] = {"]
     for j in range(128):
         v = (LN2 * j / 128).exp()
         hi = float(v)
@@ -33,7 +33,7 @@ def main():
     # the mixture fast path (pf_qfast_terms): 2^(j/1024) rounded to nearest,
     # one double per entry (1.1e-16 relative), and ln2/1024 as one double
     # (k * ln2/1024 by a single FMA: |k| < 2^17, error < 4e-20 |k|)
-    lines += ["// 2^(j/1024) = RN(2^(j/1024)) (pf_qfast_terms)", "__device__ const double pf_exp2_1024_g[1024] = {"]
+    lines += ["// 2^(j/1024) = RN(2^(j/1024)) (pf_qfast_terms)", "__device__ const __align__(16) double pf_exp2_1024_g[1024] = {"]
     for j in range(1024):
         lines.append(f"  {float((LN2 * j / 1024).exp()).hex()},")
     lines.append("};")
