@@ -159,6 +159,15 @@ struct pf_ctx {
   pf_u32 err;  // (node << 8) | code of the first error, 0 when none
 };
 
+// An index as a double, exactly, without the I2F conversion pipe: below 2^32
+// the integer is spliced into the mantissa of 2^52 and 2^52 subtracted
+// (exact); the grid walks convert one index per point (the setup's points
+// phase was bound on I2F.F64.U64).
+__device__ __forceinline__ double pf_idx2d(pf_u64 i) {
+  if (i < 0x100000000ull) return __hiloint2double(0x43300000, (int)(pf_u32)i) - 4503599627370496.0;
+  return (double)i;
+}
+
 __device__ __forceinline__ void pf_fail(pf_ctx& cx, int node, int code) {
   if (!cx.err) cx.err = ((pf_u32)node << 8) | (pf_u32)code;
 }
