@@ -36,7 +36,8 @@ def _dataset(pf, W, obs, n: Optional[int], data_path: Optional[str]):
 
 
 def bench_rows(workload: str, gpu_counts: Sequence[int], repetitions: int,
-               n_events: Optional[int] = None, data_path: Optional[str] = None) -> List[dict]:
+               n_events: Optional[int] = None, data_path: Optional[str] = None,
+               oversubscribe: bool = False) -> List[dict]:
     """One row per GPU count (no arity checks: `cmd_bench` applies them)."""
     from . import parfit as pf
     from .workloads import WORKLOADS
@@ -51,7 +52,7 @@ def bench_rows(workload: str, gpu_counts: Sequence[int], repetitions: int,
         for _ in range(repetitions):
             # one BoundModel per repetition, as the reference builds one per
             # run (parfit_cli.cpp:147-152); identical start every run
-            bm = pf.BoundModel(pdf, ds, pf.GridSpec(W.grid), pf.Backend.gpus(n))
+            bm = pf.BoundModel(pdf, ds, pf.GridSpec(W.grid), pf.Backend.gpus(n, oversubscribe=oversubscribe))
             for p in bm.registry().parameters():
                 p.value = W.start[p.name]
             r = pf.fit(bm, pf.MetricKind(W.metric))
@@ -77,7 +78,7 @@ def format_report(rows: Sequence[dict]) -> str:
 
 
 def cmd_bench(workload: str, gpu_counts: Sequence[int], repetitions: int, n_events: Optional[int] = None,
-              data_path: Optional[str] = None, out_path: Optional[str] = None) -> int:
+              data_path: Optional[str] = None, out_path: Optional[str] = None, oversubscribe: bool = False) -> int:
     from .parfit import Error
     if repetitions < 3:
         raise Error("bad-arity", "bench needs >= 3 repetitions")
@@ -91,9 +92,9 @@ def cmd_bench(workload: str, gpu_counts: Sequence[int], repetitions: int, n_even
         raise Error("bad-backend", f"GPU counts must be powers of two (got {bad})")
     from .parfit import device_count
     have = device_count()
-    if counts[-1] > have:
+    if counts[-1] > have and not oversubscribe:
         raise Error("bad-backend", f"bench asks for {counts[-1]} GPUs, {have} visible")
-    rows = bench_rows(workload, counts, repetitions, n_events, data_path)
+    rows = bench_rows(workload, counts, repetitions, n_events, data_path, oversubscribe)
     if any(r["metric_value"] != rows[0]["metric_value"] for r in rows):
         raise Error("determinism-violation", "metric value differs across GPU counts: bench aborted")
     report = format_report(rows)
@@ -115,10 +116,14 @@ def main(argv: Optional[Sequence[str]] = None) -> int:
     b.add_argument("--events", type=int, default=None)
     b.add_argument("--data", default=None)
     b.add_argument("--out", default=None)
+    b.add_argument("--oversubscribe", action="store_true",
+                   help="place the shards of a count above the visible devices round-robin on them "
+                        "(exercises the multi-device path and the determinism gate on fewer GPUs; "
+                        "the speedup column then measures nothing)")
     a = ap.parse_args(argv)
     from .parfit import Error
     try:
-        return cmd_bench(a.workload, a.gpus, a.repetitions, a.events, a.data, a.out)
+        return cmd_bench(a.workload, a.gpus, a.repetitions, a.events, a.data, a.out, a.oversubscribe)
     except Error as e:
         sys.stderr.write(f"error: {e}\n")
         return 2

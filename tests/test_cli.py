@@ -74,3 +74,16 @@ def test_bench_rejects_non_power_of_two_counts_up_front():
     with pytest.raises(pf.Error) as ei:
         cli.cmd_bench("C1", [1, 3], 3, n_events=1000)
     assert ei.value.args[0].startswith("bad-backend") and "powers of two" in str(ei.value)
+
+
+@pytest.mark.gpu
+def test_bench_full_command_oversubscribed_counts(tmp_path):
+    """`parfit bench --gpus 1 2 4 --oversubscribe` on however many GPUs there
+    are: the multi-device shards run (round-robin placed), the bitwise
+    determinism gate across counts holds, and the report has one row per count"""
+    out = tmp_path / "bench.txt"
+    assert cli.cmd_bench("C1", [1, 2, 4], 3, n_events=20_000, out_path=str(out), oversubscribe=True) == 0
+    lines = out.read_text().splitlines()
+    assert lines[0] == "backend gpus time_s speedup metric_calls" and len(lines) == 4
+    assert [ln.split()[1] for ln in lines[1:]] == ["1", "2", "4"]
+    assert len({ln.split()[4] for ln in lines[1:]}) == 1  # same fit, same call count, every count
