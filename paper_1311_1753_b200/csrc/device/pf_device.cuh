@@ -405,6 +405,33 @@ __device__ __forceinline__ void pf_fxl_add_w(pf_fxl& A, double x, long long* big
     pf_fxl_add(A, x);
 }
 
+// The same exact add into a lane's six digits kept in SHARED memory
+// (d[i * stride]): the digit position is an address, not a chain of selects
+// over six registers (the fused pass adds one chunk value per lane per chunk;
+// this is about a third of pf_fxl_add's instructions)
+__device__ __forceinline__ void pf_fxs_add(long long* d, int stride, double x) {
+  const pf_u64 bits = (pf_u64)__double_as_longlong(x);
+  const int be = (int)((bits >> 52) & 0x7ff);
+  if (be >= 1023 + 63) {  // non-finite or |x| >= 2^63: poison the sum
+    d[(PF_FX_DIGITS - 1) * stride] += 0x4000000000000000ll;
+    return;
+  }
+  pf_u64 m = (bits & 0xfffffffffffffull) | (be ? 0x10000000000000ull : 0ull);
+  int p = (be ? be : 1) - 1075 + 128;  // LSB position above 2^-128
+  if (p < 0) {
+    m = p <= -53 ? 0ull : (m >> -p);
+    p = 0;
+  }
+  const int q = p >> 5, s = p & 31;
+  const long long sg = (bits >> 63) ? -1ll : 1ll;
+  const long long d0 = (long long)((m << s) & 0xffffffffull);
+  const long long d1 = (long long)((s ? (m >> (32 - s)) : (m >> 32)) & 0xffffffffull);
+  const long long d2 = (long long)(s ? (m >> (64 - s)) : 0ull);
+  d[q * stride] += sg * d0;  // q <= 5 here (|x| < 2^63, LSB >= 2^-128)
+  if (q + 1 < PF_FX_DIGITS) d[(q + 1) * stride] += sg * d1;
+  if (q + 2 < PF_FX_DIGITS) d[(q + 2) * stride] += sg * d2;
+}
+
 // Warp-wide integer sum of the lanes' accumulators into the global one.
 // warp total of the lanes' digits (integer shuffles; exact), valid in lane 0
 __device__ __forceinline__ void pf_fxl_warp_sum(pf_fxl& A) {

@@ -8,7 +8,8 @@ for l in sys.stdin:
     elif 'Error' in l or 'error' in l: print(l)
 "; }
 run default X=1
-run pf1 PFB200_DEFINES=PF_L2_PREFETCH_FIRST=1
-run pf2 PFB200_DEFINES=PF_L2_PREFETCH_FIRST=2
-run pf3 PFB200_DEFINES=PF_L2_PREFETCH_FIRST=3
+run nsub2 PFB200_NSUB=2
+run ept8 PFB200_EPT=8
+run ept8_nst3 PFB200_EPT=8 PFB200_NST=3
+run nst3 PFB200_NST=3
 run default_again X=1
