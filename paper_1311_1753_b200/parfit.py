@@ -1071,7 +1071,7 @@ class BoundModel:
             out, info, st = C.c_double(), _abi.pf_eval_info(), _abi.pf_status()
             self._call = (out, info, st, C.byref(out), C.byref(info), C.byref(st), _eval_fast_bound())
         out, info, st, r_out, r_info, r_st, fn = self._call
-        rc = fn(self._h, p.ctypes.data, p.size, int(metric), r_out, r_info, r_st)
+        rc = fn(self._h, p.__array_interface__["data"][0], p.size, metric, r_out, r_info, r_st)
         self._evaluated()
         if rc:
             _raise(st)
