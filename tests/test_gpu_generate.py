@@ -122,6 +122,24 @@ def test_dalitz_sample_vs_restatement():
     assert np.array_equal(got, want)
 
 
+def test_tddp_sample_vs_restatement():
+    """the time-dependent Dalitz model (3-D box: m12^2, m13^2, t; 4 ToyRng
+    words per candidate) through the same generator: bit for bit the
+    restatement over the C oracle's densities, at exaggerated mixing"""
+    from paper_1311_1753_b200.workloads import WORKLOADS
+    W = WORKLOADS["C5"]
+    obs, pdf = W.build(pf)
+    for v in pf.GraphDesc(pdf, obs).vars:
+        if v.name in ("x", "y"):
+            v.value = 0.15 if v.name == "x" else -0.12
+    # grid 128: the envelope (1.1 x the midpoint-grid maximum, generate.hpp)
+    # must cover the t = 0 edge of e^-t/tau (a coarser grid raises
+    # envelope-failure, as the reference would)
+    got = pf.generate_events(pdf, obs, 2000, 29, pf.GridSpec(128)).columns()
+    want = restated_generate(pf, pdf, obs, 2000, 29, 128)
+    assert np.array_equal(got, want)
+
+
 # ---- the reference's statistical checks (test_generate.cpp), on GPU samples --
 
 def test_uniform_density_gives_uniform_sample():
