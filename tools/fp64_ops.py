@@ -8,7 +8,7 @@ import os
 import sys
 
 tag = sys.argv[1] if len(sys.argv) > 1 else "r2"
-units = {"C2": 10_000_000, "C4": 1_000_000, "C5": 1_000_000}
+units = {"C2": 10_000_000, "C4": 1_000_000, "C5": 1_000_000, "C5TI": 1_000_000}
 out = {}
 for cfg, n in units.items():
     path = os.path.join("gpurun_out", f"{tag}_fp64_{cfg}.csv")
