@@ -359,8 +359,6 @@ Model::Model(const pf_graph& g, const pf_data& d, uint32_t grid_points, const pf
       }
       ck(cudaMemcpy(sh.d_rec, init.data(), sizeof(KRec) * kMaxBatch, cudaMemcpyHostToDevice), "init rec");
     }
-    ck(cudaMalloc(&sh.d_ticket, sizeof(uint32_t)), "cudaMalloc ticket");
-    ck(cudaMemset(sh.d_ticket, 0, sizeof(uint32_t)), "memset ticket");
     ck(cudaMalloc(&sh.d_clamp, sizeof(uint64_t) * 2 * std::max(L_.n_poly, 1)), "cudaMalloc clamp");
     ck(cudaMemset(sh.d_clamp, 0, sizeof(uint64_t) * 2 * std::max(L_.n_poly, 1)), "memset clamp");
     ck(cudaHostAlloc(reinterpret_cast<void**>(&sh.h_out), sizeof(Out) * kMaxBatch, cudaHostAllocMapped),
@@ -416,7 +414,6 @@ Model::~Model() {
     cudaFree(sh.d_peers);
     cudaFree(sh.d_recv);
     cudaFree(sh.d_rec);
-    cudaFree(sh.d_ticket);
     cudaFree(sh.d_clamp);
     cudaFreeHost(sh.h_out);
     cudaFree(sh.h_norms);
@@ -584,7 +581,6 @@ Args Model::base_args(Shard& sh, int K) {
   a.fxbins = sh.d_fxbins;
   a.dpart = sh.d_part;
   a.big = sh.d_big;
-  a.ticket = sh.d_ticket;
   a.peers = sh.d_peers;
   a.gworld = group_world_;
   a.grank = group_rank_;

@@ -157,7 +157,6 @@ struct Shard {
   cudaGraphNode_t first_node = nullptr;
   int event_grid = 1;
   bool fused = false;          // K = 1 graph is the single fused kernel
-  uint32_t* d_ticket = nullptr;  // fused pass: dynamic chunk counter
   void* d_scratch = nullptr;  // L2 flush buffer (bench only)
 };
 
