@@ -365,10 +365,11 @@ extern "C" __global__ void __launch_bounds__(PF_THREADS) pf_norm_kernel(const __
 #pragma unroll
   for (int c = 0; c < 4; ++c) acc[c] = pf_dd_zero();
   if (multi) {
-    // all four components from ONE evaluation of both amplitudes per point
-    for (pf_u64 i = lo + threadIdx.x; i < hi; i += PF_THREADS) {
+    // all four components from ONE evaluation of both amplitudes per point,
+    // in runs of PF_NORM_RUN consecutive points walked row by row
+    for (pf_u64 i = lo + (pf_u64)threadIdx.x * PF_NORM_RUN; i < hi; i += (pf_u64)PF_THREADS * PF_NORM_RUN) {
       double v4[4];
-      pf_norm_point4(T.node, i, T, P, S, a.C, v4);
+      pf_norm_run4(T.node, i, (int)min((pf_u64)PF_NORM_RUN, hi - i), T, P, S, a.C, v4);
 #pragma unroll
       for (int c = 0; c < 4; ++c) acc[c] = pf_dd_add_d(acc[c], v4[c]);
     }

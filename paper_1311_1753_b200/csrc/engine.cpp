@@ -535,7 +535,7 @@ void Model::add_tddp_tasks(int node, uint32_t grid_points, int lvl, int* blocks)
       t.vol = vol;
       t.points = total;
       uint64_t per = static_cast<uint64_t>(std::max(1.0, std::floor(4096.0 / (time ? 8.0 : cost))));
-      if (!time) per = std::max<uint64_t>(per, 256ull * 4ull);
+      if (!time) per = std::max<uint64_t>(per, 256ull * 32ull);  // runs of 32 points per thread (pf_norm_run4)
       uint64_t nb = (total + per - 1) / per;
       if (nb > 4096) {
         nb = 4096;
