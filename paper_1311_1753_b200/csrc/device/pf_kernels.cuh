@@ -1359,10 +1359,9 @@ extern "C" __global__ void __launch_bounds__(PF_FUSED_THREADS, 1) pf_fused_kerne
   const unsigned long long t_setup = pf_gtime();
 #endif
   const pf_fk fk = pf_fk_load(P, S, a.C);
-  // the lane's exact digits in shared memory: fx[i * PF_FUSED_THREADS + tid]
-  long long* fx = reinterpret_cast<long long*>(S + ((PF_SS + 1) & ~1));
+  pf_fxl F;
 #pragma unroll
-  for (int i = 0; i < PF_FX_DIGITS; ++i) fx[i * PF_FUSED_THREADS + threadIdx.x] = 0;
+  for (int i = 0; i < PF_FX_DIGITS; ++i) F.d[i] = 0;
   long long* big = a.big;
   pf_lacc acc;
   int w = 0;  // sub-chunks consumed by this warp
@@ -1386,17 +1385,9 @@ extern "C" __global__ void __launch_bounds__(PF_FUSED_THREADS, 1) pf_fused_kerne
     }
     // chunk done: its exact value into the lane's fixed-point accumulator
     const pf_dd tv = pf_lacc_terms(acc, P);
-    if (fabs(tv.hi) >= 0x1p62 && fabs(tv.hi) <= 1.7976931348623157e308) {  // rare: the wide accumulator
-      pf_big_add(big, tv.hi);
-      pf_fxs_add(fx + threadIdx.x, PF_FUSED_THREADS, tv.lo);
-    } else {
-      pf_fxs_add(fx + threadIdx.x, PF_FUSED_THREADS, tv.hi);
-      pf_fxs_add(fx + threadIdx.x, PF_FUSED_THREADS, tv.lo);
-    }
+    pf_fxl_add_w(F, tv.hi, big);
+    pf_fxl_add_w(F, tv.lo, big);
   }
-  pf_fxl F;
-#pragma unroll
-  for (int i = 0; i < PF_FX_DIGITS; ++i) F.d[i] = fx[i * PF_FUSED_THREADS + threadIdx.x];
 #ifdef PF_EVENT_TRACE
   const unsigned long long t_loop = pf_gtime();
   if (lane == 0 && gw < 4096) {  // per warp: chunks taken, loop end

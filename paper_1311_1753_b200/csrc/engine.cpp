@@ -72,11 +72,9 @@ size_t event_smem(const Layout& L, int K) {
 
 // fused kernel: every warp's TMA ring, then P and S of the one parameter set
 size_t fused_smem(const Layout& L) {
-  // + every thread's six exact digits (pf_fxs_add), 16-byte aligned after S
   return static_cast<size_t>(kFusedWarps) * L.nst * L.load_cols.size() * 32 * static_cast<size_t>(L.ept) *
              sizeof(double) +
-         sizeof(double) * std::max(L.np, 1) + sizeof(double) * ((std::max(L.ss, 1) + 1) & ~1) +
-         static_cast<size_t>(kFusedWarps) * 32 * 6 * sizeof(int64_t) + 16;
+         sizeof(double) * (std::max(L.np, 1) + std::max(L.ss, 1));
 }
 
 size_t event_smem_max(const Layout& L) {
