@@ -583,3 +583,15 @@ def test_c5_tddp_vs_oracle(mix):
     r = list(p)
     r[names.index("tau")] = -0.1
     assert bm.eval_metric(r) == o.eval(r) == pf.kPenaltyValue
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3"])
+def test_small_grid_workloads_take_the_single_kernel_path(name):
+    """C1-C3 (one parameter set, small normalisation grids) run as ONE fused
+    kernel per call; a layout change that no longer fits it would silently
+    fall back to the slower two-kernel graph"""
+    W = WORKLOADS[name]
+    obs, pdf = W.build(pf)
+    bm = pf.BoundModel(pdf, W.data(pf, obs, 50_000, seed=2), pf.GridSpec(W.grid))
+    bm.eval_metric(W.params(bm))
+    assert pf.lib.pf_model_fused(bm._h) == 1
