@@ -182,6 +182,22 @@ __device__ __forceinline__ void pf_setup_core(const pf_args& a, int k, unsigned 
     // for the cluster, single-CTA (fused) and multi-block paths.
     // one loop per task (constant q: no per-point task search); the loops'
     // few iterations are independent evaluations
+#ifdef PF_SETUP_QLOOP
+    // one copy of the task loop's code (the setup runs once per call from a
+    // cold instruction cache: its code size is its cost)
+#pragma unroll 1
+    for (int q = 0; q < PF_SETUP_MAXQ; ++q) {
+      double xq = 0.0;
+      if (q < nl) {
+        PF_CHECK(t0 + q < nt && t0 + q < 16);
+        const pf_task& T = tk[t0 + q];
+        xq = pf_norm_accum(T.node, rank * PF_SETUP_THREADS + threadIdx.x, T.points, PF_SETUP_THREADS * CL, T, P, S,
+                           a.C, cx, cnt);
+      }
+      red[q][threadIdx.x] = xq;
+    }
+    PF_TRACE("points");
+#else
     double x[PF_SETUP_MAXQ];
 #pragma unroll
     for (int q = 0; q < PF_SETUP_MAXQ; ++q) {
@@ -189,19 +205,20 @@ __device__ __forceinline__ void pf_setup_core(const pf_args& a, int k, unsigned 
       if (q < nl) {
         PF_CHECK(t0 + q < nt && t0 + q < 16);
         const pf_task& T = tk[t0 + q];
-        const pf_u64 np = T.points;
-#pragma unroll 4
-        for (pf_u64 g = rank * PF_SETUP_THREADS + threadIdx.x; g < np; g += PF_SETUP_THREADS * CL)
-          x[q] += pf_norm_point(T.node, g, T, P, S, a.C, cx, cnt);
+        x[q] = pf_norm_accum(T.node, rank * PF_SETUP_THREADS + threadIdx.x, T.points, PF_SETUP_THREADS * CL, T, P, S,
+                             a.C, cx, cnt);
       }
     }
     PF_TRACE("points");
+#endif
     // the threads' partials through shared memory; then warp w sums run
     // (w % 4) of task (w / 4) -- 128 partials -- in double-double and 4 runs
     // per task are added in double-double: every task's sum is good to
     // ~1e-17 relative for a fraction of the cost of per-warp trees of all tasks
+#ifndef PF_SETUP_QLOOP
 #pragma unroll
     for (int q = 0; q < PF_SETUP_MAXQ; ++q) red[q][threadIdx.x] = x[q];
+#endif
     __syncthreads();
     static_assert(PF_SETUP_THREADS == 512, "16 warps: 4 runs of 128 partials for each of 4 tasks per pass");
     for (int q0 = 0; q0 < nl; q0 += 4) {
@@ -678,6 +695,10 @@ __device__ __forceinline__ pf_fk pf_fk_get(const pf_args& a, int k) {
 }
 
 #ifdef PF_QFAST
+#ifndef PF_QUNROLL
+#define PF_QUNROLL (PF_EPT / 2)
+#endif
+constexpr int pf_qunroll = PF_QUNROLL;
 // Mixture fast path: AddPdf of two Exp/Gauss children of one observable, the
 // per-call proof K.qfast holding (codegen.cpp: every event's terms in range,
 // no floor, |d| <= 700, d's quadratic terms <= 256).  Centred at m (a
@@ -697,7 +718,7 @@ __device__ __forceinline__ pf_lacc pf_qfast_terms(const double* st, int lane, in
   const double ba = K.q[4], bb = K.q[5], bc = K.q[6];
   double s1 = 0.0, s2 = 0.0, p0 = 1.0, p1 = 1.0;
   const double2* s2v = reinterpret_cast<const double2*>(st);
-#pragma unroll
+#pragma unroll pf_qunroll
   for (int j = 0; j < PF_EPT / 2; ++j) {
     const int i = 32 * j + lane;  // this lane's events 2i and 2i + 1 of the stage
     const double2 xv = s2v[i];
@@ -705,6 +726,10 @@ __device__ __forceinline__ pf_lacc pf_qfast_terms(const double* st, int lane, in
     for (int h = 0; h < 2; ++h) {
       const bool valid = FULL || 2 * i + h < n_valid;
       const double t = (h ? xv.y : xv.x) - zm;
+#ifdef PF_QTRIVIAL
+      s1 += t;  // experiment: the stream without the per-event math
+      continue;
+#endif
       const double d = fma(fma(qA, t, qB), t, qC);
 #ifdef PF_QFAST_LINEAR_BASE
       const double ub = fma(bb, t, bc);
@@ -714,12 +739,23 @@ __device__ __forceinline__ pf_lacc pf_qfast_terms(const double* st, int lane, in
 #endif
       const double ad = fabs(d);
       s1 += valid ? ub : 0.0;
+#ifdef PF_QMAX_INT
+      // max(d, 0) by masking d's bits with its sign (integer pipe): the sum of
+      // max(d, 0) is exactly half the sum of d + |d| term by term
+      const int dh = __double2hiint(d), dm = ~(dh >> 31);
+      s2 += valid ? __hiloint2double(dh & dm, __double2loint(d) & dm) : 0.0;
+#else
       s2 += valid ? d + ad : 0.0;
+#endif
       const double kd = fma(-ad, PF_Q_INVLN2N, 0x1.8p52);
       const int ki = __double2loint(kd);
       const double k = kd - 0x1.8p52;
       const double r = fma(k, -PF_Q_LN2N, -ad);
+#ifdef PF_QNOTABLE
+      const double T = __hiloint2double(0x3ff00000 | (ki & 1023), 0);  // experiment: no shared-memory gather
+#else
       const double T = pf_exp2_1024[ki & 1023];
+#endif
       double pp = fma(r, 1.0 / 24.0, 1.0 / 6.0);
       pp = fma(pp, r, 0.5);
       pp = fma(pp, r, 1.0);
@@ -733,7 +769,11 @@ __device__ __forceinline__ pf_lacc pf_qfast_terms(const double* st, int lane, in
     }
   }
   pf_lacc out;
+#ifdef PF_QMAX_INT
+  out.v[0] = s1 + s2;
+#else
   out.v[0] = fma(0.5, s2, s1);
+#endif
   out.v[1] = p0 * p1;
   return out;
 }
@@ -1336,6 +1376,11 @@ extern "C" __global__ void __launch_bounds__(PF_FUSED_THREADS, 1) pf_fused_kerne
   };
   pf_setup_core<PF_SETUP_CLUSTER>(a, 0, rank, P, S, r, false, cx, cnt_grid, cnt_stage, hook, &tbar);
 #else
+#ifdef PF_SETUP_TWICE
+  // experiment: the setup once more with warm instruction caches (traced twice)
+  pf_setup_core<PF_SETUP_CLUSTER>(a, 0, rank, P, S, r, false, cx, cnt_grid, cnt_stage, pf_no_hook(), &tbar);
+  __syncthreads();
+#endif
   pf_setup_core<PF_SETUP_CLUSTER>(a, 0, rank, P, S, r, false, cx, cnt_grid, cnt_stage, pf_no_hook(), &tbar);
 #endif
   // no CTA may leave while a cluster peer could still read its setup
@@ -1372,7 +1417,13 @@ extern "C" __global__ void __launch_bounds__(PF_FUSED_THREADS, 1) pf_fused_kerne
     const int c = gw + jc * nwa;
     for (int j = 0; j < PF_NSUB; ++j, ++w) {
       const int st = w % PF_NST;
+#ifdef PF_QNOWAIT
+      // experiment: the math alone -- stage 0 once, then re-read (no TMA waits)
+      if (w == 0)
+        for (int s0 = 0; s0 < PF_NST && s0 < n_mine * PF_NSUB; ++s0) pf_mbar_wait(mybar + s0, 0u);
+#else
       pf_mbar_wait(mybar + st, (unsigned)((w / PF_NST) & 1));
+#endif
       const pf_u64 base = (pf_u64)c * (PF_SUB * PF_NSUB) + (pf_u64)j * PF_SUB;
       PF_CHECK(c < nch && base < a.col_stride && st < PF_NST);
       const bool full = base + PF_SUB <= a.n_local;
@@ -1381,7 +1432,9 @@ extern "C" __global__ void __launch_bounds__(PF_FUSED_THREADS, 1) pf_fused_kerne
                              : pf_stage_terms<false>(a, 0, base, lane, my + st * PF_STAGE, n_valid, fk, P, S);
       acc = j == 0 ? t : pf_lacc_merge(acc, t);
       __syncwarp();
+#ifndef PF_QNOWAIT
       issue(w + PF_NST);  // refills the stage just read
+#endif
     }
     // chunk done: its exact value into the lane's fixed-point accumulator
     const pf_dd tv = pf_lacc_terms(acc, P);

@@ -1,4 +1,4 @@
-# C2 fused-kernel variants (device step time, L2 flushed), one line each
+# C2 QFAST loop variants: unroll depth (instruction-fetch stalls) and max(d,0) on the integer pipe
 run() { echo "== $1"; shift; env "$@" python bench.py --config C2 --steps 30 --warmup 5 --no-fit --no-cpu-baseline 2>&1 | python -c "
 import json,sys
 for l in sys.stdin:
@@ -8,8 +8,10 @@ for l in sys.stdin:
     elif 'Error' in l or 'error' in l: print(l)
 "; }
 run default X=1
-run nsub3 PFB200_NSUB=3
-run ept12 PFB200_EPT=12
-run ept20 PFB200_EPT=20
-run nsub5 PFB200_NSUB=5
+run u1 PFB200_DEFINES="PF_QUNROLL=1"
+run u2 PFB200_DEFINES="PF_QUNROLL=2"
+run u4 PFB200_DEFINES="PF_QUNROLL=4"
+run maxint PFB200_DEFINES="PF_QMAX_INT"
+run u2_maxint PFB200_DEFINES="PF_QUNROLL=2;PF_QMAX_INT"
+run u4_maxint PFB200_DEFINES="PF_QUNROLL=4;PF_QMAX_INT"
 run default_again X=1
