@@ -22,6 +22,8 @@ struct ConvTable {
   int after;      // stage after which it can be filled (-1 = pre)
 };
 
+constexpr int kConvKB = 128;  // products per chain per block of the warp-shared window sum
+
 struct Layout {
   int n_nodes = 0;
   int np = 0;                 // parameters
@@ -45,6 +47,9 @@ struct Layout {
   // convolutions with a Gaussian resolution: their normalisation grid is
   // evaluated per grid point (window + term recurrence), not per (point, tau) pair
   std::vector<int> conv_windowed;
+  // the root is such a convolution: the event pass gives each warp a
+  // shared-memory scratch of 2 x kConvKB products (PF_CONV_SHARED)
+  bool conv_shared = false;
   std::vector<std::vector<int>> level_nodes;  // normalised nodes per level
   std::string source;         // generated CUDA source (without library headers)
   std::string structure_key;  // cache key of the compiled module

@@ -155,8 +155,16 @@ struct pf_args {
 
 // ----------------------------------------------------------------------------
 // error/counter context carried through one evaluation
+#ifdef PF_CONV_TRACE_FULL
+__device__ unsigned pf_conv_full_count[2];  // experiment: full-Q fallbacks, windows not summed
+#endif
+
 struct pf_ctx {
   pf_u32 err;  // (node << 8) | code of the first error, 0 when none
+  // the event pass's warp scratch (PF_CONV_SHARED) and the mask of the lanes
+  // evaluating an event together; null elsewhere: per-lane sums
+  double* scr = nullptr;
+  pf_u32 mask = 0u;
 };
 
 // An index as a double, exactly, without the I2F conversion pipe: below 2^32

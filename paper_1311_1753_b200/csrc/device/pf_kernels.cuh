@@ -357,11 +357,34 @@ extern "C" __global__ void __launch_bounds__(PF_THREADS) pf_norm_kernel(const __
   __shared__ pf_dd sm[PF_THREADS];
   __shared__ int s_last;
   __shared__ double sums[64][4];
+#ifdef PF_NORM_POINT_TRACE
+  const unsigned long long g_in = pf_gtime();
+#endif
   if (a.level == a.n_levels - 1) pf_pdl_trigger();
-  pf_math_init();
   const int k = blockIdx.y;
   const double* P = a.P + (pf_u64)k * PF_NP;
   double* S = a.S + (pf_u64)k * PF_SS;
+#if defined(PF_S_SMEM) && PF_SS * 8 <= 96 * 1024 && PF_SS % 2 == 0 && !defined(PF_QFAST)
+#define PF_NORM_S_STAGED 1
+  // convolution tables read per (point, tau): the points read a shared-memory
+  // copy of the per-call state (LDS, not global loads on the recurrence's
+  // critical path), brought in with the exp table by two TMA bulk copies (a
+  // thread loop took 3.5 us); the last block below still finishes into global S
+  extern __shared__ __align__(16) double pf_norm_S[];
+  __shared__ __align__(8) pf_u64 nbar;
+  if (threadIdx.x == 0) {
+    pf_mbar_init(&nbar, 1);
+    pf_fence_mbar_init();
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    pf_mbar_expect_tx(&nbar, (unsigned)(PF_SS * 8 + 2048));
+    pf_tma_load(pf_norm_S, S, (unsigned)(PF_SS * 8), &nbar);
+    pf_tma_load(pf_exp_tab, pf_exp_tab_g, 2048u, &nbar);
+  }
+  __syncthreads();
+  pf_mbar_wait(&nbar, 0u);
+#else
+  pf_math_init();
+#endif
   // per block and value one partial: task t owns blocks [first_block,
   // first_block + n_blocks); value c (a TddpPdf's four Dalitz components,
   // comp 8) at part[c * gridDim.x + block]
@@ -381,22 +404,39 @@ extern "C" __global__ void __launch_bounds__(PF_THREADS) pf_norm_kernel(const __
   pf_dd acc[4];
 #pragma unroll
   for (int c = 0; c < 4; ++c) acc[c] = pf_dd_zero();
+#ifdef PF_NORM_S_STAGED
+  const double* Sp = pf_norm_S;
+#else
+  const double* Sp = S;
+#endif
   if (multi) {
     // all four components from ONE evaluation of both amplitudes per point,
     // in runs of PF_NORM_RUN consecutive points walked row by row
     for (pf_u64 i = lo + (pf_u64)threadIdx.x * PF_NORM_RUN; i < hi; i += (pf_u64)PF_THREADS * PF_NORM_RUN) {
       double v4[4];
-      pf_norm_run4(T.node, i, (int)min((pf_u64)PF_NORM_RUN, hi - i), T, P, S, a.C, v4);
+      pf_norm_run4(T.node, i, (int)min((pf_u64)PF_NORM_RUN, hi - i), T, P, Sp, a.C, v4);
 #pragma unroll
       for (int c = 0; c < 4; ++c) acc[c] = pf_dd_add_d(acc[c], v4[c]);
     }
   } else if (T.dims >= 2 && T.per_block >= (pf_u64)PF_THREADS * PF_NORM_RUN) {
     // runs of PF_NORM_RUN consecutive points per thread, walked row by row
     for (pf_u64 i = lo + (pf_u64)threadIdx.x * PF_NORM_RUN; i < hi; i += (pf_u64)PF_THREADS * PF_NORM_RUN)
-      acc[0] = pf_dd_add_d(acc[0], pf_norm_run(T.node, i, (int)min((pf_u64)PF_NORM_RUN, hi - i), T, P, S, a.C, cx, cnt));
+      acc[0] = pf_dd_add_d(acc[0], pf_norm_run(T.node, i, (int)min((pf_u64)PF_NORM_RUN, hi - i), T, P, Sp, a.C, cx, cnt));
   } else {
+#ifdef PF_NORM_POINT_TRACE
+    const long long c0 = clock64();
+    const unsigned long long g_pts = pf_gtime();
+#endif
     for (pf_u64 i = lo + threadIdx.x; i < hi; i += PF_THREADS)
-      acc[0] = pf_dd_add_d(acc[0], pf_norm_point(T.node, i, T, P, S, a.C, cx, cnt));
+      acc[0] = pf_dd_add_d(acc[0], pf_norm_point(T.node, i, T, P, Sp, a.C, cx, cnt));
+#ifdef PF_NORM_POINT_TRACE
+    (void)c0;
+    if (threadIdx.x == 0 && blockIdx.x < 2000) {
+      pf_trace_buf[(2000 + blockIdx.x) * 6 + 0] = g_in;
+      pf_trace_buf[(2000 + blockIdx.x) * 6 + 1] = g_pts;
+      pf_trace_buf[(2000 + blockIdx.x) * 6 + 2] = pf_gtime();
+    }
+#endif
   }
   for (int c = 0; c < (multi ? 4 : 1); ++c) {
     pf_dd s = pf_block_reduce(acc[c], sm);
@@ -411,8 +451,18 @@ extern "C" __global__ void __launch_bounds__(PF_THREADS) pf_norm_kernel(const __
     s_last = (prev == gridDim.x - 1);
   }
   __syncthreads();
+#ifdef PF_NORM_POINT_TRACE
+  if (threadIdx.x == 0 && blockIdx.x < 2000) pf_trace_buf[(2000 + blockIdx.x) * 6 + 3] = pf_gtime();
+#endif
   if (!s_last) return;
   __threadfence();
+#ifdef PF_CONV_TRACE_FULL
+  if (threadIdx.x == 0) {
+    printf("norm level %d: full-Q fallbacks %u, windows not summed %u\n", a.level, pf_conv_full_count[0],
+           pf_conv_full_count[1]);
+    pf_conv_full_count[0] = pf_conv_full_count[1] = 0u;
+  }
+#endif
   for (int tt = 0; tt < a.n_tasks; ++tt) {
     const pf_task& U = a.tasks[tt];
     const int nv = U.comp == PF_COMP_ALL4 ? 4 : 1;
@@ -440,6 +490,9 @@ extern "C" __global__ void __launch_bounds__(PF_THREADS) pf_norm_kernel(const __
   pf_stage_post(a.level, k, P, S, a.C, cx2, cnt2, threadIdx.x, blockDim.x);
   if (cx2.err) atomicMin(&a.rec[k].norm_error, cx2.err);
   if (pf_grid_counts(a, k)) pf_cnt_flush(cnt2, a.clamp);
+#ifdef PF_NORM_POINT_TRACE
+  if (threadIdx.x == 0 && blockIdx.x < 2000) pf_trace_buf[(2000 + blockIdx.x) * 6 + 4] = pf_gtime();
+#endif
 }
 
 // ---------------------------------------------------------------------------
@@ -782,7 +835,7 @@ __device__ __forceinline__ pf_lacc pf_qfast_terms(const double* st, int lane, in
 template <bool FULL>
 __device__ __forceinline__ pf_lacc pf_stage_terms(const pf_args& a, int k, pf_u64 base, int lane,
                                                 const double* st, int n_valid, const pf_fk& K,
-                                                const double* P, const double* S) {
+                                                const double* P, const double* S, double* scr = nullptr) {
 #if !PF_BINNED && PF_LOGFORM
   pf_lform A;
   pf_lform_init(A);
@@ -841,6 +894,7 @@ __device__ __forceinline__ pf_lacc pf_stage_terms(const pf_args& a, int k, pf_u6
 #else
   pf_ctx cx;
   cx.err = 0;
+  cx.scr = scr;
   pf_cnt cnt;
   pf_cnt_init(cnt);
   pf_u32 floors = 0;
@@ -854,6 +908,10 @@ __device__ __forceinline__ pf_lacc pf_stage_terms(const pf_args& a, int k, pf_u6
 #pragma unroll pf_unroll
   for (int j = 0; j < PF_EPT; ++j) {
     const int i = 32 * j + lane;
+#ifdef PF_CONV_SHARED
+    // the lanes that evaluate event j of the stage together (whole warp here)
+    cx.mask = __ballot_sync(0xffffffffu, FULL || i < n_valid);
+#endif
     // padding events (the column tail up to a whole chunk) are not evaluated:
     // they would count clamps the reference never sees
     if (!FULL && i >= n_valid) continue;
@@ -1146,6 +1204,12 @@ extern "C" __global__ void __launch_bounds__(PF_EV_THREADS, PF_EVENT_MIN_BLOCKS)
     for (int i = threadIdx.x; i < a.K * PF_SS; i += PF_EV_THREADS) sS[i] = a.S[i];
     __syncthreads();
   }
+#ifdef PF_CONV_SHARED
+  // this warp's scratch for the shared window products (engine.cpp event_smem)
+  double* scr = sS + (a.s_smem ? a.K * PF_SS : 0) + warp * 2 * PF_CONV_KB;
+#else
+  double* scr = nullptr;
+#endif
   for (int w = 0; w < W; ++w) {
     const int s = w % PF_NST;
     pf_mbar_wait(mybar + s, (unsigned)((w / PF_NST) & 1));
@@ -1163,14 +1227,14 @@ extern "C" __global__ void __launch_bounds__(PF_EV_THREADS, PF_EVENT_MIN_BLOCKS)
       // pointer's address space is known), not generic loads
       if (a.s_smem) {
         const double* Sk = sS + (pf_u64)k * PF_SS;
-        t = full ? pf_stage_terms<true>(a, k, base, lane, my + s * PF_STAGE, n_valid, fk, Pk, Sk)
-                 : pf_stage_terms<false>(a, k, base, lane, my + s * PF_STAGE, n_valid, fk, Pk, Sk);
+        t = full ? pf_stage_terms<true>(a, k, base, lane, my + s * PF_STAGE, n_valid, fk, Pk, Sk, scr)
+                 : pf_stage_terms<false>(a, k, base, lane, my + s * PF_STAGE, n_valid, fk, Pk, Sk, scr);
       } else
 #endif
       {
         const double* Sk = a.S + (pf_u64)k * PF_SS;
-        t = full ? pf_stage_terms<true>(a, k, base, lane, my + s * PF_STAGE, n_valid, fk, Pk, Sk)
-                 : pf_stage_terms<false>(a, k, base, lane, my + s * PF_STAGE, n_valid, fk, Pk, Sk);
+        t = full ? pf_stage_terms<true>(a, k, base, lane, my + s * PF_STAGE, n_valid, fk, Pk, Sk, scr)
+                 : pf_stage_terms<false>(a, k, base, lane, my + s * PF_STAGE, n_valid, fk, Pk, Sk, scr);
       }
       double* slot = accs + k * PF_LACC_N * PF_EV_THREADS + threadIdx.x;
       if (!first) {

@@ -57,6 +57,8 @@ ModuleCache& cache() {
 // pair: the event pass copies it into shared memory when it fits
 // (PF_S_SMEM; the kernel's pointer then resolves to LDS, not L1).
 bool event_s_staged(const Layout& L, int K) {
+  if (const char* env = std::getenv("PFB200_EVENT_S_SMEM"))  // A/B hook
+    if (std::atoi(env) == 0) return false;
   return !L.conv_tables.empty() && static_cast<size_t>(K) * L.ss * sizeof(double) <= 96 * 1024;
 }
 
@@ -67,6 +69,8 @@ size_t event_smem(const Layout& L, int K) {
   // doubles) and an exact fixed-point accumulator (6 x 8 B)
   size_t bytes = stages + static_cast<size_t>(K) * 32 * kEventWarps * (8 * L.lacc_n + 48);
   if (event_s_staged(L, K)) bytes += static_cast<size_t>(K) * L.ss * sizeof(double);
+  // per warp: the scratch of the warp-shared convolution window products
+  if (L.conv_shared) bytes += static_cast<size_t>(kEventWarps) * 2 * kConvKB * sizeof(double);
   return bytes;
 }
 
@@ -75,6 +79,13 @@ size_t fused_smem(const Layout& L) {
   return static_cast<size_t>(kFusedWarps) * L.nst * L.load_cols.size() * 32 * static_cast<size_t>(L.ept) *
              sizeof(double) +
          sizeof(double) * (std::max(L.np, 1) + std::max(L.ss, 1));
+}
+
+// the normalisation kernel's copy of the per-call state (convolution models,
+// pf_norm_kernel under PF_S_SMEM)
+size_t norm_smem(const Layout& L) {
+  const size_t b = static_cast<size_t>(L.ss) * sizeof(double);
+  return !L.conv_tables.empty() && b <= 96 * 1024 && L.ss % 2 == 0 ? b : 0;
 }
 
 size_t event_smem_max(const Layout& L) {
@@ -118,6 +129,10 @@ const Module* load_module(const Layout& L, int device) {
   ck(cudaKernelSetAttributeForDevice(m->event, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(event_smem_max(L)), device),
      "event kernel smem attribute");
+  if (norm_smem(L) > 0)
+    ck(cudaKernelSetAttributeForDevice(m->norm, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(norm_smem(L)), device),
+       "norm kernel smem attribute");
   {
     cudaFuncAttributes fa{};
     if (cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(m->fused)) == cudaSuccess)
@@ -471,8 +486,14 @@ void Model::build_tasks(uint32_t grid_points) {
         // (PF_NORM_RUN, walked row by row) for all 256 threads of a block
         uint64_t per = static_cast<uint64_t>(std::max(1.0, std::floor(4096.0 / cost)));
         if (dims >= 2 && !pairs) per = std::max<uint64_t>(per, 256ull * 32ull);
-        // a windowed convolution point is one thread's loop: a point per thread
-        if (conv_windowed(node)) per = std::max<uint64_t>(per, 256ull);
+        // a windowed convolution point is one thread's loop (a few hundred
+        // dependent steps): one warp's worth of points per block spreads the
+        // grid over many SMs (C4: 12 blocks of 256 points took 25 us)
+        if (conv_windowed(node)) {
+          per = kConvNormPointsPerBlock;
+          if (const char* env = std::getenv("PFB200_CONV_NORM_PER"))  // A/B hook
+            per = std::max<uint64_t>(1, std::strtoull(env, nullptr, 10));
+        }
         uint64_t nb = (total + per - 1) / per;
         if (nb > 4096) {
           nb = 4096;
@@ -640,7 +661,7 @@ cudaGraphExec_t Model::graph_for(Shard& sh, int K) {
       b.level = static_cast<int>(lvl);
       b.n_tasks = level_n_tasks_[lvl];
       b.tasks = sh.d_tasks + level_first_task_[lvl];
-      launch(sh.mod->norm, dim3(level_blocks_[lvl], K), dim3(256), 0, sh.stream, b);
+      launch(sh.mod->norm, dim3(level_blocks_[lvl], K), dim3(256), norm_smem(L_), sh.stream, b);
       ++kernels;
     }
   }

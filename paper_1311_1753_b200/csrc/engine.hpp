@@ -19,6 +19,7 @@ namespace pfb {
 constexpr double kPenaltyValue = 1e300;  // engine.hpp:52
 constexpr int kMaxBatch = 16;            // parameter sets per launch
 constexpr int kEventWarps = 2;           // warps per event-pass block (PF_EV_WARPS)
+constexpr uint64_t kConvNormPointsPerBlock = 32;  // windowed convolution grid points per norm block
 constexpr int kEventBlocksPerSM = 8;     // resident event blocks per SM (PF_EVENT_MIN_BLOCKS)
 constexpr int kCompAll4 = 8;               // Task.comp: a TddpPdf Dalitz task yielding its 4 components (PF_COMP_ALL4)
 constexpr int kMaxGroup = 16;              // PF_GROUP_MAX: ranks of a peer-memory exchange group

@@ -12,7 +12,7 @@ W = WORKLOADS[sys.argv[1] if len(sys.argv) > 1 else "C2"]
 obs, pdf = W.build(pf)
 g = pf.GraphDesc(pdf, obs)
 o = (C.c_int32 * len(obs))(*[g.var_index(x) for x in obs])
-binned = 1 if getattr(W, "binned", False) else 0
+binned = 1 if (getattr(W, "binned", False) or W.metric == 1) else 0
 data = _abi.pf_data(binned, len(obs), o, 0, None, 0.0)
 st, n = _abi.pf_status(), C.c_size_t()
 buf = C.create_string_buffer(1 << 22)
