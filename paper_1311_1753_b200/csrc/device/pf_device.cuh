@@ -707,6 +707,39 @@ __device__ __forceinline__ pf_cplx pf_dalitz_res_fast(double s, double quarter, 
   return r;
 }
 
+// sin/cos and sinh/cosh of |u| <= 1/8 by Taylor polynomials in u^2 (terms
+// to u^11 and u^12: the first omitted term is below 1e-19 relative), the
+// TddpPdf mixing factors when x t / tau and y t / tau are small
+__device__ __forceinline__ void pf_trig_small(double u, double& s, double& c) {
+  const double u2 = u * u;
+  double ps = fma(u2, -1.0 / 39916800.0, 1.0 / 362880.0);
+  ps = fma(ps, u2, -1.0 / 5040.0);
+  ps = fma(ps, u2, 1.0 / 120.0);
+  ps = fma(ps, u2, -1.0 / 6.0);
+  s = fma(u * u2, ps, u);
+  double pc = fma(u2, 1.0 / 479001600.0, -1.0 / 3628800.0);
+  pc = fma(pc, u2, 1.0 / 40320.0);
+  pc = fma(pc, u2, -1.0 / 720.0);
+  pc = fma(pc, u2, 1.0 / 24.0);
+  pc = fma(pc, u2, -0.5);
+  c = fma(u2, pc, 1.0);
+}
+
+__device__ __forceinline__ void pf_hyp_small(double u, double& s, double& c) {
+  const double u2 = u * u;
+  double ps = fma(u2, 1.0 / 39916800.0, 1.0 / 362880.0);
+  ps = fma(ps, u2, 1.0 / 5040.0);
+  ps = fma(ps, u2, 1.0 / 120.0);
+  ps = fma(ps, u2, 1.0 / 6.0);
+  s = fma(u * u2, ps, u);
+  double pc = fma(u2, 1.0 / 479001600.0, 1.0 / 3628800.0);
+  pc = fma(pc, u2, 1.0 / 40320.0);
+  pc = fma(pc, u2, 1.0 / 720.0);
+  pc = fma(pc, u2, 1.0 / 24.0);
+  pc = fma(pc, u2, 0.5);
+  c = fma(u2, pc, 1.0);
+}
+
 // inside the kinematic boundary of the (m12^2, m13^2) plane
 __device__ __forceinline__ bool pf_dalitz_inside(double s12, double s13, double M, double m1, double m2,
                                                  double m3) {
