@@ -331,19 +331,49 @@ extern "C" __global__ void __launch_bounds__(PF_SETUP_THREADS) pf_setup_kernel(c
 
 // ---------------------------------------------------------------------------
 // pre (large grids): parameters, call records and the pre stage.
+#if defined(PF_S_SMEM) && PF_SS * 8 <= 96 * 1024 && PF_SS % 2 == 0 && !defined(PF_QFAST)
+#define PF_S_STAGE_TMA 1  // pre and norm kernels work on a shared-memory copy of S (engine.cpp norm_smem)
+#endif
+
 extern "C" __global__ void __launch_bounds__(PF_THREADS) pf_pre_kernel(const __grid_constant__ pf_args a) {
-  pf_math_init();
   const int k = blockIdx.x;
   pf_krec* r = a.rec + k;
+#ifdef PF_S_STAGE_TMA
+  // convolution tables: the pre stage fills them in a shared-memory copy of
+  // the per-call state (its reads, table writes and max/min atomics on LDS /
+  // STS / shared atomics instead of global round trips), written back whole
+  extern __shared__ __align__(16) double pf_pre_S[];
+  __shared__ __align__(8) pf_u64 pbar;
+  double* gS = a.S + (pf_u64)k * PF_SS;
+  if (threadIdx.x == 0) {
+    pf_mbar_init(&pbar, 1);
+    pf_fence_mbar_init();
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    pf_mbar_expect_tx(&pbar, (unsigned)(PF_SS * 8 + 2048));
+    pf_tma_load(pf_pre_S, gS, (unsigned)(PF_SS * 8), &pbar);
+    pf_tma_load(pf_exp_tab, pf_exp_tab_g, 2048u, &pbar);
+  }
   pf_load_params(a, k);
   if (threadIdx.x == 0) pf_rec_init(r);
   __syncthreads();
+  pf_mbar_wait(&pbar, 0u);
+  double* S = pf_pre_S;
+#else
+  pf_math_init();
+  pf_load_params(a, k);
+  if (threadIdx.x == 0) pf_rec_init(r);
+  __syncthreads();
+  double* S = a.S + (pf_u64)k * PF_SS;
+#endif
   pf_ctx cx;
   cx.err = 0;
   pf_cnt cnt;
   pf_cnt_init(cnt);
-  pf_stage_pre(k, a.P + (pf_u64)k * PF_NP, a.S + (pf_u64)k * PF_SS, a.C, cx, cnt, threadIdx.x,
-               blockDim.x);
+  pf_stage_pre(k, a.P + (pf_u64)k * PF_NP, S, a.C, cx, cnt, threadIdx.x, blockDim.x);
+#ifdef PF_S_STAGE_TMA
+  __syncthreads();  // (pf_stage_pre ends with one too)
+  for (int i = threadIdx.x; i < PF_SS; i += PF_THREADS) gS[i] = S[i];
+#endif
   if (cx.err) atomicMin(&r->norm_error, cx.err);
   if (pf_grid_counts(a, k)) pf_cnt_flush(cnt, a.clamp);
 }
@@ -364,7 +394,7 @@ extern "C" __global__ void __launch_bounds__(PF_THREADS) pf_norm_kernel(const __
   const int k = blockIdx.y;
   const double* P = a.P + (pf_u64)k * PF_NP;
   double* S = a.S + (pf_u64)k * PF_SS;
-#if defined(PF_S_SMEM) && PF_SS * 8 <= 96 * 1024 && PF_SS % 2 == 0 && !defined(PF_QFAST)
+#ifdef PF_S_STAGE_TMA
 #define PF_NORM_S_STAGED 1
   // convolution tables read per (point, tau): the points read a shared-memory
   // copy of the per-call state (LDS, not global loads on the recurrence's
@@ -463,14 +493,14 @@ extern "C" __global__ void __launch_bounds__(PF_THREADS) pf_norm_kernel(const __
     pf_conv_full_count[0] = pf_conv_full_count[1] = 0u;
   }
 #endif
-  for (int tt = 0; tt < a.n_tasks; ++tt) {
+  // one warp per task (the tasks' partials in parallel: each sum is the
+  // same fixed-shape reduction whichever warp does it)
+  for (int tt = (int)(threadIdx.x >> 5); tt < a.n_tasks; tt += PF_THREADS / 32) {
     const pf_task& U = a.tasks[tt];
     const int nv = U.comp == PF_COMP_ALL4 ? 4 : 1;
-    if (threadIdx.x < 32) {
-      for (int c = 0; c < nv; ++c) {
-        pf_dd s = pf_warp_reduce_runs(part + (pf_u64)c * gridDim.x + U.first_block, U.n_blocks);
-        if (threadIdx.x == 0) sums[tt][c] = __dmul_rn(pf_dd_to_double(s), U.vol);
-      }
+    for (int c = 0; c < nv; ++c) {
+      pf_dd s = pf_warp_reduce_runs(part + (pf_u64)c * gridDim.x + U.first_block, U.n_blocks);
+      if ((threadIdx.x & 31) == 0) sums[tt][c] = __dmul_rn(pf_dd_to_double(s), U.vol);
     }
   }
   __syncthreads();
@@ -1063,6 +1093,10 @@ __device__ void pf_finalize_warp0(const pf_args& a, int lane, const double* S0 =
       long long d[PF_FX_DIGITS];
 #pragma unroll
       for (int i = 0; i < PF_FX_DIGITS; ++i) d[i] = (long long)__ldcg((const unsigned long long*)(bin + i));
+      // the wide-digit count in the same round trip as the bins (it was
+      // loaded after the digit shuffles: one more L2 latency on the tail)
+      long long* bg = a.big + (pf_u64)k * PF_BIG_STRIDE;
+      const long long nbig = (long long)__ldcg((const unsigned long long*)(bg + PF_BIG_COUNT));
       pf_u64 floors = 0, nonfinite = 0, evterr = 0;
       pf_u32 normerr = 0;
       if (lane == 0) {
@@ -1086,8 +1120,6 @@ __device__ void pf_finalize_warp0(const pf_args& a, int lane, const double* S0 =
       }
       // chunk sums beyond the fixed-point range: snapshot the wide digits for
       // the host (which then combines them with d) and reset them
-      long long* bg = a.big + (pf_u64)k * PF_BIG_STRIDE;
-      const long long nbig = (long long)__ldcg((const unsigned long long*)(bg + PF_BIG_COUNT));
       if (nbig) {
         for (int i = lane; i < PF_BIG_DIGITS; i += 32) {
           bg[PF_BIG_SNAP + i] = (long long)__ldcg((const unsigned long long*)(bg + i));

@@ -129,10 +129,14 @@ const Module* load_module(const Layout& L, int device) {
   ck(cudaKernelSetAttributeForDevice(m->event, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(event_smem_max(L)), device),
      "event kernel smem attribute");
-  if (norm_smem(L) > 0)
+  if (norm_smem(L) > 0) {
     ck(cudaKernelSetAttributeForDevice(m->norm, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(norm_smem(L)), device),
        "norm kernel smem attribute");
+    ck(cudaKernelSetAttributeForDevice(m->pre, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(norm_smem(L)), device),
+       "pre kernel smem attribute");
+  }
   {
     cudaFuncAttributes fa{};
     if (cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(m->fused)) == cudaSuccess)
@@ -654,7 +658,7 @@ cudaGraphExec_t Model::graph_for(Shard& sh, int K) {
            L_.setup_cluster);
     ++kernels;
   } else {
-    launch(sh.mod->pre, dim3(K), dim3(256), 0, sh.stream, a);
+    launch(sh.mod->pre, dim3(K), dim3(256), norm_smem(L_), sh.stream, a);
     ++kernels;
     for (size_t lvl = 0; lvl < L_.level_nodes.size(); ++lvl) {
       Args b = a;
@@ -827,7 +831,8 @@ void Model::launch_graphs(const double* params, int K) {
       kp.gridDim = dim3(sh.fused ? fused_grid(sh) : setup ? L_.setup_cluster : 1);
       kp.blockDim = dim3(sh.fused ? 32 * kFusedWarps : setup ? 512 : 256);
       kp.sharedMemBytes = sh.fused ? static_cast<unsigned>(fused_smem(L_))
-                                   : setup ? static_cast<unsigned>(setup_smem_bytes()) : 0u;
+                                   : setup ? static_cast<unsigned>(setup_smem_bytes())
+                                           : static_cast<unsigned>(norm_smem(L_));
       Args inl = sh.first_args;
       inl.npin = L_.np;
       inl.gmask = call_mask_;

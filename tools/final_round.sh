@@ -31,6 +31,10 @@ done
 CMD="python bench.py --config C5 --steps 2 --warmup 3 --no-cpu-baseline --no-fit"
 ncu --set full --clock-control none --import-source on -k regex:"pf_norm" -s 1 -c 1 -o $O/${T}_c5_norm \
   --force-overwrite $CMD > $O/${T}_ncu_c5norm.log 2>&1
+for c in C4 C5; do
+  ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"pf_" --csv --log-file $O/${T}_${c,,}_launches.csv \
+    python bench.py --config $c --steps 2 --warmup 3 --no-cpu-baseline --no-fit > /dev/null 2>&1
+done
 python tools/gen_probe.py 10000000 1000000 > $O/${T}_generate_1e7.json 2> $O/${T}_generate.err
 bash tools/fp64_count.sh $T > $O/${T}_fp64_count.log 2>&1
 PFB200_DEFINES="PF_EVENT_TRACE" python tools/trace_fused.py C2 > $O/${T}_trace_c2.txt 2>&1
