@@ -332,48 +332,24 @@ extern "C" __global__ void __launch_bounds__(PF_SETUP_THREADS) pf_setup_kernel(c
 // ---------------------------------------------------------------------------
 // pre (large grids): parameters, call records and the pre stage.
 #if defined(PF_S_SMEM) && PF_SS * 8 <= 96 * 1024 && PF_SS % 2 == 0 && !defined(PF_QFAST)
-#define PF_S_STAGE_TMA 1  // pre and norm kernels work on a shared-memory copy of S (engine.cpp norm_smem)
+#define PF_S_STAGE_TMA 1  // the norm kernel works on a shared-memory copy of S (engine.cpp norm_smem)
 #endif
 
 extern "C" __global__ void __launch_bounds__(PF_THREADS) pf_pre_kernel(const __grid_constant__ pf_args a) {
+  // (a shared-memory copy of S staged by TMA and written back measured slower
+  // for C4's tables: 8.3 vs 7.1 us)
+  pf_math_init();
   const int k = blockIdx.x;
   pf_krec* r = a.rec + k;
-#ifdef PF_S_STAGE_TMA
-  // convolution tables: the pre stage fills them in a shared-memory copy of
-  // the per-call state (its reads, table writes and max/min atomics on LDS /
-  // STS / shared atomics instead of global round trips), written back whole
-  extern __shared__ __align__(16) double pf_pre_S[];
-  __shared__ __align__(8) pf_u64 pbar;
-  double* gS = a.S + (pf_u64)k * PF_SS;
-  if (threadIdx.x == 0) {
-    pf_mbar_init(&pbar, 1);
-    pf_fence_mbar_init();
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    pf_mbar_expect_tx(&pbar, (unsigned)(PF_SS * 8 + 2048));
-    pf_tma_load(pf_pre_S, gS, (unsigned)(PF_SS * 8), &pbar);
-    pf_tma_load(pf_exp_tab, pf_exp_tab_g, 2048u, &pbar);
-  }
   pf_load_params(a, k);
   if (threadIdx.x == 0) pf_rec_init(r);
   __syncthreads();
-  pf_mbar_wait(&pbar, 0u);
-  double* S = pf_pre_S;
-#else
-  pf_math_init();
-  pf_load_params(a, k);
-  if (threadIdx.x == 0) pf_rec_init(r);
-  __syncthreads();
-  double* S = a.S + (pf_u64)k * PF_SS;
-#endif
   pf_ctx cx;
   cx.err = 0;
   pf_cnt cnt;
   pf_cnt_init(cnt);
-  pf_stage_pre(k, a.P + (pf_u64)k * PF_NP, S, a.C, cx, cnt, threadIdx.x, blockDim.x);
-#ifdef PF_S_STAGE_TMA
-  __syncthreads();  // (pf_stage_pre ends with one too)
-  for (int i = threadIdx.x; i < PF_SS; i += PF_THREADS) gS[i] = S[i];
-#endif
+  pf_stage_pre(k, a.P + (pf_u64)k * PF_NP, a.S + (pf_u64)k * PF_SS, a.C, cx, cnt, threadIdx.x,
+               blockDim.x);
   if (cx.err) atomicMin(&r->norm_error, cx.err);
   if (pf_grid_counts(a, k)) pf_cnt_flush(cnt, a.clamp);
 }
@@ -382,8 +358,13 @@ extern "C" __global__ void __launch_bounds__(PF_THREADS) pf_pre_kernel(const __g
 // norm (large grids): one level, many blocks per midpoint sum; the last
 // block to arrive combines the block partials, applies Richardson and runs
 // the post stage.
-#define PF_NORM_RUN 32  // grid points per thread and run (>= 2-D boxes; engine.cpp build_tasks)
-extern "C" __global__ void __launch_bounds__(PF_THREADS) pf_norm_kernel(const __grid_constant__ pf_args a) {
+#ifndef PF_NORM_RUN
+#define PF_NORM_RUN 32  // grid points per thread and run (>= 2-D boxes; engine.cpp build_tasks, kNormRun)
+#endif
+#ifndef PF_NORM_MIN_BLOCKS
+#define PF_NORM_MIN_BLOCKS 2  // resident norm blocks per SM: <= 128 registers (C5 TDDP grid: 164 regs, 1 block/SM, 147 us -> 2 blocks, 122 us despite spills)
+#endif
+extern "C" __global__ void __launch_bounds__(PF_THREADS, PF_NORM_MIN_BLOCKS) pf_norm_kernel(const __grid_constant__ pf_args a) {
   __shared__ pf_dd sm[PF_THREADS];
   __shared__ int s_last;
   __shared__ double sums[64][4];

@@ -81,6 +81,13 @@ size_t fused_smem(const Layout& L) {
          sizeof(double) * (std::max(L.np, 1) + std::max(L.ss, 1));
 }
 
+// grid points per thread and run of the normalisation kernel (PF_NORM_RUN;
+// env PFB200_NORM_RUN with PFB200_DEFINES=PF_NORM_RUN=n: A/B hook)
+uint64_t norm_run() {
+  if (const char* env = std::getenv("PFB200_NORM_RUN")) return std::max<uint64_t>(1, std::strtoull(env, nullptr, 10));
+  return 32;
+}
+
 // the normalisation kernel's copy of the per-call state (convolution models,
 // pf_norm_kernel under PF_S_SMEM)
 size_t norm_smem(const Layout& L) {
@@ -133,9 +140,6 @@ const Module* load_module(const Layout& L, int device) {
     ck(cudaKernelSetAttributeForDevice(m->norm, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(norm_smem(L)), device),
        "norm kernel smem attribute");
-    ck(cudaKernelSetAttributeForDevice(m->pre, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(norm_smem(L)), device),
-       "pre kernel smem attribute");
   }
   {
     cudaFuncAttributes fa{};
@@ -489,7 +493,7 @@ void Model::build_tasks(uint32_t grid_points) {
         // boxes of >= 2 dimensions: runs of 32 points per thread
         // (PF_NORM_RUN, walked row by row) for all 256 threads of a block
         uint64_t per = static_cast<uint64_t>(std::max(1.0, std::floor(4096.0 / cost)));
-        if (dims >= 2 && !pairs) per = std::max<uint64_t>(per, 256ull * 32ull);
+        if (dims >= 2 && !pairs) per = std::max<uint64_t>(per, 256ull * norm_run());
         // a windowed convolution point is one thread's loop (a few hundred
         // dependent steps): one warp's worth of points per block spreads the
         // grid over many SMs (C4: 12 blocks of 256 points took 25 us)
@@ -558,7 +562,7 @@ void Model::add_tddp_tasks(int node, uint32_t grid_points, int lvl, int* blocks)
       t.vol = vol;
       t.points = total;
       uint64_t per = static_cast<uint64_t>(std::max(1.0, std::floor(4096.0 / (time ? 8.0 : cost))));
-      if (!time) per = std::max<uint64_t>(per, 256ull * 32ull);  // runs of 32 points per thread (pf_norm_run4)
+      if (!time) per = std::max<uint64_t>(per, 256ull * norm_run());  // runs of PF_NORM_RUN points per thread (pf_norm_run4)
       uint64_t nb = (total + per - 1) / per;
       if (nb > 4096) {
         nb = 4096;
@@ -658,7 +662,7 @@ cudaGraphExec_t Model::graph_for(Shard& sh, int K) {
            L_.setup_cluster);
     ++kernels;
   } else {
-    launch(sh.mod->pre, dim3(K), dim3(256), norm_smem(L_), sh.stream, a);
+    launch(sh.mod->pre, dim3(K), dim3(256), 0, sh.stream, a);
     ++kernels;
     for (size_t lvl = 0; lvl < L_.level_nodes.size(); ++lvl) {
       Args b = a;
@@ -831,8 +835,7 @@ void Model::launch_graphs(const double* params, int K) {
       kp.gridDim = dim3(sh.fused ? fused_grid(sh) : setup ? L_.setup_cluster : 1);
       kp.blockDim = dim3(sh.fused ? 32 * kFusedWarps : setup ? 512 : 256);
       kp.sharedMemBytes = sh.fused ? static_cast<unsigned>(fused_smem(L_))
-                                   : setup ? static_cast<unsigned>(setup_smem_bytes())
-                                           : static_cast<unsigned>(norm_smem(L_));
+                                   : setup ? static_cast<unsigned>(setup_smem_bytes()) : 0u;
       Args inl = sh.first_args;
       inl.npin = L_.np;
       inl.gmask = call_mask_;
