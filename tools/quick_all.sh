@@ -10,7 +10,7 @@ for l in sys.stdin:
     elif 'Error' in l or 'error' in l: print(l)
 "
 done
-for c in C4; do
+for c in C4 C5; do
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"pf_" --csv --log-file gpurun_out/q_$c.csv python bench.py --config $c --steps 2 --warmup 3 --no-cpu-baseline --no-fit > /dev/null 2>&1
 python - $c <<'PY'
 import csv,sys
