@@ -3,6 +3,9 @@
 // objective behind it runs on the GPU.
 #include "fit.hpp"
 
+#include <cstdio>
+#include <cstdlib>
+
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -418,9 +421,24 @@ struct Internal : Objective {
     for (size_t k = 0; k < u.size(); ++k) p[free_idx[k]] = tr.to_external(free_idx[k], u[k]);
     return p;
   }
+  // diagnostics: PFB200_FIT_TRACE=<file> appends every evaluated point
+  // (external parameters) and its metric, %.17g, one line per call
+  static void trace(const std::vector<double>& p, double v) {
+    static const char* path = std::getenv("PFB200_FIT_TRACE");
+    if (!path) return;
+    if (FILE* fh = std::fopen(path, "a")) {
+      std::fprintf(fh, "%.17g", v);
+      for (double x : p) std::fprintf(fh, " %.17g", x);
+      std::fprintf(fh, "\n");
+      std::fclose(fh);
+    }
+  }
   double f(const std::vector<double>& u) override {
     ++calls;
-    return metric(expand(u));
+    const std::vector<double> p = expand(u);
+    const double v = metric(p);
+    trace(p, v);
+    return v;
   }
   void batch(const std::vector<std::vector<double>>& us, std::vector<double>& out) override {
     if (!mbatch) {
@@ -432,6 +450,7 @@ struct Internal : Objective {
     for (const auto& u : us) ps.push_back(expand(u));
     calls += us.size();
     mbatch(ps, out);
+    for (size_t i = 0; i < ps.size() && i < out.size(); ++i) trace(ps[i], out[i]);
   }
 };
 
