@@ -50,6 +50,9 @@ struct Layout {
   // the root is such a convolution: the event pass gives each warp a
   // shared-memory scratch of 2 x kConvKB products (PF_CONV_SHARED)
   bool conv_shared = false;
+  // TddpPdf grids: doubles per column of the norm kernel's column table
+  // (qt and the channel-A lineshapes, PF_TDDP_TAB_ARRAYS); 0: none
+  int tddp_tab_arrays = 0;
   std::vector<std::vector<int>> level_nodes;  // normalised nodes per level
   std::string source;         // generated CUDA source (without library headers)
   std::string structure_key;  // cache key of the compiled module

@@ -117,7 +117,7 @@ struct pf_args {
   int n_nodes;
   int fuse_final;       // K == 1: the last event block runs the final tree
   int n_levels;
-  int pad0;
+  int tddp_tab;         // norm kernel: a TddpPdf column table in dynamic shared memory (pf_tddp_cols)
   const double* data;   // column-major shard: data[col * col_stride + e]
   pf_u64 col_stride;
   pf_u64 n_local;       // events (bins) in this shard

@@ -422,10 +422,18 @@ extern "C" __global__ void __launch_bounds__(PF_THREADS, PF_NORM_MIN_BLOCKS) pf_
 #endif
   if (multi) {
     // all four components from ONE evaluation of both amplitudes per point,
-    // in runs of PF_NORM_RUN consecutive points walked row by row
+    // in runs of PF_NORM_RUN consecutive points walked row by row; channel A
+    // (s13) from the block's column table when the engine gave it room
+    const double* tab = nullptr;
+    if (a.tddp_tab) {
+      extern __shared__ __align__(16) double pf_norm_tab[];
+      pf_tddp_cols(T.node, T, P, Sp, a.C, pf_norm_tab, threadIdx.x, PF_THREADS);
+      __syncthreads();
+      tab = pf_norm_tab;
+    }
     for (pf_u64 i = lo + (pf_u64)threadIdx.x * PF_NORM_RUN; i < hi; i += (pf_u64)PF_THREADS * PF_NORM_RUN) {
       double v4[4];
-      pf_norm_run4(T.node, i, (int)min((pf_u64)PF_NORM_RUN, hi - i), T, P, Sp, a.C, v4);
+      pf_norm_run4(T.node, i, (int)min((pf_u64)PF_NORM_RUN, hi - i), T, P, Sp, a.C, v4, tab);
 #pragma unroll
       for (int c = 0; c < 4; ++c) acc[c] = pf_dd_add_d(acc[c], v4[c]);
     }

@@ -342,6 +342,10 @@ Model::Model(const pf_graph& g, const pf_data& d, uint32_t grid_points, const pf
     ck(cudaSetDevice(sh.device), "cudaSetDevice");
     ck(cudaStreamCreateWithFlags(&sh.stream, cudaStreamNonBlocking), "cudaStreamCreate");
     sh.mod = load_module(L_, sh.device);
+    if (tddp_tab_bytes_ > 0)
+      ck(cudaKernelSetAttributeForDevice(sh.mod->norm, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(std::max(tddp_tab_bytes_, norm_smem(L_))), sh.device),
+         "norm kernel smem attribute (TddpPdf column table)");
     const size_t np = std::max(L_.np, 1);
     ck(cudaMalloc(&sh.d_P, sizeof(double) * kMaxBatch * np), "cudaMalloc P");
     ck(cudaMalloc(&sh.d_S, sizeof(double) * kMaxBatch * std::max(L_.ss, 1)), "cudaMalloc S");
@@ -521,6 +525,15 @@ void Model::build_tasks(uint32_t grid_points) {
     level_blocks_[lvl] = blocks;
     max_norm_blocks_ = std::max(max_norm_blocks_, blocks);
   }
+  // TddpPdf Dalitz tasks: a column table per norm block when it fits beside
+  // two resident blocks per SM (pf_tddp_cols; env PFB200_NOTDDPTAB: A/B hook)
+  if (L_.tddp_tab_arrays > 0 && !std::getenv("PFB200_NOTDDPTAB")) {
+    uint64_t n = 0;
+    for (const Task& t : tasks_)
+      if (t.comp == kCompAll4) n = std::max<uint64_t>(n, static_cast<uint64_t>(t.n));
+    const size_t bytes = static_cast<size_t>(L_.tddp_tab_arrays) * (n + n / 32) * sizeof(double);
+    if (n > 0 && bytes <= 100 * 1024) tddp_tab_bytes_ = bytes;
+  }
 }
 
 // TddpPdf: its 3-D midpoint sums (pdf.hpp:148-176 over (s12, s13, t)) are
@@ -669,7 +682,9 @@ cudaGraphExec_t Model::graph_for(Shard& sh, int K) {
       b.level = static_cast<int>(lvl);
       b.n_tasks = level_n_tasks_[lvl];
       b.tasks = sh.d_tasks + level_first_task_[lvl];
-      launch(sh.mod->norm, dim3(level_blocks_[lvl], K), dim3(256), norm_smem(L_), sh.stream, b);
+      b.tddp_tab = tddp_tab_bytes_ > 0 ? 1 : 0;
+      launch(sh.mod->norm, dim3(level_blocks_[lvl], K), dim3(256), std::max(norm_smem(L_), tddp_tab_bytes_),
+             sh.stream, b);
       ++kernels;
     }
   }

@@ -75,7 +75,7 @@ struct Args {
   int n_nodes;
   int fuse_final;
   int n_levels;
-  int pad0;
+  int tddp_tab;  // norm kernel: TddpPdf column table in dynamic shared memory
   const double* data;
   uint64_t col_stride;
   uint64_t n_local;
@@ -255,6 +255,7 @@ class Model {
   std::vector<Task> tasks_;  // host copy, all levels
   std::vector<int> level_first_task_, level_n_tasks_, level_blocks_;
   int max_norm_blocks_ = 0;
+  size_t tddp_tab_bytes_ = 0;  // norm kernel: TddpPdf column table (dynamic shared memory), 0: none
   double* h_params_ = nullptr;  // mapped, kMaxBatch x np
   uint32_t* h_mask_ = nullptr;  // mapped: grid-clamp counting mask of the call (pf_grid_counts)
   uint32_t call_mask_ = 0;      // the mask of the call in flight
