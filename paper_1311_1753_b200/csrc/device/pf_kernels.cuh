@@ -439,8 +439,17 @@ extern "C" __global__ void __launch_bounds__(PF_THREADS, PF_NORM_MIN_BLOCKS) pf_
     }
   } else if (T.dims >= 2 && T.per_block >= (pf_u64)PF_THREADS * PF_NORM_RUN) {
     // runs of PF_NORM_RUN consecutive points per thread, walked row by row
+    // (a DalitzPlotPdf's channel 13 from the block's column table)
+    const double* tab = nullptr;
+    if (a.tddp_tab) {
+      extern __shared__ __align__(16) double pf_norm_tab[];
+      pf_dalitz_cols(T.node, T, P, Sp, a.C, pf_norm_tab, threadIdx.x, PF_THREADS);
+      __syncthreads();
+      tab = pf_norm_tab;
+    }
     for (pf_u64 i = lo + (pf_u64)threadIdx.x * PF_NORM_RUN; i < hi; i += (pf_u64)PF_THREADS * PF_NORM_RUN)
-      acc[0] = pf_dd_add_d(acc[0], pf_norm_run(T.node, i, (int)min((pf_u64)PF_NORM_RUN, hi - i), T, P, Sp, a.C, cx, cnt));
+      acc[0] = pf_dd_add_d(acc[0], pf_norm_run(T.node, i, (int)min((pf_u64)PF_NORM_RUN, hi - i), T, P, Sp, a.C, cx, cnt,
+                                               tab));
   } else {
 #ifdef PF_NORM_POINT_TRACE
     const long long c0 = clock64();

@@ -530,7 +530,8 @@ void Model::build_tasks(uint32_t grid_points) {
   if (L_.tddp_tab_arrays > 0 && !std::getenv("PFB200_NOTDDPTAB")) {
     uint64_t n = 0;
     for (const Task& t : tasks_)
-      if (t.comp == kCompAll4) n = std::max<uint64_t>(n, static_cast<uint64_t>(t.n));
+      if (t.comp == kCompAll4 || (t.dims == 2 && pg_.nodes[t.node].kind == PF_DALITZ))
+        n = std::max<uint64_t>(n, static_cast<uint64_t>(t.n));
     const size_t bytes = static_cast<size_t>(L_.tddp_tab_arrays) * (n + n / 32) * sizeof(double);
     if (n > 0 && bytes <= 100 * 1024) tddp_tab_bytes_ = bytes;
   }
