@@ -595,3 +595,29 @@ def test_small_grid_workloads_take_the_single_kernel_path(name):
     bm = pf.BoundModel(pdf, W.data(pf, obs, 50_000, seed=2), pf.GridSpec(W.grid))
     bm.eval_metric(W.params(bm))
     assert pf.lib.pf_model_fused(bm._h) == 1
+
+
+@pytest.mark.parametrize("name", ["C5", "C5TI"])
+def test_dalitz_grid_column_tables_match_the_per_point_path(name, monkeypatch):
+    """The Dalitz / TDDP normalisation grids take channel A (s13) from a
+    per-block column table (pf_tddp_cols / pf_dalitz_cols); with the table
+    off (PFB200_NOTDDPTAB) every point evaluates it.  Both agree to rounding
+    and with the oracle, for one parameter set and a batch."""
+    W = WORKLOADS[name]
+    obs, pdf = W.build(pf)
+    ds = pf.UnbinnedDataSet.from_columns(obs, W.columns(20011, seed=6))
+    grid = 128
+    on = pf.BoundModel(pdf, ds, pf.GridSpec(grid))
+    monkeypatch.setenv("PFB200_NOTDDPTAB", "1")
+    off = pf.BoundModel(pdf, ds, pf.GridSpec(grid))
+    monkeypatch.delenv("PFB200_NOTDDPTAB")
+    o = oracle.Oracle(pdf, ds, grid)
+    names = [v.name for v in on.registry().parameters()]
+    p = [W.truth[n] for n in names]
+    q = list(p)
+    q[names.index("rhop_re" if "rhop_re" in names else names[2])] *= 0.9
+    for x in (p, q):
+        a, b, want = on.eval_metric(x), off.eval_metric(x), o.eval(x)
+        assert abs(a - b) <= 1e-14 * abs(b), (a, b)
+        assert close(a, want), (a, want)
+    assert np.array_equal(on.eval_metric_batch(np.array([p, q])), [on.eval_metric(p), on.eval_metric(q)])
