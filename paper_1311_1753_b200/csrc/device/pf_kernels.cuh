@@ -1125,6 +1125,9 @@ __device__ void pf_finalize_warp0(const pf_args& a, int lane, const double* S0 =
         }
       }
       int gbig = nbig != 0;
+#ifdef PF_EVENT_TRACE
+      if (lane == 0 && k == 0) pf_trace_buf[4095 * 6 + 1] = pf_gtime();  // digits summed
+#endif
       if (a.peers) pf_group_exchange(a, k, lane, d, normerr, nonfinite, evterr, gbig);
       if (lane == 0) {
         bg[PF_BIG_COUNT] = 0ll;
@@ -1149,6 +1152,9 @@ __device__ void pf_finalize_warp0(const pf_args& a, int lane, const double* S0 =
         a.done[1 + k] = seq;
         o.pad = seq;
         o.check = pf_out_check(o);
+#ifdef PF_EVENT_TRACE
+        if (k == 0) pf_trace_buf[4095 * 6 + 2] = pf_gtime();  // record built (rounded)
+#endif
         volatile pf_out* dst = a.hout + k;
         dst->result = o.result;
         dst->floor_count = o.floor_count;
@@ -1162,6 +1168,9 @@ __device__ void pf_finalize_warp0(const pf_args& a, int lane, const double* S0 =
         // reaches the host first, and the host sees the record right away
         // rather than when the grid drains (measured: e2e 58 -> 48 us, C2)
         asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(&a.hout[k].pad), "r"(o.pad) : "memory");
+#ifdef PF_EVENT_TRACE
+        if (k == 0) pf_trace_buf[4095 * 6 + 3] = pf_gtime();  // published
+#endif
       }
       // the norms the reference's nodes now cache: device memory, read by
       // the host only when asked (pf_node_norms); a call whose normalisation

@@ -29,6 +29,9 @@ for name, col in zip(["enter", "setup done", "loop done", "block done"], range(4
     v = rel[:, col]
     print("%-11s min %7.2f  median %7.2f  max %7.2f us" % (name, v.min(), np.median(v), v.max()))
 print("finalize: starts %.2f, ends %.2f us" % ((t[4094, 0] - t0) / 1000, (t[4094, 2] - t0) / 1000))
+if t[4095, 1] > 0:
+    print("  finalize steps: digits summed %.2f, record built %.2f, published %.2f us"
+          % tuple((t[4095, c] - t0) / 1000 for c in (1, 2, 3)))
 print("CTAs traced:", len(blk))
 wb = (C.c_uint64 * (4096 * 2))()
 pf.lib.pf_debug_trace(bm._h, wb, -4096 * 2)
