@@ -87,11 +87,11 @@ struct pf_out {
   pf_u64 check;     // pf_out_check of every field above: the record is complete
 };
 
-// The record is published with plain stores (no system-scope fence, which
-// costs microseconds at the end of every call): the host accepts it once
-// `pad` carries the call's sequence number AND `check` matches every field,
-// so a record read while its stores are still landing is retried (host twin:
-// engine.cpp out_check).
+// The record is published with uncached system-scope stores and no
+// system-scope fence (which costs ~1.5 us at the end of every call,
+// pf_finalize_warp0): the host accepts it once `pad` carries the call's
+// sequence number AND `check` matches every field, so a record read while
+// its stores are still landing is retried (host twin: engine.cpp out_check).
 __device__ __forceinline__ pf_u64 pf_mix64(pf_u64 h, pf_u64 v) {
   h ^= v + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
   h ^= h >> 31;

@@ -1155,6 +1155,29 @@ __device__ void pf_finalize_warp0(const pf_args& a, int lane, const double* S0 =
 #ifdef PF_EVENT_TRACE
         if (k == 0) pf_trace_buf[4095 * 6 + 2] = pf_gtime();  // record built (rounded)
 #endif
+#ifndef PF_PUBLISH_RELEASE
+        // every field by an uncached system-scope store (STG.MMIO.SYS: not
+        // held in L2 until the grid drains) and no release fence: the host
+        // accepts the record once `pad` is this call's sequence number and
+        // `check` matches every field, whatever order the stores land in.
+        // Measured (C2, profiles/r2e_publish_ab.txt): device step 40.2 ->
+        // 38.8 us, end to end unchanged or better; PF_PUBLISH_RELEASE keeps
+        // the volatile stores + st.release.sys of the sequence word
+        {
+          pf_out* h = a.hout + k;
+          auto st = [](void* p, pf_u64 v) {
+            asm volatile("st.mmio.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+          };
+          st(&h->result, (pf_u64)__double_as_longlong(o.result));
+          st(&h->floor_count, o.floor_count);
+          st(&h->first_nonfinite, o.first_nonfinite);
+          st(&h->first_event_error, o.first_event_error);
+#pragma unroll
+          for (int i = 0; i < PF_FX_DIGITS; ++i) st(&h->fx[i], (pf_u64)o.fx[i]);
+          st(&h->check, o.check);
+          st(&h->norm_error, (pf_u64)o.norm_error | ((pf_u64)o.pad << 32));
+        }
+#else
         volatile pf_out* dst = a.hout + k;
         dst->result = o.result;
         dst->floor_count = o.floor_count;
@@ -1168,6 +1191,7 @@ __device__ void pf_finalize_warp0(const pf_args& a, int lane, const double* S0 =
         // reaches the host first, and the host sees the record right away
         // rather than when the grid drains (measured: e2e 58 -> 48 us, C2)
         asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(&a.hout[k].pad), "r"(o.pad) : "memory");
+#endif
 #ifdef PF_EVENT_TRACE
         if (k == 0) pf_trace_buf[4095 * 6 + 3] = pf_gtime();  // published
 #endif
