@@ -116,7 +116,7 @@ def peaks():
         return 6650.0, "fallback"
 
 
-NCU_TAGS = ("r2e", "r2d", "r2c", "r2", "r1n", "r1m", "r1l", "r1j", "r1i", "r1h", "r1g", "r1f", "r1e")  # newest first
+NCU_TAGS = ("r2f", "r2e", "r2d", "r2c", "r2", "r1n", "r1m", "r1l", "r1j", "r1i", "r1h", "r1g", "r1f", "r1e")  # newest first
 FP64_BOUND = ("C4", "C5", "C5TI")  # FP64-pipe-bound configs (ncu: FP64 pipe 42-61 %, HBM < 11 %)
 
 
