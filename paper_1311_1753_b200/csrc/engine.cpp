@@ -140,6 +140,7 @@ const Module* load_module(const Layout& L, int device) {
     ck(cudaKernelSetAttributeForDevice(m->norm, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(norm_smem(L)), device),
        "norm kernel smem attribute");
+    m->norm_dyn_max = norm_smem(L);
   }
   {
     cudaFuncAttributes fa{};
@@ -342,10 +343,18 @@ Model::Model(const pf_graph& g, const pf_data& d, uint32_t grid_points, const pf
     ck(cudaSetDevice(sh.device), "cudaSetDevice");
     ck(cudaStreamCreateWithFlags(&sh.stream, cudaStreamNonBlocking), "cudaStreamCreate");
     sh.mod = load_module(L_, sh.device);
-    if (tddp_tab_bytes_ > 0)
-      ck(cudaKernelSetAttributeForDevice(sh.mod->norm, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(std::max(tddp_tab_bytes_, norm_smem(L_))), sh.device),
-         "norm kernel smem attribute (TddpPdf column table)");
+    if (tddp_tab_bytes_ > 0) {
+      // the module (and its kernel attribute) is shared by every model of the
+      // same structure: raise the limit, never lower it under another model
+      std::lock_guard<std::mutex> lock(cache().mu);
+      const size_t need = std::max(tddp_tab_bytes_, norm_smem(L_));
+      if (need > sh.mod->norm_dyn_max) {
+        ck(cudaKernelSetAttributeForDevice(sh.mod->norm, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(need), sh.device),
+           "norm kernel smem attribute (TddpPdf column table)");
+        sh.mod->norm_dyn_max = need;
+      }
+    }
     const size_t np = std::max(L_.np, 1);
     ck(cudaMalloc(&sh.d_P, sizeof(double) * kMaxBatch * np), "cudaMalloc P");
     ck(cudaMalloc(&sh.d_S, sizeof(double) * kMaxBatch * std::max(L_.ss, 1)), "cudaMalloc S");

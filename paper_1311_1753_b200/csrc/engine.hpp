@@ -115,6 +115,9 @@ struct Module {
   cudaKernel_t setup = nullptr, pre = nullptr, norm = nullptr, event = nullptr, final = nullptr,
                publish = nullptr, fused = nullptr;
   size_t fused_static_smem = 0;  // static shared memory of pf_fused_kernel
+  // largest dynamic shared memory any model sharing this module asked of
+  // pf_norm_kernel (TddpPdf column tables depend on the grid): only raised
+  mutable size_t norm_dyn_max = 0;
   cudaKernel_t flush_read = nullptr;  // bench: read half of the L2 flush
   // generator modules only (PF_GEN, pf_generate.cuh)
   cudaKernel_t gen_max = nullptr, gen_mt = nullptr, gen_mt_jump = nullptr, gen_eval = nullptr,

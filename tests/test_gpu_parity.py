@@ -621,3 +621,20 @@ def test_dalitz_grid_column_tables_match_the_per_point_path(name, monkeypatch):
         assert abs(a - b) <= 1e-14 * abs(b), (a, b)
         assert close(a, want), (a, want)
     assert np.array_equal(on.eval_metric_batch(np.array([p, q])), [on.eval_metric(p), on.eval_metric(q)])
+
+
+def test_tddp_models_of_different_grids_share_a_module():
+    """Two TddpPdf models of one structure share the compiled module and its
+    norm-kernel shared-memory limit; the larger grid's column table must not
+    break the smaller one's launches, whichever is created first"""
+    W = WORKLOADS["C5"]
+    obs, pdf = W.build(pf)
+    ds = pf.UnbinnedDataSet.from_columns(obs, W.columns(5003, seed=8))
+    big = pf.BoundModel(pdf, ds, pf.GridSpec(256))
+    small = pf.BoundModel(pdf, ds, pf.GridSpec(64))
+    p = big.registry().export_values()
+    a, b = big.eval_metric(p), small.eval_metric(p)
+    assert np.isfinite(a) and np.isfinite(b)
+    assert big.eval_metric(p) == a and small.eval_metric(p) == b
+    o = oracle.Oracle(pdf, ds, 256)
+    assert close(a, o.eval(p))
