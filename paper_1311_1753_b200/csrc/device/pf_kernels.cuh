@@ -1595,8 +1595,16 @@ extern "C" __global__ void __launch_bounds__(PF_FUSED_THREADS, 1) pf_fused_kerne
   }
   __syncthreads();
   if (threadIdx.x == 0) {
+#ifdef PF_DONE_ACQREL
+    // experiment: one acq_rel atomic instead of fence + atomic (the block's
+    // digit atomics happen-before it through the barrier above)
+    unsigned prev;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(a.done) : "memory");
+    s_last = prev == gridDim.x - 1;
+#else
     __threadfence();
     s_last = atomicAdd(a.done, 1u) == gridDim.x - 1;
+#endif
   }
   __syncthreads();
   if (PF_SETUP_CLUSTER > 1) asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
